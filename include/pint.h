@@ -1,0 +1,156 @@
+/*
+ * pint.h — C ABI of the B200-native ParaDiag waveform-relaxation hot path of
+ * arXiv 2007.13125 (Wu & Zhou): parallel-in-time BDFk (k = 1..6) for u_t + A u = f and
+ * CQ-BDFk for the Caputo subdiffusion problem d_t^alpha u + A u = f, A = -Delta_h (FD,
+ * homogeneous Dirichlet, unit interval / unit square, h = 1/(m+1)).
+ *
+ * One waveform-relaxation (WR) iteration U_{m-1} -> U_m solves the kappa-periodic
+ * all-at-once system   (1/tau^a)(B_k(kappa) (x) I) U_m + (I (x) A) U_m = F_{m-1}
+ * (PAPER.md:403-430 eq:BDF-k-matrix; PAPER.md:1021-1038 eq:BDF-k-matrix-frac) by
+ * Algorithm 1/2:
+ *   F_{m-1}  = f̄ + tau^-a (sum_{j<n} w_j) v + kappa-wrap(U_{m-1})   (eqn:BDF-k-F, eq:BDF-subdiff-F)
+ *   Step 1   H = V^{-1} Gamma_kappa F         (scale by kappa^{(n-1)/N}, batched time FFT / N)
+ *   Step 2   (d_p/tau^a + A) Q_p = H_p, p = 0..N-1   (complex-shifted spatial solves)
+ *   Step 3   U_m = Gamma_kappa^{-1} V Q        (inverse time FFT, unscale)
+ * Data layout, kernels and readings of the paper: DESIGN.md.
+ *
+ * Conventions
+ *   - All entry points return pint_status; no exception or abort crosses the ABI.  On error
+ *     pint_last_error() (thread-local) holds a one-line message naming the bound violated.
+ *   - Complex data are complex128: interleaved (re, im) doubles, 16 bytes per value.
+ *   - Space index i = iy*mx + ix (x fastest); space-time arrays are time-major [n][i],
+ *     n = 1..N stored at rows 0..N-1 (U^n = approximation at t_n = n*tau).
+ *   - mem = PINT_HOST: the pointer is host memory (pageable or pinned); PINT_DEVICE: device
+ *     memory on the plan's device.  Inputs are copied during the call (the caller may free
+ *     them on return); outputs are written into caller buffers before the call returns.
+ *   - A plan is bound to one device and one CUDA stream, is not thread-safe, and owns all
+ *     its device workspace.  Distinct plans are independent.
+ *   - Calls that return host scalars (pint_wr_iterate, pint_wr_solve, getters) synchronise
+ *     the plan stream.
+ *   - Multi-GPU (2D operators only): each rank creates a plan with the GLOBAL sizes and its
+ *     rank/nranks; the plan owns the contiguous x-mode slab [q_begin, q_end) of the hoisted
+ *     DST-I basis (pint_get_partition).  The WR iteration needs no data exchange between
+ *     slabs (the x-modes decouple exactly); the only collective is the all-reduce(max) of
+ *     the update norm, done through the caller-supplied allreduce_max callback.
+ */
+#ifndef PINT_H_
+#define PINT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pint_plan_s* pint_plan;
+
+typedef enum {
+  PINT_OK = 0,
+  PINT_ERR_ARG = 1,            /* argument outside its documented range (message names it) */
+  PINT_ERR_ALLOC = 2,          /* device/host allocation failed */
+  PINT_ERR_CUDA = 3,           /* CUDA runtime error (message holds cudaGetErrorString) */
+  PINT_ERR_COMM = 4,           /* allreduce_max callback returned non-zero */
+  PINT_ERR_STATE = 5,          /* call out of order (e.g. iterate before set_problem) */
+  PINT_ERR_NOT_CONVERGED = 6,  /* pint_wr_solve hit max_iters; solution still retrievable */
+  PINT_ERR_DIVERGED = 7,       /* update grew 3 times in a row, or became NaN/Inf */
+  PINT_ERR_UNSUPPORTED = 8     /* valid but not implemented on this path (message says what) */
+} pint_status;
+
+enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2 };
+enum { PINT_HOST = 0, PINT_DEVICE = 1 };
+enum {
+  PINT_FLAG_U0_ZERO = 1        /* WR initial guess U_0 = 0 instead of U_0^n = v */
+};
+
+typedef struct {
+  int32_t kind;                /* PINT_OP_FD1D_DIRICHLET or PINT_OP_FD2D_DIRICHLET */
+  int64_t mx, my;              /* grid points per axis (1D: my = 1); M = mx*my */
+} pint_operator;
+
+/* All-reduce(max) over ranks of one double, in place.  Return 0 on success. */
+typedef int (*pint_allreduce_max_fn)(double* inout, void* ctx);
+
+typedef struct {
+  double alpha;                /* 1.0 = heat (BDFk); (0,1) = Caputo order, CQ-BDFk weights */
+  int32_t device;              /* CUDA device ordinal */
+  void* stream;                /* cudaStream_t to run on; NULL = plan-owned stream */
+  int32_t flags;               /* PINT_FLAG_* */
+  int32_t rank, nranks;        /* x-mode slab partition (2D); 0, 1 for one GPU */
+  pint_allreduce_max_fn allreduce_max;   /* required when nranks > 1 */
+  void* allreduce_ctx;
+} pint_options;
+
+/* Create a plan for N time steps of size tau with BDF order k and relaxation parameter kappa.
+ * M must equal op->mx * op->my.  Errors (PINT_ERR_ARG): k not in 1..6; kappa not in (0,1);
+ * tau <= 0; N < k+1; alpha not in (0,1]; M != mx*my; mx, my < 1; rank/nranks invalid or
+ * nranks > mx; nranks > 1 with a 1D operator.  PINT_ERR_UNSUPPORTED: N not a power of two in
+ * [16, 4096]; line length (1D: mx, 2D: my) > 1024; 2D with 2(mx+1) not a power of two <= 4096.
+ * Validation happens before any CUDA call.  On success *out owns device buffers of about
+ * 2*N*M*16 bytes (this rank's slab) plus O((k+R)*M) vectors and O(N) tables. */
+pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double kappa, double tau,
+                             const pint_operator* op, const pint_options* opt, pint_plan* out);
+
+/* Problem data with separable forcing f(t, x) = sum_{r<R} phi_r(t) g_r(x):
+ *   v    [M] complex: initial value u(0)
+ *   g    [R][M] complex (R may be 0, then g/phi/dphi may be NULL)
+ *   phi  [R][N+1] double: phi_r(t_n), n = 0..N (host memory always)
+ *   dphi [R][max(k-2,0)] double: d^l phi_r / dt^l (0), l = 1..k-2, for the Table-1 starting
+ *        corrections b_{l,n} (host memory always)
+ * v and g are read from mem (PINT_HOST / PINT_DEVICE; full global arrays on every rank).
+ * Builds the static right-hand side coefficients and bootstraps the iteration from U_0
+ * (U_0^n = v, or 0 with PINT_FLAG_U0_ZERO): afterwards the iteration count is m = 0. */
+pint_status pint_set_problem_separable(pint_plan plan, const void* v, int32_t R, const void* g,
+                                       const double* phi, const double* dphi, int32_t mem);
+
+/* Replace the WR initial guess by a full space-time array U0 [N][M] (this is U_0^1..U_0^N;
+ * requires a prior pint_set_problem_separable).  Resets m to 0. */
+pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
+
+/* One WR iteration m-1 -> m.  *update_inf (may be NULL) receives the max over ranks of
+ * max |U_m^n(x) - U_{m-1}^n(x)| over the monitored levels n = N-k+1..N (the wrap state,
+ * which determines the next iterate for heat). */
+pint_status pint_wr_iterate(pint_plan plan, double* update_inf);
+
+/* Iterate until update < tol, or max_iters iterations (PINT_ERR_NOT_CONVERGED), or the update
+ * grows 3 consecutive times / is not finite (PINT_ERR_DIVERGED).  *iters, *update_inf may be NULL. */
+pint_status pint_wr_solve(pint_plan plan, double tol, int32_t max_iters, int32_t* iters,
+                          double* update_inf);
+
+/* Copy the current iterate U_m, time levels n_begin+1 .. n_begin+n_count (0-based row
+ * n_begin .. n_begin+n_count-1 of the [N][M] array), into U [n_count][M] complex in mem.
+ * 2D with nranks > 1: returns PINT_ERR_UNSUPPORTED (use the modal-slab calls below). */
+pint_status pint_get_levels(pint_plan plan, int64_t n_begin, int64_t n_count, void* U, int32_t mem);
+/* = pint_get_levels(plan, 0, N, U, mem) */
+pint_status pint_get_solution(pint_plan plan, void* U, int32_t mem);
+
+/* Multi-GPU output path: this rank's slab of U_m in the DST-x basis, layout
+ * [n_count][my][q_end-q_begin] (mode q global index q_begin+j), and the inverse DST-I that
+ * maps a gathered full modal array [n_count][my][mx] to physical [n_count][my][mx]. */
+pint_status pint_get_modal_levels(pint_plan plan, int64_t n_begin, int64_t n_count, void* Uq, int32_t mem);
+pint_status pint_modal_to_physical(pint_plan plan, int64_t n_count, const void* Uq_full, void* U, int32_t mem);
+
+/* This rank's x-mode slab [q_begin, q_end) (1D: [0, 1)). */
+pint_status pint_get_partition(pint_plan plan, int64_t* q_begin, int64_t* q_end);
+
+/* Per-pass timing with CUDA events on the plan stream (bench/profiling):
+ * enable != 0 starts accumulating; pint_get_timing returns total milliseconds and launch
+ * counts of the T-pass (time-axis kernel) and S-pass (shifted-solve kernel) since enabled. */
+pint_status pint_set_timing(pint_plan plan, int32_t enable);
+pint_status pint_get_timing(pint_plan plan, double* tpass_ms, double* spass_ms,
+                            int64_t* tpass_launches, int64_t* spass_launches);
+
+/* Introspection: iteration count m, total kernel launches issued by this plan, device bytes. */
+pint_status pint_get_info(pint_plan plan, int64_t* m, int64_t* kernel_launches, int64_t* device_bytes);
+
+pint_status pint_plan_destroy(pint_plan plan);
+
+const char* pint_status_string(pint_status s);
+const char* pint_last_error(void);
+
+/* kappa = min(1/ln N, 0.5) (the paper's kappa = O(1/log N) choice for subdiffusion). */
+double pint_kappa_log_rule(int64_t N);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINT_H_ */

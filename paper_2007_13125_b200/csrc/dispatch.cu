@@ -1,0 +1,81 @@
+// dispatch.cu — runtime dispatch over the compiled FFT lengths and S-pass chunk sizes.
+#define PINT_DEFINE_PLAIN_KERNELS
+#include "kernels.h"
+
+namespace pint {
+
+cudaError_t launch_tpass(int N, int mi, int mo, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  switch (N) {
+    case 16: return launch_tpass_16(mi, mo, cq, a, ntiles, st);
+    case 32: return launch_tpass_32(mi, mo, cq, a, ntiles, st);
+    case 64: return launch_tpass_64(mi, mo, cq, a, ntiles, st);
+    case 128: return launch_tpass_128(mi, mo, cq, a, ntiles, st);
+    case 256: return launch_tpass_256(mi, mo, cq, a, ntiles, st);
+    case 512: return launch_tpass_512(mi, mo, cq, a, ntiles, st);
+    case 1024: return launch_tpass_1024(mi, mo, cq, a, ntiles, st);
+    case 2048: return launch_tpass_2048(mi, mo, cq, a, ntiles, st);
+    case 4096: return launch_tpass_4096(mi, mo, cq, a, ntiles, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st) {
+  switch (NE) {
+    case 16: return launch_dst_16(a, mode, st);
+    case 32: return launch_dst_32(a, mode, st);
+    case 64: return launch_dst_64(a, mode, st);
+    case 128: return launch_dst_128(a, mode, st);
+    case 256: return launch_dst_256(a, mode, st);
+    case 512: return launch_dst_512(a, mode, st);
+    case 1024: return launch_dst_1024(a, mode, st);
+    case 2048: return launch_dst_2048(a, mode, st);
+    case 4096: return launch_dst_4096(a, mode, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+constexpr int SG = 4;   // lines (warps) per S-pass CTA
+
+template <int C>
+static cudaError_t spass_go(const SPassArgs& a, long Qb, cudaStream_t st) {
+  auto kern = spass_kernel<C, SG>;
+  const int off = (a.WB >= 8) ? 0 : (a.WB > 8 / SG ? a.WB : 8 / SG);
+  const int smem = SG * (32 * (C + 1) + off) * (int)sizeof(double2);
+  static int attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  dim3 grid((unsigned)(a.N / SG), (unsigned)Qb);
+  kern<<<grid, 32 * SG, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
+  switch (C) {
+    case 1: return spass_go<1>(a, Qb, st);
+    case 2: return spass_go<2>(a, Qb, st);
+    case 4: return spass_go<4>(a, Qb, st);
+    case 8: return spass_go<8>(a, Qb, st);
+    case 16: return spass_go<16>(a, Qb, st);
+    case 32: return spass_go<32>(a, Qb, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st) {
+  if (a.count <= 0) return cudaSuccess;
+  const long blocks = (a.count + 255) / 256;
+  remap_kernel<<<(unsigned)(blocks < 148L * 64 ? blocks : 148L * 64), 256, 0, st>>>(a, mode);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st) {
+  const long M = (long)mx * my;
+  const long blocks = (M + 255) / 256;
+  stencil_kernel<<<(unsigned)(blocks < 148L * 64 ? blocks : 148L * 64), 256, 0, st>>>(v, Av, mx, my, ihx2, ihy2);
+  return cudaGetLastError();
+}
+
+}  // namespace pint

@@ -1,0 +1,61 @@
+// inst_n.cu — per-FFT-length instantiation unit; compiled once per PINT_N (build.py).
+#include "kernels.h"
+
+#ifndef PINT_N
+#error "define PINT_N"
+#endif
+#define PINT_CAT2(a, b) a##b
+#define PINT_CAT(a, b) PINT_CAT2(a, b)
+
+namespace pint {
+
+template <int MI, int MO, bool CQ>
+static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
+  auto kern = tpass_kernel<PINT_N, MI, MO, CQ>;
+  const int smem = phys_size(TILE) * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (ntiles <= 0) return cudaSuccess;
+  kern<<<(unsigned)ntiles, TPB, smem, st>>>(a, ntiles);
+  return cudaGetLastError();
+}
+
+cudaError_t PINT_CAT(launch_tpass_, PINT_N)(int mi, int mo, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  if (mo == OUT_U) return go<IN_FREQ, OUT_U, false>(a, ntiles, st);
+  if (!cq) {
+    switch (mi) {
+      case IN_FREQ: return go<IN_FREQ, OUT_H, false>(a, ntiles, st);
+      case IN_TIME_V: return go<IN_TIME_V, OUT_H, false>(a, ntiles, st);
+      case IN_TIME_ZERO: return go<IN_TIME_ZERO, OUT_H, false>(a, ntiles, st);
+      default: return go<IN_TIME_BUF, OUT_H, false>(a, ntiles, st);
+    }
+  }
+  switch (mi) {
+    case IN_FREQ: return go<IN_FREQ, OUT_H, true>(a, ntiles, st);
+    case IN_TIME_V: return go<IN_TIME_V, OUT_H, true>(a, ntiles, st);
+    case IN_TIME_ZERO: return go<IN_TIME_ZERO, OUT_H, true>(a, ntiles, st);
+    default: return go<IN_TIME_BUF, OUT_H, true>(a, ntiles, st);
+  }
+}
+
+cudaError_t PINT_CAT(launch_dst_, PINT_N)(const DstArgs& a, int mode, cudaStream_t st) {
+  auto kern = dst_kernel<PINT_N>;
+  const int smem = phys_size(TILE) * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long rb = TILE / PINT_N;
+  const long blocks = (a.rows + rb - 1) / rb;
+  if (blocks <= 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, TPB, smem, st>>>(a, mode);
+  return cudaGetLastError();
+}
+
+}  // namespace pint

@@ -1,0 +1,35 @@
+// kernels.h — host-side launch interface of the device kernels (one .cu per FFT length).
+#pragma once
+#include <cuda_runtime.h>
+#include "tpass.cuh"
+#include "spass.cuh"
+#include "dst.cuh"
+
+namespace pint {
+
+// T-pass for FFT length N (power of two, 16..4096); returns the launch error.
+cudaError_t launch_tpass(int N, int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st);
+// S-pass: chunk C = ceil(L/32) rounded up to a power of two (1..32), G lines per CTA.
+cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st);
+// layout remaps and the FD stencil (dispatch.cu)
+cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);
+// DST-I rows, extended FFT length NE = 2(mx+1).
+cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st);
+
+#define PINT_DECLARE_N(NN)                                                                         \
+  cudaError_t launch_tpass_##NN(int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, \
+                                cudaStream_t st);                                                  \
+  cudaError_t launch_dst_##NN(const DstArgs& a, int mode, cudaStream_t st);
+PINT_DECLARE_N(16)
+PINT_DECLARE_N(32)
+PINT_DECLARE_N(64)
+PINT_DECLARE_N(128)
+PINT_DECLARE_N(256)
+PINT_DECLARE_N(512)
+PINT_DECLARE_N(1024)
+PINT_DECLARE_N(2048)
+PINT_DECLARE_N(4096)
+#undef PINT_DECLARE_N
+
+}  // namespace pint

@@ -1,0 +1,216 @@
+// tpass.cuh — the time-axis pass ("T-pass") of one WR iteration, fused per spatial tile.
+//
+// One CTA owns one tile: all N time levels of WB = 4096/N contiguous spatial columns
+// (64 KB complex128, contiguous in the blocked layout [q][yb][n][WB]).  Per iteration
+// (mode FREQ -> H):
+//   W_m --(inverse time FFT, unscale: Step 3)--> U_m            [registers]
+//   update |U_m - U_{m-1}| on the wrap window n = N-k+1..N; store the new wrap state
+//   F_m = f̄ + tau^-a (sum_{j<n} w_j) v + kappa-wrap(U_m)   (eqn:BDF-k-F / eq:BDF-subdiff-F)
+//   H_{m+1} = (h^2/N) FFT(Gamma F_m)                           (Step 1)
+// HBM traffic: read 16 B + write 16 B per space-time unknown.
+//
+// CQ (subdiffusion) wrap: kappa Wup U = (C(kappa) U - C(-kappa) U) / 2 with C(c) the
+// c-circulant of omega_0..omega_{N-1} (B_k(kappa) = C(kappa)), both
+// diagonalised by scaled DFTs (Lemma 3.2); in the frequency domain
+//   H = (h^2/N) FFT(Gamma F_static) + (h^2/2 tau^a) [ D W - V^{-1} Theta^{-1} V D' V^{-1} Theta V W ],
+//   Theta = diag(e^{i pi n/N}), D' = eigenvalues of C(-kappa).  DESIGN.md "CQ wrap".
+#pragma once
+#include "fft.cuh"
+
+namespace pint {
+
+enum { IN_FREQ = 0, IN_TIME_V = 1, IN_TIME_ZERO = 2, IN_TIME_BUF = 3 };
+enum { OUT_H = 0, OUT_U = 1 };
+
+struct TPassArgs {
+  const double2* in;        // W (FREQ) or U (TIME_BUF), tile-blocked layout
+  double2* out;             // H (OUT_H) or U (OUT_U); may alias `in` (tile-local in place)
+  const double2* wrap_old;  // [ntiles][k][WB] last-k levels of U_{m-1} (FREQ mode monitor)
+  double2* wrap_new;        // [ntiles][k][WB] last-k levels of U_m
+  const double2* src;       // [S][ntiles][WB] spatial source vectors (g_r, Av, v) in tile layout
+  const double* coef;       // [S][N] time coefficients of F_static
+  const int* nhi;           // [S] coef[s][n] == 0 for n >= nhi[s]
+  int S;
+  const double2* vsrc;      // the v source (for IN_TIME_V), tile layout [ntiles][WB]
+  const double2* tw;        // [N] exp(-2 pi i m/N)
+  const double* gsf;        // [N] kappa^{n/N} h^2/N      (forward scale, heat)
+  const double* igs;        // [N] kappa^{-n/N}           (unscale)
+  const double* gsN;        // [N] kappa^{n/N} / N        (CQ time-mode bootstrap)
+  const double* wk;         // [k+1] (kappa/tau) omega_j  (heat wrap)
+  int k;
+  // CQ tables
+  const double2* dh;        // [N] (h^2 / (2 tau^a)) d_p
+  const double2* dpr;       // [N] d'_p (eigenvalues of C(-kappa))
+  const double2* thp;       // [N] theta^n / N
+  const double2* thm;       // [N] -(h^2/(2 N tau^a)) theta^{-n}
+  const double* gsfq;       // [N] kappa^{n/N} h^2/N (CQ static part)
+  unsigned long long* upd;  // max |update| as ordered bits
+};
+
+__device__ __forceinline__ void block_max_atomic(double x, unsigned long long* dst) {
+  __shared__ double red[TPB / 32];
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  // NaN must survive: fmax drops NaN, so track it separately
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int i = 1; i < TPB / 32; ++i) m = fmax(m, red[i]);
+    atomicMax(dst, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]
+__device__ __forceinline__ double2 static_rhs(const TPassArgs& a, long tile, int WB, int N, int n, int c, long ntiles) {
+  double2 f = make_double2(0.0, 0.0);
+  for (int s = 0; s < a.S; ++s) {
+    if (n < __ldg(&a.nhi[s])) {
+      const double cf = __ldg(&a.coef[(long)s * N + n]);
+      const double2 g = __ldg(&a.src[((long)s * ntiles + tile) * WB + c]);
+      f = cfmar(g, cf, f);
+    }
+  }
+  return f;
+}
+
+template <int N, int MODE_IN, int MODE_OUT, bool CQ>
+__global__ void __launch_bounds__(TPB, CQ ? 2 : 3) tpass_kernel(const TPassArgs a, long ntiles) {
+  using TM = TimeMap<N>;
+  using FM = FreqMap<N>;
+  constexpr int WB = TILE / N;
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const long tile = blockIdx.x;
+  const long base = tile * (long)TILE;
+  const int k = a.k;
+  double2 v[16];
+  double2 dw[CQ ? 16 : 1];
+  double upd = 0.0;
+  bool nonfinite = false;
+
+  // ---------------- input ----------------
+  if constexpr (MODE_IN == IN_FREQ) {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
+    if constexpr (CQ) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
+    }
+    run_passes<N, +1, false>(v, sm, a.tw, tid);        // u = V W  (unnormalised inverse DFT)
+  } else {
+    // time-domain input U (registers in TimeMap)
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) {
+        const int r = j * TM::RL + s;
+        if constexpr (MODE_IN == IN_TIME_V) v[r] = __ldg(&a.vsrc[tile * WB + TM::c(j, tid)]);
+        else if constexpr (MODE_IN == IN_TIME_ZERO) v[r] = make_double2(0.0, 0.0);
+        else v[r] = a.in[base + TM::e(j, s, tid)];
+      }
+    if constexpr (CQ) {
+      // W = FFT(Gamma U)/N, then u = V W (recomputed) so the frequency-domain path is shared
+#pragma unroll
+      for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+        for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cscale(v[j * TM::RL + s], __ldg(&a.gsN[TM::n(j, s, tid)]));
+      run_passes<N, -1, true>(v, sm, a.tw, tid);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
+      run_passes<N, +1, false>(v, sm, a.tw, tid);
+    }
+    // heat time modes: v holds U itself (HAVE_U_DIRECT below)
+  }
+
+  // ---------------- U_m = Gamma^{-1} u ; wrap window ----------------
+  // v holds u (FREQ or CQ time modes) or U (heat time modes).
+  constexpr bool HAVE_U_DIRECT = (MODE_IN != IN_FREQ) && !CQ;
+  if constexpr (MODE_OUT == OUT_U) {
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) {
+        const int r = j * TM::RL + s;
+        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[TM::n(j, s, tid)]));
+        a.out[base + TM::e(j, s, tid)] = U;
+      }
+    return;
+  }
+
+  __syncthreads();   // sm free: all readers of the last exchange are done
+  double2* sW = sm;  // [k][WB] wrap window values of U_m
+#pragma unroll
+  for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+    for (int s = 0; s < TM::RL; ++s) {
+      const int n = TM::n(j, s, tid);
+      if (n >= N - k) {
+        const int r = j * TM::RL + s, c = TM::c(j, tid), jj = n - (N - k);
+        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[n]));
+        const long wi = (tile * k + jj) * WB + c;
+        if constexpr (MODE_IN == IN_FREQ) {
+          const double2 o = a.wrap_old[wi];
+          const double d = sqrt(cabs2(csub(U, o)));
+          if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+          upd = fmax(upd, d);
+        }
+        a.wrap_new[wi] = U;
+        sW[jj * WB + c] = U;
+      }
+    }
+  __syncthreads();
+
+  if constexpr (!CQ) {
+    // ---------------- heat: F = F_static + wrap ; X = Gamma F h^2/N ----------------
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) {
+        const int n = TM::n(j, s, tid), c = TM::c(j, tid);
+        double2 F = static_rhs(a, tile, WB, N, n, c, ntiles);
+        if (n < k) {
+          // (kappa/tau) sum_{j=n+1}^{k} omega_j U_m^{N+n-j} (0-based levels), window index k+n-j
+          for (int jw = n + 1; jw <= k; ++jw) F = cfmar(sW[(k + n - jw) * WB + c], __ldg(&a.wk[jw]), F);
+        }
+        v[j * TM::RL + s] = cscale(F, __ldg(&a.gsf[n]));
+      }
+    run_passes<N, -1, true>(v, sm, a.tw, tid);   // H = (h^2/N) FFT(Gamma F)
+  } else {
+    // ---------------- CQ ----------------
+    // z = V^{-1} Theta u
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cmul(v[j * TM::RL + s], __ldg(&a.thp[TM::n(j, s, tid)]));
+    run_passes<N, -1, true>(v, sm, a.tw, tid);
+    // s = V (D' z)
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[FM::p(t, tid)]));
+    run_passes<N, +1, false>(v, sm, a.tw, tid);
+    // X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) {
+        const int n = TM::n(j, s, tid), c = TM::c(j, tid);
+        const double2 F = static_rhs(a, tile, WB, N, n, c, ntiles);
+        const int r = j * TM::RL + s;
+        v[r] = cfmar(F, __ldg(&a.gsfq[n]), cmul(v[r], __ldg(&a.thm[n])));
+      }
+    run_passes<N, -1, true>(v, sm, a.tw, tid);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = cadd(v[t], dw[t]);
+  }
+
+#pragma unroll
+  for (int t = 0; t < 16; ++t) a.out[base + FM::e(t, tid)] = v[t];
+
+  if constexpr (MODE_IN == IN_FREQ) {
+    // fmax drops NaN: report any non-finite update as +inf (orders above all finite bits)
+    if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
+    block_max_atomic(upd, a.upd);
+  }
+}
+
+}  // namespace pint

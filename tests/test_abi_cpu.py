@@ -1,0 +1,69 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/pint.h
+declares, and rejects bad arguments (PINT_ERR_ARG / UNSUPPORTED) before any CUDA call."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2007_13125_b200 import pint as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "pint.h")).read()
+    return sorted(set(re.findall(r"\b(pint_[a-z_0-9]+)\s*\(", src)) - {"pint_allreduce_max_fn"})
+
+
+def test_exports_every_declared_symbol():
+    L = P.lib()
+    decl = declared_symbols()
+    assert len(decl) >= 17
+    for name in decl:
+        assert hasattr(L, name), name
+    assert sorted(P.EXPORTED) == decl
+
+
+def test_status_strings_and_kappa_rule():
+    L = P.lib()
+    assert L.pint_status_string(0) == b"PINT_OK"
+    assert L.pint_status_string(8) == b"PINT_ERR_UNSUPPORTED"
+    assert abs(P.kappa_log_rule(1024) - 1 / 6.931471805599453) < 1e-15
+    assert P.kappa_log_rule(2) == 0.5
+
+
+@pytest.mark.parametrize("kw,status,needle", [
+    (dict(k=0), P.PINT_ERR_ARG, "k must be in 1..6"),
+    (dict(k=7), P.PINT_ERR_ARG, "k must be in 1..6"),
+    (dict(kappa=0.0), P.PINT_ERR_ARG, "kappa"),
+    (dict(kappa=1.0), P.PINT_ERR_ARG, "kappa"),
+    (dict(tau=0.0), P.PINT_ERR_ARG, "tau"),
+    (dict(N=2, k=2), P.PINT_ERR_ARG, "N must be >= k+1"),
+    (dict(alpha=1.5), P.PINT_ERR_ARG, "alpha"),
+    (dict(alpha=0.0), P.PINT_ERR_ARG, "alpha"),
+    (dict(N=100), P.PINT_ERR_UNSUPPORTED, "power of two"),
+    (dict(mx=2000), P.PINT_ERR_UNSUPPORTED, "line length"),
+    (dict(mx=100, my=10), P.PINT_ERR_UNSUPPORTED, "2(mx+1)"),
+    (dict(nranks=2, rank=0), P.PINT_ERR_ARG, "1D operators do not shard"),
+])
+def test_create_rejects(kw, status, needle):
+    a = dict(mx=63, my=1, N=64, k=2, kappa=0.1, tau=1 / 64, alpha=1.0)
+    nr = kw.pop("nranks", 1)
+    rk = kw.pop("rank", 0)
+    a.update(kw)
+    with pytest.raises(P.PintError) as e:
+        P.Plan(a["mx"], a["my"], a["N"], a["k"], a["kappa"], a["tau"], a["alpha"], rank=rk, nranks=nr)
+    assert e.value.status == status
+    assert needle in str(e.value)
+
+
+def test_null_arguments():
+    L = P.lib()
+    op = P.pint_operator(P.PINT_OP_FD1D_DIRICHLET, 63, 1)
+    assert L.pint_plan_create(63, 64, 2, 0.1, 1 / 64, ctypes.byref(op), None, None) == P.PINT_ERR_ARG
+    h = ctypes.c_void_p()
+    assert L.pint_plan_create(64, 64, 2, 0.1, 1 / 64, ctypes.byref(op), None, ctypes.byref(h)) == P.PINT_ERR_ARG
+    assert b"M must equal" in L.pint_last_error()
+    assert L.pint_wr_iterate(None, None) == P.PINT_ERR_ARG
+    assert L.pint_plan_destroy(None) == P.PINT_ERR_ARG

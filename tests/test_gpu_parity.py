@@ -1,0 +1,170 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element on the same
+seeded inputs, at fixed iteration counts m (SURVEY §8(c) "Parity metric").
+
+Gate (BASELINE.json north_star): full space-time array relative L2 <= 1e-10 (fp64 complex).
+"""
+import numpy as np
+import pytest
+
+from oracle import modal, sequential, wr
+from paper_2007_13125_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def pint():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2007_13125_b200 import pint as P
+    P.lib()
+    return P
+
+
+def gpu_iterates(P, prob, iters, **kw):
+    out, upd = [], []
+    with P.Plan.from_problem(prob, **kw) as plan:
+        for _ in range(iters):
+            upd.append(plan.iterate())
+            out.append(plan.get_solution())
+    return out, upd
+
+
+def check(P, prob, iters, tol=TOL, oracle_kw=None):
+    g, _ = gpu_iterates(P, prob, iters)
+    o = wr.wr_naive(prob, iters, **(oracle_kw or {}))
+    errs = [rel(g[m], o[m + 1]) for m in range(iters)]
+    assert max(errs) <= tol, errs
+    return errs
+
+
+def test_c1_parity_and_fixed_point(pint):
+    prob = inputs.config_c1()
+    errs = check(pint, prob, 5)
+    assert max(errs) < 1e-12, errs
+    with pint.Plan.from_problem(prob) as p:
+        it, u, st = p.solve(1e-12, 20)
+        assert st == 0 and it <= 6 and u < 1e-12
+        assert rel(p.get_solution(), sequential.sequential(prob)) < 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("kappa", [1e-1, 1e-2, 1e-3])
+def test_c2_sweep(pint, k, kappa):
+    """C2: 1D M=1023, N=1024, every k and kappa (18 runs), m = 1..3."""
+    check(pint, inputs.config_c2(k=k, kappa=kappa), 3)
+
+
+CASES = [
+    # mx, my, N, k, kappa, alpha, R   (ragged line lengths, every FFT length, heat + CQ, 1D + 2D)
+    (37, 1, 16, 1, 0.3, 1.0, 2),
+    (1, 1, 32, 2, 0.2, 1.0, 1),          # M = 1: scalar ODE (degenerate)
+    (100, 1, 32, 3, 0.1, 1.0, 2),
+    (200, 1, 128, 6, 0.05, 1.0, 1),
+    (1000, 1, 64, 2, 0.1, 0.5, 1),
+    (333, 1, 512, 4, 0.02, 0.3, 2),
+    (127, 1, 2048, 6, 0.01, 1.0, 0),
+    (63, 1, 4096, 2, 0.1, 1.0, 1),
+    (15, 9, 64, 4, 0.2, 1.0, 2),
+    (31, 40, 256, 5, 0.05, 1.0, 1),
+    (63, 33, 128, 2, 0.05, 0.5, 1),
+    (7, 100, 512, 3, 0.1, 0.7, 1),
+    (255, 17, 1024, 1, 0.1, 0.5, 0),
+    (127, 1024, 16, 2, 0.3, 1.0, 1),     # longest line, shortest N
+]
+
+
+@pytest.mark.parametrize("mx,my,N,k,kappa,alpha,R", CASES)
+def test_random_complex(pint, mx, my, N, k, kappa, alpha, R):
+    prob = inputs.random_complex_problem(mx, my, N, k, kappa, alpha, R=R, seed=mx + my + N + k)
+    check(pint, prob, 3, oracle_kw={"dft": "fft", "wrap": "fft"} if N * mx * my > 2e6 else None)
+
+
+def test_c3_parity(pint):
+    """C3: 2D 511^2, N = 256, BDF4, kappa = 0.05 (full size, full array), m = 1..2."""
+    check(pint, inputs.config_c3(), 2)
+
+
+def test_c5_reduced_parity(pint):
+    """C5 recipe at 127^2 (N = 1024, CQ-BDF2, alpha = 0.5): full array, m = 1..3."""
+    check(pint, inputs.config_c5(m=127), 3, oracle_kw={"dft": "fft", "wrap": "fft"})
+
+
+def test_c4_modal_sampled(pint):
+    """C4 at full size (1023^2 x 2048, 34 GB per buffer): sampled levels vs the per-mode oracle O4."""
+    prob = inputs.config_c4()
+    basis = modal.ModalBasis(1023, 1023, np.arange(1, 33), np.arange(1, 33))
+    C = inputs.c4_mode_coefficients()          # C[p-1, q-1] multiplies sin(p pi x) sin(q pi y)
+    coef = C.T.reshape(-1)                     # basis layout [q][p]
+    iters = 3
+    md = modal.modal_wr(prob, basis, coef, np.zeros((0, coef.size)), iters)
+    levels = [0, 1, 5, 1023, 2046, 2047]
+    with pint.Plan.from_problem(prob) as p:
+        for m in range(1, iters + 1):
+            p.iterate()
+            for n in levels:
+                g = p.get_levels(n, 1)[0]
+                o = basis.to_grid(md[m][n])
+                assert rel(g, o) < TOL, (m, n, rel(g, o))
+
+
+def test_u0_zero_and_initial_guess(pint):
+    prob = inputs.example1_fd(3, M=99, N=64)            # U_0 = 0 (table setting)
+    check(pint, prob, 3)
+    prob = inputs.config_c1()
+    Us = sequential.sequential(prob)
+    with pint.Plan.from_problem(prob) as p:
+        p.set_initial_guess(np.ascontiguousarray(Us))   # the fixed point
+        u = p.iterate()
+        assert u < 1e-12
+        assert rel(p.get_solution(), Us) < 1e-12
+
+
+def test_reading_does_not_perturb(pint):
+    prob = inputs.config_c2(k=3, kappa=0.01)
+    a, ua = gpu_iterates(pint, prob, 3)
+    with pint.Plan.from_problem(prob) as p:
+        ub = [p.iterate() for _ in range(3)]
+        b = p.get_solution()
+    assert np.array_equal(a[-1], b)
+    assert ua == ub
+
+
+def test_device_arrays_and_levels(pint):
+    import torch
+    prob = inputs.random_complex_problem(40, 30, 64, 3, 0.1, 1.0, R=2, seed=4)
+    with pint.Plan.from_problem(prob, device_arrays=True) as p:
+        p.iterate(); p.iterate()
+        full = p.get_solution()
+        dev = torch.empty((10, prob.M), dtype=torch.complex128, device="cuda")
+        p.get_levels(20, 10, out=dev)
+        assert np.array_equal(dev.cpu().numpy(), full[20:30])
+    o = wr.wr_naive(prob, 2)[2]
+    assert rel(full, o) < TOL
+
+
+def test_state_errors_and_timing(pint):
+    P = pint
+    with P.Plan(63, 1, 64, 2, 0.1, 1 / 64) as p:
+        with pytest.raises(P.PintError) as e:
+            p.iterate()
+        assert e.value.status == P.PINT_ERR_STATE
+        prob = inputs.config_c1()
+        p.set_problem(prob.v, prob.g, prob.phi, prob.dphi)
+        with pytest.raises(P.PintError) as e:
+            p.get_solution()
+        assert e.value.status == P.PINT_ERR_STATE
+        p.set_timing(True)
+        for _ in range(3):
+            p.iterate()
+        t = p.get_timing()
+        assert t["tpass_launches"] == 3 and t["spass_launches"] == 3
+        assert t["tpass_ms"] > 0 and t["spass_ms"] > 0
+        it, u, st = p.solve(0.0, 2, raise_on_fail=False)
+        assert st == P.PINT_ERR_NOT_CONVERGED and it == 2
