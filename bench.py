@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark: space-time unknowns per second per WR iteration (complex128), BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+A step is one waveform-relaxation iteration (S-pass + fused T-pass, all of SURVEY §8(a)'s
+per-iteration rows) over the whole space-time array, inputs resident in HBM.  Default
+workload C4 (2D heat 1023^2, N = 2048, BDF6, kappa = 0.01: 2.14e9 unknowns, 34.3 GB per
+buffer) — the config the metric's 1/2/4/8-GPU scaling is quoted on.
+For N > 1 (torchrun) each rank owns an x-mode slab (strong scaling, no data-path collective;
+the update norm is all-reduced with NCCL).  Rank 0 prints one JSON line.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time unknowns/sec per WR iteration (complex128) and HBM fraction, 1/2/4/8 GPU"
+UNIT = "unknowns/s"
+BYTES_PER_UNKNOWN_PASS = 32        # each pass reads 16 B and writes 16 B per unknown
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def make_problem(name: str, mx: int | None = None):
+    from paper_2007_13125_b200 import inputs
+    if name == "C4":
+        return inputs.config_c4(m=mx or 1023) if mx is None else _c4_narrow(mx)
+    if name == "C3":
+        return inputs.config_c3()
+    if name == "C5":
+        return inputs.config_c5()
+    if name == "C2":
+        return inputs.config_c2(k=6, kappa=1e-3)
+    if name == "C1":
+        return inputs.config_c1()
+    raise ValueError(name)
+
+
+def _c4_narrow(mx: int):
+    """C4 with fewer x-modes (same N, k, kappa, line length 1023, kernels and tile shapes): profiling."""
+    from paper_2007_13125_b200 import inputs
+    p = inputs.config_c4()
+    v = p.v.reshape(1023, 1023)[:, :mx].copy().reshape(-1)
+    return p.with_(mx=mx, v=v, g=np.zeros((0, 1023 * mx), np.complex128))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        pw = [float(r[7]) for r in self.rows if len(r) > 7 and r[7].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+
+
+def cpu_baseline(prob_name: str, budget_s: float = 30.0):
+    """The oracle (oracle.wr.wr_naive, as it stands) on host cores, one WR iteration on a bounded
+    sample of the workload: same N, k, kappa, alpha and recipe on a reduced spatial grid."""
+    from oracle import wr
+    from paper_2007_13125_b200 import inputs
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:   # noqa: BLE001
+        cores = os.cpu_count()
+    if prob_name == "C4":
+        prob = inputs.config_c4(m=95)
+        sample = "oracle O2 (naive-DFT WR) 1 iteration on the C4 recipe at 95x95, N=2048, BDF6, kappa=0.01"
+    elif prob_name == "C5":
+        prob = inputs.config_c5(m=31)
+        sample = "oracle O2 1 iteration on the C5 recipe at 31x31, N=1024, CQ-BDF2"
+    elif prob_name == "C3":
+        prob = inputs.config_c3(m=127)
+        sample = "oracle O2 1 iteration on the C3 recipe at 127x127, N=256, BDF4"
+    else:
+        prob = make_problem(prob_name)
+        sample = f"oracle O2 1 iteration on {prob_name} (full size)"
+    t = []
+    wr.wr_naive(prob, 1, keep=False, timings=t)
+    return {"value": prob.M * prob.N / t[0], "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": sample, "seconds": t[0]}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals, secs = [], []
+    base = None
+    for _ in range(args.warmup + args.steps):
+        base = cpu_baseline(args.config)
+        vals.append(base["value"])
+        secs.append(base["seconds"])
+    v = vals[args.warmup:]
+    value = statistics.mean(v)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(secs[args.warmup:]),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+           "data": "synthetic (seeded recipe, SURVEY §8(d))",
+           "config": {"workload": f"{args.config} (oracle sample)", "sample": base["sample"]},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
+                            "sample": base["sample"]},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--mx", type=int, default=None, help="C4 only: fewer x-modes (profiling)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2007_13125_b200 import pint
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    red = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def allreduce_max(x: float) -> float:
+        red.fill_(x)
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+        return float(red.item())
+
+    prob = make_problem(args.config, args.mx)
+    stream = torch.cuda.Stream(device=dev)
+    plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
+                     stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
+                     allreduce_max=allreduce_max if world > 1 else None)
+    v = torch.from_numpy(prob.v).to(dev)
+    g = torch.from_numpy(np.ascontiguousarray(prob.g)).to(dev) if prob.R else None
+    plan.set_problem(v, g, prob.phi if prob.R else None, prob.dphi if prob.R else None)
+    q0, q1 = plan.partition()
+    local_unknowns = (q1 - q0) * (prob.M // prob.mx) * prob.N if prob.my > 1 else prob.M * prob.N
+
+    for _ in range(args.warmup):
+        plan.iterate()
+    launches0 = plan.info()["kernel_launches"]
+    plan.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        upd = []
+        for _ in range(args.steps):
+            upd.append(plan.iterate())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    tm = plan.get_timing()
+    plan.set_timing(False)
+    launches = plan.info()["kernel_launches"] - launches0
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_unknowns = prob.M * prob.N
+    value = total_unknowns / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (CUDA events around each launch on the plan stream)
+    hbm, peak_src = peaks()
+    t_avg = tm["tpass_ms"] / max(tm["tpass_launches"], 1)
+    s_avg = tm["spass_ms"] / max(tm["spass_launches"], 1)
+    bytes_launch = BYTES_PER_UNKNOWN_PASS * local_unknowns
+    dom = ("tpass", t_avg) if t_avg >= s_avg else ("spass", s_avg)
+    achieved = bytes_launch / (dom[1] / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(f"{args.config}:{dom[0]}")
+    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_launch,
+                "passes": {"tpass_ms": t_avg, "spass_ms": s_avg,
+                           "tpass_GBs": bytes_launch / (t_avg / 1e3) / 1e9,
+                           "spass_GBs": bytes_launch / (s_avg / 1e3) / 1e9,
+                           "iteration_GBs": 2 * bytes_launch / (ms_step / 1e3) / 1e9,
+                           "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm}}
+
+    # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host
+    e2e = None
+    if not args.no_e2e and world == 1:
+        vh = np.ascontiguousarray(prob.v)
+        out = np.empty((1, prob.M), np.complex128)
+        steps, t_tot, its = args.e2e_steps, 0.0, 0
+        for i in range(steps + 1):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            plan.set_problem(vh, np.ascontiguousarray(prob.g) if prob.R else None,
+                             prob.phi if prob.R else None, prob.dphi if prob.R else None)
+            it, u, st = plan.solve(prob.tol, 20, raise_on_fail=False)
+            plan.get_levels(prob.N - 1, 1, out)
+            dt = time.perf_counter() - t0
+            if i > 0:
+                t_tot += dt
+                its += it
+        e2e = {"value": total_unknowns * its / t_tot, "unit": UNIT,
+               "h2d_bytes_per_step": int(vh.nbytes + (prob.g.nbytes if prob.R else 0)),
+               "d2h_bytes_per_step": int(out.nbytes + 8 * its // steps),
+               "what": f"set_problem(host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
+                       "final time level to host, per step; unknowns/s per WR iteration"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args.config)
+
+    if rank == 0:
+        res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded recipe, SURVEY §8(d))",
+               "config": {"workload": args.config if args.mx is None else f"{args.config}(mx={args.mx})",
+                          "grid": f"{prob.mx}x{prob.my}", "N": prob.N, "k": prob.k, "kappa": prob.kappa,
+                          "alpha": prob.alpha, "unknowns": total_unknowns,
+                          "parallelism": f"x-mode slabs x{world}" if world > 1 else "1 GPU",
+                          "l2": f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed"},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+               "clocks": clk.summary(), "last_update": upd[-1] if upd else None}
+        print(json.dumps(res))
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -12,6 +12,8 @@ with S = Lambda V, Lambda = diag(kappa^{-(n-1)/N}) = Gamma^{-1}, V_{lp} = e^{+2 
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from . import bdf, problem, spatial
@@ -93,7 +95,7 @@ def initial_guess(prob) -> np.ndarray:
 
 def wr_naive(prob, iters: int, U0: np.ndarray | None = None, dft: str = "naive",
              wrap: str = "matrix", op: Operator | None = None, F_static: np.ndarray | None = None,
-             callback=None) -> list[np.ndarray]:
+             callback=None, keep: bool = True, timings: list | None = None) -> list[np.ndarray]:
     """Run `iters` WR iterations; returns [U_0, U_1, ..., U_iters] (each [N][M]).
 
     dft="naive": explicit N x N DFT matrices applied by zgemm (the default, obviously correct);
@@ -113,13 +115,19 @@ def wr_naive(prob, iters: int, U0: np.ndarray | None = None, dft: str = "naive",
     U = initial_guess(prob) if U0 is None else U0
     out = [U]
     for _ in range(iters):
+        t0 = time.perf_counter()
         F = rhs(prob, U, F_static, w, wrap)
         X = gam[:, None] * F                              # Step 1a: Gamma F
         H = (Vinv @ X) if dft == "naive" else np.fft.fft(X, axis=0) / N   # Step 1b
         Q = op.solve(shifts, H)                           # Step 2
         Y = (V @ Q) if dft == "naive" else np.fft.ifft(Q, axis=0) * N     # Step 3: V Q
         U = Y / gam[:, None]                              # Step 3: Gamma^{-1}
-        out.append(U)
+        if timings is not None:
+            timings.append(time.perf_counter() - t0)
+        if keep:
+            out.append(U)
+        else:
+            out[-1:] = [U]
         if callback is not None:
             callback(U)
     return out
