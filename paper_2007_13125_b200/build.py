@@ -48,19 +48,25 @@ def _compile(src: str, obj: str, defines: list[str]) -> tuple[str, str]:
     return obj, r.stderr
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
+          defines: list[str] | None = None, lib: str | None = None) -> str:
+    """defines/lib: experimental variants (e.g. ["-DPINT_TPASS_MINB=3"], "libpint_minb3.so")."""
+    defines = defines or []
+    LIB = os.path.join(HERE, lib) if lib else globals()["LIB"]
+    build_dir = BUILD + ("_" + os.path.splitext(lib)[0] if lib else "")
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_dep():
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
-    units = [(os.path.join(CSRC, "inst_n.cu"), os.path.join(BUILD, f"inst_{n}.o"), [f"-DPINT_N={n}"]) for n in NS]
-    units += [(os.path.join(CSRC, "dispatch.cu"), os.path.join(BUILD, "dispatch.o"), []),
-              (os.path.join(CSRC, "pint.cu"), os.path.join(BUILD, "pint.o"), [])]
+    os.makedirs(build_dir, exist_ok=True)
+    units = [(os.path.join(CSRC, "inst_n.cu"), os.path.join(build_dir, f"inst_{n}.o"), [f"-DPINT_N={n}", *defines])
+             for n in NS]
+    units += [(os.path.join(CSRC, "dispatch.cu"), os.path.join(build_dir, "dispatch.o"), defines),
+              (os.path.join(CSRC, "pint.cu"), os.path.join(build_dir, "pint.o"), defines)]
     jobs = jobs or min(len(units), os.cpu_count() or 4)
     logs = []
     with cf.ThreadPoolExecutor(jobs) as ex:
         for obj, log in ex.map(lambda u: _compile(*u), units):
             logs.append((obj, log))
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+    with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
         for obj, log in logs:
             f.write(f"== {os.path.basename(obj)}\n{log}\n")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *[u[1] for u in units]]
@@ -77,6 +83,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("-D", action="append", default=[], help="extra define (variant builds)")
+    ap.add_argument("--lib", default=None, help="variant library file name")
     args = ap.parse_args()
-    build(force=args.force, jobs=args.j, verbose=True)
+    build(force=args.force, jobs=args.j, verbose=True, defines=[f"-D{d}" for d in args.D], lib=args.lib)
     sys.exit(0)

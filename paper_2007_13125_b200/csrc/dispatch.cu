@@ -1,6 +1,7 @@
 // dispatch.cu — runtime dispatch over the compiled FFT lengths and S-pass chunk sizes.
 #define PINT_DEFINE_PLAIN_KERNELS
 #include "kernels.h"
+#include <algorithm>
 
 namespace pint {
 
@@ -47,8 +48,20 @@ static cudaError_t spass_go(const SPassArgs& a, long Qb, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  dim3 grid((unsigned)(a.N / SG), (unsigned)Qb);
-  kern<<<grid, 32 * SG, smem, st>>>(a);
+  SPassArgs b = a;
+  int lwb = 0;
+  while ((1 << lwb) < a.WB) ++lwb;
+  int lg = 0;
+  while ((1 << lg) < SG) ++lg;
+  b.lwb = lwb;
+  b.lgw = lwb + lg;
+  b.nwork = Qb * (a.N / SG);
+  int dev = 0, nsm = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * SG, smem);
+  const long grid = std::min<long>(b.nwork, (long)nsm * std::max(per, 1));
+  kern<<<(unsigned)grid, 32 * SG, smem, st>>>(b);
   return cudaGetLastError();
 }
 

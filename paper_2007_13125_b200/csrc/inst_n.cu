@@ -13,14 +13,19 @@ template <int MI, int MO, bool CQ>
 static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
   auto kern = tpass_kernel<PINT_N, MI, MO, CQ>;
   const int smem = phys_size(TILE) * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static long resident = 0;   // persistent grid: SMs x resident CTAs per SM
+  if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    int dev = 0, nsm = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
+    resident = (long)nsm * (per > 0 ? per : 1);
   }
   if (ntiles <= 0) return cudaSuccess;
-  kern<<<(unsigned)ntiles, TPB, smem, st>>>(a, ntiles);
+  const long grid = ntiles < resident ? ntiles : resident;
+  kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
   return cudaGetLastError();
 }
 

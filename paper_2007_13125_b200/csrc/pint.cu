@@ -116,6 +116,7 @@ struct pint_plan_s {
   double* coef = nullptr;    // [S][N]
   int* nhi = nullptr;        // [S]
   int S = 0;
+  int nmax = 0;               // max_s nhi[s]
   double2 *tw = nullptr, *twE = nullptr;
   double *gsf = nullptr, *igs = nullptr, *gsN = nullptr, *wk = nullptr;
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
@@ -342,6 +343,7 @@ static TPassArgs targs(pint_plan p) {
   a.tw = p->tw; a.gsf = p->gsf; a.igs = p->igs; a.gsN = p->gsN; a.wk = p->wk; a.k = p->k;
   a.dh = p->dh; a.dpr = p->dpr; a.thp = p->thp; a.thm = p->thm; a.gsfq = p->gsf;
   a.upd = p->upd;
+  a.nmax = p->nmax;
   return a;
 }
 
@@ -474,6 +476,7 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
   for (int s = 0; s < S; ++s)
     for (int64_t n = 0; n < N; ++n)
       if (coef[(size_t)s * N + n] != 0.0) nhi[s] = (int)(n + 1);
+  p->nmax = *std::max_element(nhi.begin(), nhi.end());
   TRY(h2d(p, p->coef, coef));
   TRY(h2d(p, p->nhi, nhi));
   p->problem_set = true;

@@ -23,7 +23,21 @@ struct SPassArgs {
   const double* sig_q;    // [Qb] h^2 lambda_q (0 in 1D)
   long N, NB;
   int WB, L;
+  int lwb, lgw;           // log2(WB), log2(G*WB)
+  long nwork;             // Qb * (N / G) strips
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   const double s = 1.0 / fma(b.x, b.x, b.y * b.y);
@@ -59,134 +73,147 @@ template <int C, int G>
 __global__ void __launch_bounds__(32 * G, (C >= 32 ? 3 : 4)) spass_kernel(const SPassArgs a) {
   extern __shared__ double2 sm[];
   constexpr int SLINE0 = 32 * (C + 1);
-  const int WB = a.WB;
+  const int WB = a.WB, lwb = a.lwb, lgw = a.lgw;
   const int off = (WB >= 8) ? 0 : (WB > 8 / G ? WB : 8 / G);
   const int SLINE = SLINE0 + off;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const long q = blockIdx.y;
-  const long p0 = (long)blockIdx.x * G;
   const long N = a.N, NB = a.NB;
+  const long nblk = N / G;
   const int L = a.L;
   const int total = (int)NB * G * WB;
+  const int gwm = G * WB - 1, wbm = WB - 1;
 
-  // ---- stage the strip [NB][G][WB] (coalesced) into line-major padded smem ----
-  for (int e = threadIdx.x; e < total; e += 32 * G) {
-    const int yb = e / (G * WB), rem = e % (G * WB), g = rem / WB, j = rem % WB;
-    const int y = yb * WB + j;
-    if (y < 32 * C) sm[g * SLINE + y + y / C] = a.in[((q * NB + yb) * N + p0 + g) * WB + j];
-  }
-  __syncthreads();
+  for (long work = blockIdx.x; work < a.nwork; work += gridDim.x) {
+    const long q = work / nblk;
+    const long p0 = (work - q * nblk) * G;
+    const double2* in_base = a.in + (q * NB * N + p0) * WB;
+    // prefetch the next strip's runs into L2 (NB runs of G*WB*16 bytes, stride N*WB*16)
+    const long nxt = work + gridDim.x;
+    if (nxt < a.nwork) {
+      const long qn = nxt / nblk, pn = (nxt - qn * nblk) * G;
+      const double2* nb = a.in + (qn * NB * N + pn) * WB;
+      for (long yb = threadIdx.x; yb < NB; yb += 32 * G) prefetch_l2(nb + yb * N * WB, G * WB * 16);
+    }
+    // ---- stage the strip [NB][G][WB] into line-major padded smem (all copies in flight) ----
+    for (int e = threadIdx.x; e < total; e += 32 * G) {
+      const int yb = e >> lgw, rem = e & gwm, g = rem >> lwb, j = rem & wbm;
+      const int y = (yb << lwb) + j;
+      if (y < 32 * C) cp_async16(&sm[g * SLINE + y + y / C], in_base + ((long)yb * N + g) * WB + j);
+    }
+    cp_async_wait_all();
+    __syncthreads();
 
-  // ---- per line setup: sigma -> t -> u = 1 - a ----
-  const long p = p0 + warp;
-  const double2 sp = a.sig_p[p];
-  const double2 sig = make_double2(sp.x + a.sig_q[q], sp.y);
-  const double2 s = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
-  const double2 t1 = cscale(cadd(sig, s), 0.5), t2 = cscale(csub(sig, s), 0.5);
-  const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
-  const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);          // tb * ts = -sigma
-  const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
-  const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
-  const double2 rr = make_double2(1.0 + tt.x, tt.y);                  // r = 1/a, |r| > 1
-  const double2 u = cdiv(tt, rr);                                     // u = 1 - a
-  // u-forms of a^{C 2^j}
-  double2 uc[5];
-  uc[0] = upow(u, C);
+    // ---- per line setup: sigma -> t -> u = 1 - a ----
+    const long p = p0 + warp;
+    const double2 sp = a.sig_p[p];
+    const double2 sig = make_double2(sp.x + a.sig_q[q], sp.y);
+    const double2 s = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
+    const double2 t1 = cscale(cadd(sig, s), 0.5), t2 = cscale(csub(sig, s), 0.5);
+    const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
+    const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);          // tb * ts = -sigma
+    const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
+    const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
+    const double2 rr = make_double2(1.0 + tt.x, tt.y);                  // r = 1/a, |r| > 1
+    const double2 u = cdiv(tt, rr);                                     // u = 1 - a
+    double2 uc[5];                                                      // u-forms of a^{C 2^j}
+    uc[0] = upow(u, C);
 #pragma unroll
-  for (int i = 1; i < 5; ++i) uc[i] = uprod(uc[i - 1], uc[i - 1]);
+    for (int i = 1; i < 5; ++i) uc[i] = uprod(uc[i - 1], uc[i - 1]);
 
-  // ---- registers: rows y = lane*C + r ----
-  double2 d[C];
-  double2* line = sm + warp * SLINE + lane * (C + 1);
+    // ---- registers: rows y = lane*C + r ----
+    double2 d[C];
+    double2* line = sm + warp * SLINE + lane * (C + 1);
 #pragma unroll
-  for (int r = 0; r < C; ++r) {
-    const int y = lane * C + r;
-    d[r] = (y < L) ? line[r] : make_double2(0.0, 0.0);
-  }
+    for (int r = 0; r < C; ++r) {
+      const int y = lane * C + r;
+      d[r] = (y < L) ? line[r] : make_double2(0.0, 0.0);
+    }
 
-  // ---- forward recurrence f_y = d_y + a f_{y-1} ----
-  double2 f = make_double2(0.0, 0.0);
+    // ---- forward recurrence f_y = d_y + a f_{y-1} ----
+    double2 f = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
-  // inclusive scan S_t = sum_{s<=t} a^{C(t-s)} loc_s
+    for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int o = 1 << i;
-    double2 x;
-    x.x = __shfl_up_sync(0xffffffffu, f.x, o);
-    x.y = __shfl_up_sync(0xffffffffu, f.y, o);
-    if (lane >= o) f = cadd(f, amul(uc[i], x));
-  }
-  double2 carry;
-  carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
-  carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
-  if (lane == 0) carry = make_double2(0.0, 0.0);
-  f = carry;
+    for (int i = 0; i < 5; ++i) {                                       // S_t = sum_{s<=t} a^{C(t-s)} loc_s
+      const int o = 1 << i;
+      double2 x;
+      x.x = __shfl_up_sync(0xffffffffu, f.x, o);
+      x.y = __shfl_up_sync(0xffffffffu, f.y, o);
+      if (lane >= o) f = cadd(f, amul(uc[i], x));
+    }
+    double2 carry;
+    carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
+    carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
+    if (lane == 0) carry = make_double2(0.0, 0.0);
+    f = carry;
 #pragma unroll
-  for (int r = 0; r < C; ++r) {
-    f = cadd(d[r], amul(u, f));
-    d[r] = (lane * C + r < L) ? f : make_double2(0.0, 0.0);
-  }
+    for (int r = 0; r < C; ++r) {
+      f = cadd(d[r], amul(u, f));
+      d[r] = (lane * C + r < L) ? f : make_double2(0.0, 0.0);
+    }
 
-  // ---- backward recurrence w_y = f_y + a w_{y+1} ----
-  double2 w = make_double2(0.0, 0.0);
+    // ---- backward recurrence w_y = f_y + a w_{y+1} ----
+    double2 w = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
+    for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int o = 1 << i;
-    double2 x;
-    x.x = __shfl_down_sync(0xffffffffu, w.x, o);
-    x.y = __shfl_down_sync(0xffffffffu, w.y, o);
-    if (lane + o < 32) w = cadd(w, amul(uc[i], x));
-  }
-  carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
-  carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
-  if (lane == 31) carry = make_double2(0.0, 0.0);
-  w = carry;
+    for (int i = 0; i < 5; ++i) {
+      const int o = 1 << i;
+      double2 x;
+      x.x = __shfl_down_sync(0xffffffffu, w.x, o);
+      x.y = __shfl_down_sync(0xffffffffu, w.y, o);
+      if (lane + o < 32) w = cadd(w, amul(uc[i], x));
+    }
+    carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
+    carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
+    if (lane == 31) carry = make_double2(0.0, 0.0);
+    w = carry;
 #pragma unroll
-  for (int r = C - 1; r >= 0; --r) {
-    w = cadd(d[r], amul(u, w));
-    d[r] = w;
-  }
+    for (int r = C - 1; r >= 0; --r) {
+      w = cadd(d[r], amul(u, w));
+      d[r] = w;
+    }
 
-  // ---- rank-1 Dirichlet correction: x = a (w - w_0 phi) ----
-  double2 w0;
-  w0.x = __shfl_sync(0xffffffffu, d[0].x, 0);
-  w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
-  const double2 u2L = upow(u, 2L * L + 2);             // 1 - a^{2L+2}
-  const double2 K = cdiv(w0, u2L);                      // w_0 / (1 - a^{2L+2})
-  const int y0 = lane * C;
-  if (y0 < L) {
-    // skip chunks where |phi| < 1e-18 throughout (|a^{y+2}| falls and |a^{2L+2-y}| rises along y)
-    const double2 a1 = make_double2(1.0 - u.x, -u.y);   // a as a value
-    const double la = 0.5 * log(cabs2(a1));             // log|a| < 0
-    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));   // log(1e-18 |1-a^{2L+2}|)
-    const int ylast = min(y0 + C, L) - 1;
-    if ((y0 + 2) * la > thr || (2.0 * L + 2 - ylast) * la > thr) {
-      const double2 uP = upow(u, y0 + 2);               // a^{y0+2} = 1 - uP
-      const double2 uQ = upow(u, 2L * L + 2 - y0);      // a^{2L+2-y0}
-      double2 P = make_double2(1.0 - uP.x, -uP.y);
-      double2 Q = make_double2(1.0 - uQ.x, -uQ.y);
+    // ---- rank-1 Dirichlet correction: x = a (w - w_0 phi) ----
+    double2 w0;
+    w0.x = __shfl_sync(0xffffffffu, d[0].x, 0);
+    w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
+    const double2 u2L = upow(u, 2L * L + 2);             // 1 - a^{2L+2}
+    const double2 K = cdiv(w0, u2L);                      // w_0 / (1 - a^{2L+2})
+    const int y0 = lane * C;
+    if (y0 < L) {
+      // skip chunks where |phi| < 1e-18 throughout (|a^{y+2}| falls and |a^{2L+2-y}| rises along y)
+      const double2 a1 = make_double2(1.0 - u.x, -u.y);   // a as a value
+      const double la = 0.5 * log(cabs2(a1));             // log|a| < 0
+      const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));   // log(1e-18 |1-a^{2L+2}|)
+      const int ylast = min(y0 + C, L) - 1;
+      if ((y0 + 2) * la > thr || (2.0 * L + 2 - ylast) * la > thr) {
+        const double2 uP = upow(u, y0 + 2);               // a^{y0+2} = 1 - uP
+        const double2 uQ = upow(u, 2L * L + 2 - y0);      // a^{2L+2-y0}
+        double2 P = make_double2(1.0 - uP.x, -uP.y);
+        double2 Q = make_double2(1.0 - uQ.x, -uQ.y);
 #pragma unroll
-      for (int r = 0; r < C; ++r) {
-        d[r] = csub(d[r], cmul(K, csub(P, Q)));
-        P = cmul(P, a1);
-        Q = cmul(Q, rr);
+        for (int r = 0; r < C; ++r) {
+          d[r] = csub(d[r], cmul(K, csub(P, Q)));
+          P = cmul(P, a1);
+          Q = cmul(Q, rr);
+        }
       }
     }
-  }
 #pragma unroll
-  for (int r = 0; r < C; ++r) {
-    const int y = lane * C + r;
-    line[r] = (y < L) ? amul(u, d[r]) : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
+    for (int r = 0; r < C; ++r) {
+      const int y = lane * C + r;
+      line[r] = (y < L) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
 
-  for (int e = threadIdx.x; e < total; e += 32 * G) {
-    const int yb = e / (G * WB), rem = e % (G * WB), g = rem / WB, j = rem % WB;
-    const int y = yb * WB + j;
-    a.out[((q * NB + yb) * N + p0 + g) * WB + j] = (y < 32 * C) ? sm[g * SLINE + y + y / C] : make_double2(0.0, 0.0);
+    double2* out_base = a.out + (q * NB * N + p0) * WB;
+    for (int e = threadIdx.x; e < total; e += 32 * G) {
+      const int yb = e >> lgw, rem = e & gwm, g = rem >> lwb, j = rem & wbm;
+      const int y = (yb << lwb) + j;
+      out_base[((long)yb * N + g) * WB + j] = (y < 32 * C) ? sm[g * SLINE + y + y / C] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();   // smem reused by the next strip
   }
 }
 

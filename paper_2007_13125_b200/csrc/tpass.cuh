@@ -19,6 +19,10 @@
 
 namespace pint {
 
+#ifndef PINT_TPASS_MINB
+#define PINT_TPASS_MINB 2
+#endif
+
 enum { IN_FREQ = 0, IN_TIME_V = 1, IN_TIME_ZERO = 2, IN_TIME_BUF = 3 };
 enum { OUT_H = 0, OUT_U = 1 };
 
@@ -45,7 +49,12 @@ struct TPassArgs {
   const double2* thm;       // [N] -(h^2/(2 N tau^a)) theta^{-n}
   const double* gsfq;       // [N] kappa^{n/N} h^2/N (CQ static part)
   unsigned long long* upd;  // max |update| as ordered bits
+  int nmax;                 // max_s nhi[s]: F_static(n) == 0 for n >= nmax
 };
+
+__device__ __forceinline__ void prefetch_l2_t(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* dst) {
   __shared__ double red[TPB / 32];
@@ -64,6 +73,7 @@ __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* d
 // F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]
 __device__ __forceinline__ double2 static_rhs(const TPassArgs& a, long tile, int WB, int N, int n, int c, long ntiles) {
   double2 f = make_double2(0.0, 0.0);
+  if (n >= a.nmax) return f;
   for (int s = 0; s < a.S; ++s) {
     if (n < __ldg(&a.nhi[s])) {
       const double cf = __ldg(&a.coef[(long)s * N + n]);
@@ -75,19 +85,23 @@ __device__ __forceinline__ double2 static_rhs(const TPassArgs& a, long tile, int
 }
 
 template <int N, int MODE_IN, int MODE_OUT, bool CQ>
-__global__ void __launch_bounds__(TPB, CQ ? 2 : 3) tpass_kernel(const TPassArgs a, long ntiles) {
+__global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPassArgs a, long ntiles) {
   using TM = TimeMap<N>;
   using FM = FreqMap<N>;
   constexpr int WB = TILE / N;
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
-  const long tile = blockIdx.x;
-  const long base = tile * (long)TILE;
   const int k = a.k;
-  double2 v[16];
-  double2 dw[CQ ? 16 : 1];
   double upd = 0.0;
   bool nonfinite = false;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const long base = tile * (long)TILE;
+  if (MODE_IN == IN_FREQ || MODE_IN == IN_TIME_BUF) {
+    const long nt = tile + gridDim.x;
+    if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
+  }
+  double2 v[16];
+  double2 dw[CQ ? 16 : 1];
 
   // ---------------- input ----------------
   if constexpr (MODE_IN == IN_FREQ) {
@@ -135,7 +149,7 @@ __global__ void __launch_bounds__(TPB, CQ ? 2 : 3) tpass_kernel(const TPassArgs 
         const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[TM::n(j, s, tid)]));
         a.out[base + TM::e(j, s, tid)] = U;
       }
-    return;
+    continue;
   }
 
   __syncthreads();   // sm free: all readers of the last exchange are done
@@ -205,6 +219,8 @@ __global__ void __launch_bounds__(TPB, CQ ? 2 : 3) tpass_kernel(const TPassArgs 
 
 #pragma unroll
   for (int t = 0; t < 16; ++t) a.out[base + FM::e(t, tid)] = v[t];
+  __syncthreads();   // smem reused by the next tile
+  }  // tile loop
 
   if constexpr (MODE_IN == IN_FREQ) {
     // fmax drops NaN: report any non-finite update as +inf (orders above all finite bits)

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpint.so")
+LIB_PATH = os.environ.get("PINT_LIB", os.path.join(HERE, "libpint.so"))
 
 PINT_OK, PINT_ERR_ARG, PINT_ERR_ALLOC, PINT_ERR_CUDA, PINT_ERR_COMM, PINT_ERR_STATE, \
     PINT_ERR_NOT_CONVERGED, PINT_ERR_DIVERGED, PINT_ERR_UNSUPPORTED = range(9)

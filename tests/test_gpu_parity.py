@@ -147,7 +147,7 @@ def test_reading_does_not_perturb(pint):
 
 def test_device_arrays_and_levels(pint):
     import torch
-    prob = inputs.random_complex_problem(40, 30, 64, 3, 0.1, 1.0, R=2, seed=4)
+    prob = inputs.random_complex_problem(31, 30, 64, 3, 0.1, 1.0, R=2, seed=4)
     with pint.Plan.from_problem(prob, device_arrays=True) as p:
         p.iterate(); p.iterate()
         full = p.get_solution()
