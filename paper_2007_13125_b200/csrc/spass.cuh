@@ -87,18 +87,27 @@ __global__ void __launch_bounds__(32 * G, (C >= 32 ? 3 : 4)) spass_kernel(const 
     const long q = work / nblk;
     const long p0 = (work - q * nblk) * G;
     const double2* in_base = a.in + (q * NB * N + p0) * WB;
-    // prefetch the next strip's runs into L2 (NB runs of G*WB*16 bytes, stride N*WB*16)
-    const long nxt = work + gridDim.x;
-    if (nxt < a.nwork) {
-      const long qn = nxt / nblk, pn = (nxt - qn * nblk) * G;
-      const double2* nb = a.in + (qn * NB * N + pn) * WB;
-      for (long yb = threadIdx.x; yb < NB; yb += 32 * G) prefetch_l2(nb + yb * N * WB, G * WB * 16);
-    }
     // ---- stage the strip [NB][G][WB] into line-major padded smem (all copies in flight) ----
-    for (int e = threadIdx.x; e < total; e += 32 * G) {
-      const int yb = e >> lgw, rem = e & gwm, g = rem >> lwb, j = rem & wbm;
-      const int y = (yb << lwb) + j;
-      if (y < 32 * C) cp_async16(&sm[g * SLINE + y + y / C], in_base + ((long)yb * N + g) * WB + j);
+    // element e = tid + i*32G: (yb, g, j) = (e >> lgw, .., ..); y = yb*WB + j advances by 32 per
+    // i and y/C by 32/C, so both addresses are linear in i.
+    {
+      const int e0 = threadIdx.x;
+      const int yb0 = e0 >> lgw, rem = e0 & gwm, g = rem >> lwb, j = rem & wbm;
+      const int y0s = (yb0 << lwb) + j;
+      const double2* gp = in_base + ((long)yb0 * N + g) * WB + j;
+      double2* sp_ = sm + g * SLINE + y0s + y0s / C;
+      const long gstep = (long)(32 / WB) * N * WB;
+      const int nit = (total + 32 * G - 1) / (32 * G);
+      if (WB <= 32) {
+        for (int i = 0; i < nit; ++i)
+          if (e0 + i * 32 * G < total && y0s + 32 * i < 32 * C) cp_async16(sp_ + i * (32 + 32 / C), gp + i * gstep);
+      } else {
+        for (int e = threadIdx.x; e < total; e += 32 * G) {
+          const int yb = e >> lgw, rm = e & gwm, gg = rm >> lwb, jj = rm & wbm;
+          const int y = (yb << lwb) + jj;
+          if (y < 32 * C) cp_async16(&sm[gg * SLINE + y + y / C], in_base + ((long)yb * N + gg) * WB + jj);
+        }
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -207,11 +216,26 @@ __global__ void __launch_bounds__(32 * G, (C >= 32 ? 3 : 4)) spass_kernel(const 
     }
     __syncthreads();
 
-    double2* out_base = a.out + (q * NB * N + p0) * WB;
-    for (int e = threadIdx.x; e < total; e += 32 * G) {
-      const int yb = e >> lgw, rem = e & gwm, g = rem >> lwb, j = rem & wbm;
-      const int y = (yb << lwb) + j;
-      out_base[((long)yb * N + g) * WB + j] = (y < 32 * C) ? sm[g * SLINE + y + y / C] : make_double2(0.0, 0.0);
+    {
+      double2* out_base = a.out + (q * NB * N + p0) * WB;
+      const int e0 = threadIdx.x;
+      const int yb0 = e0 >> lgw, rem = e0 & gwm, g = rem >> lwb, j = rem & wbm;
+      const int y0s = (yb0 << lwb) + j;
+      double2* gp = out_base + ((long)yb0 * N + g) * WB + j;
+      const double2* sp_ = sm + g * SLINE + y0s + y0s / C;
+      const long gstep = (long)(32 / WB) * N * WB;
+      const int nit = (total + 32 * G - 1) / (32 * G);
+      if (WB <= 32) {
+        for (int i = 0; i < nit; ++i)
+          if (e0 + i * 32 * G < total)
+            gp[i * gstep] = (y0s + 32 * i < 32 * C) ? sp_[i * (32 + 32 / C)] : make_double2(0.0, 0.0);
+      } else {
+        for (int e = threadIdx.x; e < total; e += 32 * G) {
+          const int yb = e >> lgw, rm = e & gwm, gg = rm >> lwb, jj = rm & wbm;
+          const int y = (yb << lwb) + jj;
+          out_base[((long)yb * N + gg) * WB + jj] = (y < 32 * C) ? sm[gg * SLINE + y + y / C] : make_double2(0.0, 0.0);
+        }
+      }
     }
     __syncthreads();   // smem reused by the next strip
   }

@@ -92,6 +92,16 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
   const int k = a.k;
+  // twiddle table in shared memory (N <= 2048: 32 KB next to the 68 KB tile)
+  constexpr bool TW_SM = N <= 2048;
+  const double2* tw = a.tw;
+  if constexpr (TW_SM) {
+    double2* stw = sm + phys_size(TILE);
+    for (int i = tid; i < N; i += TPB) stw[i] = __ldg(&a.tw[i]);
+    __syncthreads();
+    tw = stw;
+  }
+  const bool dense = a.nmax > TM::PL;   // F_static nonzero beyond the first PL levels
   double upd = 0.0;
   bool nonfinite = false;
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
       for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
     }
-    run_passes<N, +1, false>(v, sm, a.tw, tid);        // u = V W  (unnormalised inverse DFT)
+    run_passes<N, +1, false>(v, sm, tw, tid);        // u = V W  (unnormalised inverse DFT)
   } else {
     // time-domain input U (registers in TimeMap)
 #pragma unroll
@@ -129,10 +139,10 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
       for (int j = 0; j < TM::NJ; ++j)
 #pragma unroll
         for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cscale(v[j * TM::RL + s], __ldg(&a.gsN[TM::n(j, s, tid)]));
-      run_passes<N, -1, true>(v, sm, a.tw, tid);
+      run_passes<N, -1, true>(v, sm, tw, tid);
 #pragma unroll
       for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
-      run_passes<N, +1, false>(v, sm, a.tw, tid);
+      run_passes<N, +1, false>(v, sm, tw, tid);
     }
     // heat time modes: v holds U itself (HAVE_U_DIRECT below)
   }
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
     for (int s = 0; s < TM::RL; ++s) {
       const int n = TM::n(j, s, tid);
-      if (n >= N - k) {
+      if ((s == TM::RL - 1 || TM::PL < 8) && n >= N - k) {
         const int r = j * TM::RL + s, c = TM::c(j, tid), jj = n - (N - k);
         const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[n]));
         const long wi = (tile * k + jj) * WB + c;
@@ -182,14 +192,18 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
         const int n = TM::n(j, s, tid), c = TM::c(j, tid);
-        double2 F = static_rhs(a, tile, WB, N, n, c, ntiles);
-        if (n < k) {
+        const int r = j * TM::RL + s;
+        // F_static is zero for n >= nmax; with nmax <= PL only s == 0 slots can be nonzero
+        const bool live = (s == 0) || dense || (TM::PL < 8);
+        double2 F = make_double2(0.0, 0.0);
+        if (live) F = static_rhs(a, tile, WB, N, n, c, ntiles);
+        if ((s == 0 || TM::PL < 8) && n < k) {
           // (kappa/tau) sum_{j=n+1}^{k} omega_j U_m^{N+n-j} (0-based levels), window index k+n-j
           for (int jw = n + 1; jw <= k; ++jw) F = cfmar(sW[(k + n - jw) * WB + c], __ldg(&a.wk[jw]), F);
         }
-        v[j * TM::RL + s] = cscale(F, __ldg(&a.gsf[n]));
+        v[r] = live ? cscale(F, __ldg(&a.gsf[n])) : F;
       }
-    run_passes<N, -1, true>(v, sm, a.tw, tid);   // H = (h^2/N) FFT(Gamma F)
+    run_passes<N, -1, true>(v, sm, tw, tid);   // H = (h^2/N) FFT(Gamma F)
   } else {
     // ---------------- CQ ----------------
     // z = V^{-1} Theta u
@@ -197,11 +211,11 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
     for (int j = 0; j < TM::NJ; ++j)
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cmul(v[j * TM::RL + s], __ldg(&a.thp[TM::n(j, s, tid)]));
-    run_passes<N, -1, true>(v, sm, a.tw, tid);
+    run_passes<N, -1, true>(v, sm, tw, tid);
     // s = V (D' z)
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[FM::p(t, tid)]));
-    run_passes<N, +1, false>(v, sm, a.tw, tid);
+    run_passes<N, +1, false>(v, sm, tw, tid);
     // X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s
 #pragma unroll
     for (int j = 0; j < TM::NJ; ++j)
@@ -212,7 +226,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
         const int r = j * TM::RL + s;
         v[r] = cfmar(F, __ldg(&a.gsfq[n]), cmul(v[r], __ldg(&a.thm[n])));
       }
-    run_passes<N, -1, true>(v, sm, a.tw, tid);
+    run_passes<N, -1, true>(v, sm, tw, tid);
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = cadd(v[t], dw[t]);
   }
