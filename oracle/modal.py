@@ -83,8 +83,11 @@ def modal_wr(prob, basis: ModalBasis, v_coef, g_coef, iters: int):
             if b != 0 and prob.R:
                 row = row + float(b) * tau ** l * (prob.dphi[:, l - 1] @ mp.g)
         fb[n - 1] = row
-    w = bdf.time_weights(k, prob.alpha, N)
-    psum = np.cumsum(w)[:N]
+    if prob.alpha == 1.0:    # exact: zero for n > k
+        bw = bdf.bdf_weights(k)
+        psum = np.array([float(sum(bw[:min(n, k + 1)])) for n in range(1, N + 1)])
+    else:
+        psum = np.cumsum(bdf.time_weights(k, prob.alpha, N))[:N]
     F_static = fb + (tau ** -prob.alpha) * psum[:, None] * mp.v[None, :]
     op = wr.Operator(mp, diag=lam)
     return wr.wr_naive(mp, iters, op=op, F_static=F_static)

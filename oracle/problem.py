@@ -43,6 +43,11 @@ def static_rhs(prob) -> np.ndarray:
     """F_static_n = f̄_n + tau^{-alpha} (sum_{j=0}^{n-1} omega_j) v, n = 1..N
     (PAPER.md:411-414 eqn:BDF-k-F last term; PAPER.md:1025-1027 eq:BDF-subdiff-F last term).
     Heat: the partial sums vanish for n > k because sum_j omega_j = 0."""
-    w = bdf.time_weights(prob.k, prob.alpha, prob.N)
-    psum = np.cumsum(w)[:prob.N]          # psum[n-1] = sum_{j=0}^{n-1} omega_j
+    if prob.alpha == 1.0:
+        # exact rational partial sums: zero for n > k (sum_j omega_j = 0, PAPER.md:429-430)
+        w = bdf.bdf_weights(prob.k)
+        psum = np.array([float(sum(w[:min(n, prob.k + 1)])) for n in range(1, prob.N + 1)])
+    else:
+        w = bdf.time_weights(prob.k, prob.alpha, prob.N)
+        psum = np.cumsum(w)[:prob.N]      # psum[n-1] = sum_{j=0}^{n-1} omega_j
     return fbar(prob) + (prob.tau ** -prob.alpha) * psum[:, None] * prob.v[None, :]

@@ -134,7 +134,7 @@ __device__ __forceinline__ void butterfly_pass(double2 (&v)[16], const double2* 
       const int b = tid + j * TPB, i = b / WB, k = i % P;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
-        double2 w = tw[t * k * (N / (P * R))];   // shared (T-pass) or global (DST) table
+        double2 w = __ldg(&tw[t * k * (N / (P * R))]);   // global table, L1-resident
         if (DIR > 0) w.y = -w.y;
         v[j * R + t] = cmul(v[j * R + t], w);
       }

@@ -12,7 +12,7 @@ namespace pint {
 template <int MI, int MO, bool CQ>
 static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
   auto kern = tpass_kernel<PINT_N, MI, MO, CQ>;
-  const int smem = (phys_size(TILE) + (PINT_N <= 2048 ? PINT_N : 0)) * (int)sizeof(double2);
+  const int smem = phys_size(TILE) * (int)sizeof(double2);
   static long resident = 0;   // persistent grid: SMs x resident CTAs per SM
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

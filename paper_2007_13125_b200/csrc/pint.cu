@@ -461,6 +461,8 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
   ld ps = 0.0L;
   for (int64_t n = 1; n <= N; ++n) {
     ps += w[n - 1];
+    // heat: sum_{j<n} omega_j vanishes exactly for n > k; keep it exact
+    if (p->alpha == 1.0 && n > k) ps = 0.0L;
     coef[0 * N + n - 1] = (double)(ta * ps);
     coef[1 * N + n - 1] = (double)(-table1_a(k, (int)n));
     for (int r = 0; r < R; ++r) {

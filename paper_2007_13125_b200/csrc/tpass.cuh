@@ -70,17 +70,12 @@ __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* d
   }
 }
 
-// F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]
-__device__ __forceinline__ double2 static_rhs(const TPassArgs& a, long tile, int WB, int N, int n, int c, long ntiles) {
+// F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]; zero for n >= nmax.
+// srcp = src + tile*WB + c, sstride = ntiles*WB (one spatial vector per source).
+__device__ __forceinline__ double2 static_rhs(const TPassArgs& a, const double2* srcp, long sstride, int N, int n) {
   double2 f = make_double2(0.0, 0.0);
   if (n >= a.nmax) return f;
-  for (int s = 0; s < a.S; ++s) {
-    if (n < __ldg(&a.nhi[s])) {
-      const double cf = __ldg(&a.coef[(long)s * N + n]);
-      const double2 g = __ldg(&a.src[((long)s * ntiles + tile) * WB + c]);
-      f = cfmar(g, cf, f);
-    }
-  }
+  for (int s = 0; s < a.S; ++s) f = cfmar(__ldg(&srcp[s * sstride]), __ldg(&a.coef[(long)s * N + n]), f);
   return f;
 }
 
@@ -92,15 +87,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
   const int k = a.k;
-  // twiddle table in shared memory (N <= 2048: 32 KB next to the 68 KB tile)
-  constexpr bool TW_SM = N <= 2048;
   const double2* tw = a.tw;
-  if constexpr (TW_SM) {
-    double2* stw = sm + phys_size(TILE);
-    for (int i = tid; i < N; i += TPB) stw[i] = __ldg(&a.tw[i]);
-    __syncthreads();
-    tw = stw;
-  }
   const bool dense = a.nmax > TM::PL;   // F_static nonzero beyond the first PL levels
   double upd = 0.0;
   bool nonfinite = false;
@@ -196,7 +183,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
         // F_static is zero for n >= nmax; with nmax <= PL only s == 0 slots can be nonzero
         const bool live = (s == 0) || dense || (TM::PL < 8);
         double2 F = make_double2(0.0, 0.0);
-        if (live) F = static_rhs(a, tile, WB, N, n, c, ntiles);
+        if (live) F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n);
         if ((s == 0 || TM::PL < 8) && n < k) {
           // (kappa/tau) sum_{j=n+1}^{k} omega_j U_m^{N+n-j} (0-based levels), window index k+n-j
           for (int jw = n + 1; jw <= k; ++jw) F = cfmar(sW[(k + n - jw) * WB + c], __ldg(&a.wk[jw]), F);
@@ -222,7 +209,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
         const int n = TM::n(j, s, tid), c = TM::c(j, tid);
-        const double2 F = static_rhs(a, tile, WB, N, n, c, ntiles);
+        const double2 F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n);
         const int r = j * TM::RL + s;
         v[r] = cfmar(F, __ldg(&a.gsfq[n]), cmul(v[r], __ldg(&a.thm[n])));
       }
