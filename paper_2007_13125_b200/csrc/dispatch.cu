@@ -2,6 +2,7 @@
 #define PINT_DEFINE_PLAIN_KERNELS
 #include "kernels.h"
 #include <algorithm>
+#include <cstdlib>
 
 namespace pint {
 
@@ -65,7 +66,29 @@ static cudaError_t spass_go(const SPassArgs& a, long Qb, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int C>
+static cudaError_t spass_direct_go(const SPassArgs& a, long Qb, cudaStream_t st) {
+  SPassArgs b = a;
+  int lwb = 0;
+  while ((1 << lwb) < a.WB) ++lwb;
+  b.lwb = lwb;
+  b.nwork = Qb * a.N;                        // lines
+  const long grid = (b.nwork + 3) / 4;
+  spass_direct_kernel<C><<<(unsigned)grid, 128, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
+  static const bool staged = getenv("PINT_SPASS_STAGED") != nullptr;   // A/B switch for profiling
+  if (!staged && a.WB >= 2 && C >= 2) {
+    switch (C) {
+      case 2: return spass_direct_go<2>(a, Qb, st);
+      case 4: return spass_direct_go<4>(a, Qb, st);
+      case 8: return spass_direct_go<8>(a, Qb, st);
+      case 16: return spass_direct_go<16>(a, Qb, st);
+      case 32: return spass_direct_go<32>(a, Qb, st);
+    }
+  }
   switch (C) {
     case 1: return spass_go<1>(a, Qb, st);
     case 2: return spass_go<2>(a, Qb, st);

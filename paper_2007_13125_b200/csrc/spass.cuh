@@ -241,4 +241,136 @@ __global__ void __launch_bounds__(32 * G, (C >= 32 ? 3 : 4)) spass_kernel(const 
   }
 }
 
+
+// ---- direct variant (WB >= 2, C even): each lane moves its row pairs (y, y+1) as one full
+// 32-byte sector with 256-bit loads/stores straight between HBM and registers.  No shared
+// memory and no barriers: warps desynchronise freely, and a lane issues all C/2 loads at once.
+__device__ __forceinline__ void ld256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void st256(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+
+template <int C>
+__device__ __forceinline__ void solve_line_regs(double2 (&d)[C], double2 sig, int L, int lane) {
+  const double2 s = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
+  const double2 t1 = cscale(cadd(sig, s), 0.5), t2 = cscale(csub(sig, s), 0.5);
+  const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
+  const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);          // tb * ts = -sigma
+  const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
+  const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
+  const double2 rr = make_double2(1.0 + tt.x, tt.y);                  // r = 1/a, |r| > 1
+  const double2 u = cdiv(tt, rr);                                     // u = 1 - a
+  double2 uc[5];
+  uc[0] = u;
+#pragma unroll
+  for (int c = 1; c < C; c <<= 1) uc[0] = uprod(uc[0], uc[0]);        // a^C (C power of two)
+#pragma unroll
+  for (int i = 1; i < 5; ++i) uc[i] = uprod(uc[i - 1], uc[i - 1]);
+  const int nv = min(max(L - lane * C, 0), C);                         // valid rows of this lane
+
+  double2 f = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int o = 1 << i;
+    double2 x;
+    x.x = __shfl_up_sync(0xffffffffu, f.x, o);
+    x.y = __shfl_up_sync(0xffffffffu, f.y, o);
+    if (lane >= o) f = cadd(f, amul(uc[i], x));
+  }
+  double2 carry;
+  carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
+  carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
+  if (lane == 0) carry = make_double2(0.0, 0.0);
+  f = carry;
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    f = cadd(d[r], amul(u, f));
+    d[r] = (r < nv) ? f : make_double2(0.0, 0.0);
+  }
+  double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int o = 1 << i;
+    double2 x;
+    x.x = __shfl_down_sync(0xffffffffu, w.x, o);
+    x.y = __shfl_down_sync(0xffffffffu, w.y, o);
+    if (lane + o < 32) w = cadd(w, amul(uc[i], x));
+  }
+  carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
+  carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
+  if (lane == 31) carry = make_double2(0.0, 0.0);
+  w = carry;
+#pragma unroll
+  for (int r = C - 1; r >= 0; --r) {
+    w = cadd(d[r], amul(u, w));
+    d[r] = w;
+  }
+  // rank-1 Dirichlet correction x = a (w - w_0 phi), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2})
+  double2 w0;
+  w0.x = __shfl_sync(0xffffffffu, d[0].x, 0);
+  w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
+  const double2 u2L = upow(u, 2L * L + 2);
+  const double2 K = cdiv(w0, u2L);
+  const int y0 = lane * C;
+  if (nv > 0) {
+    const double2 a1 = make_double2(1.0 - u.x, -u.y);
+    const double la = 0.5 * log(cabs2(a1));                           // log|a| < 0
+    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));    // log(1e-18 |1 - a^{2L+2}|)
+    const bool needP = (y0 + 2) * la > thr;                             // |a^{y+2}| largest at y0
+    const bool needQ = (2.0 * L + 2 - (y0 + nv - 1)) * la > thr;        // |a^{2L+2-y}| largest at the chunk end
+    if (needP) {
+      const double2 uP = upow(u, y0 + 2);
+      double2 KP = cmul(K, make_double2(1.0 - uP.x, -uP.y));          // K a^{y+2}
+#pragma unroll
+      for (int r = 0; r < C; ++r) { d[r] = csub(d[r], KP); KP = cmul(KP, a1); }
+    }
+    if (needQ) {
+      const double2 uQ = upow(u, 2L * L + 2 - y0);
+      double2 KQ = cmul(K, make_double2(1.0 - uQ.x, -uQ.y));          // K a^{2L+2-y}
+#pragma unroll
+      for (int r = 0; r < C; ++r) { d[r] = cadd(d[r], KQ); KQ = cmul(KQ, rr); }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < C; ++r) d[r] = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+}
+
+template <int C>
+__global__ void __launch_bounds__(128, 3) spass_direct_kernel(const SPassArgs a) {
+  static_assert(C % 2 == 0, "row pairs");
+  const int lane = threadIdx.x % 32;
+  const long line = (long)blockIdx.x * 4 + threadIdx.x / 32;         // line = q * N + p
+  const long N = a.N, NB = a.NB;
+  if (line >= (long)a.nwork) return;
+  const long q = line / N, p = line - q * N;
+  const int WB = a.WB, lwb = a.lwb, L = a.L;
+  const int Lpad = (int)NB * WB;
+  const double2* in = a.in + (q * NB * N + p) * WB;
+  double2* out = a.out + (q * NB * N + p) * WB;
+  double2 d[C];
+#pragma unroll
+  for (int r = 0; r < C; r += 2) {
+    const int y = lane * C + r;
+    if (y < Lpad) ld256(in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+    else { d[r] = make_double2(0.0, 0.0); d[r + 1] = d[r]; }
+  }
+  const double2 sp = __ldg(&a.sig_p[p]);
+  const double2 sig = make_double2(sp.x + __ldg(&a.sig_q[q]), sp.y);
+  const int nv = min(max(L - lane * C, 0), C);
+#pragma unroll
+  for (int r = 0; r < C; ++r) if (r >= nv) d[r] = make_double2(0.0, 0.0);
+  solve_line_regs<C>(d, sig, L, lane);
+#pragma unroll
+  for (int r = 0; r < C; r += 2) {
+    const int y = lane * C + r;
+    if (y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+  }
+}
+
 }  // namespace pint
