@@ -129,6 +129,11 @@ pint_status pint_get_solution(pint_plan plan, void* U, int32_t mem);
 pint_status pint_get_modal_levels(pint_plan plan, int64_t n_begin, int64_t n_count, void* Uq, int32_t mem);
 pint_status pint_modal_to_physical(pint_plan plan, int64_t n_count, const void* Uq_full, void* U, int32_t mem);
 
+/* Host-only (no CUDA call): the contiguous, balanced x-mode slab of `rank` among `nranks`
+ * for mx modes: [floor(rank*mx/nranks), floor((rank+1)*mx/nranks)).  PINT_ERR_ARG if
+ * nranks < 1, rank outside [0, nranks) or nranks > mx. */
+pint_status pint_partition(int64_t mx, int32_t rank, int32_t nranks, int64_t* q_begin, int64_t* q_end);
+
 /* This rank's x-mode slab [q_begin, q_end) (1D: [0, 1)). */
 pint_status pint_get_partition(pint_plan plan, int64_t* q_begin, int64_t* q_end);
 

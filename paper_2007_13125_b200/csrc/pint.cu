@@ -178,6 +178,8 @@ static void free_plan(pint_plan p) {
   delete p;
 }
 
+extern "C" pint_status pint_partition(int64_t mx, int32_t rank, int32_t nranks, int64_t* q_begin, int64_t* q_end);
+
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 
 extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double kappa, double tau,
@@ -219,8 +221,10 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   p->allreduce = opt ? opt->allreduce_max : nullptr; p->actx = opt ? opt->allreduce_ctx : nullptr;
   p->L = L; p->h = 1.0 / (double)(L + 1); p->NE = NE;
   if (dim == 2) {
-    p->q0 = (rank * op->mx) / nranks;
-    p->Qb = ((rank + 1) * op->mx) / nranks - p->q0;
+    int64_t qb = 0, qe = 0;
+    pint_partition(op->mx, rank, nranks, &qb, &qe);
+    p->q0 = qb;
+    p->Qb = qe - qb;
   } else {
     p->q0 = 0; p->Qb = 1;
   }
@@ -674,6 +678,14 @@ extern "C" pint_status pint_modal_to_physical(pint_plan p, int64_t n_count, cons
   ++p->launches;
   if (mem == PINT_HOST) CUDA_TRY(cudaMemcpyAsync(U, stage_out, bytes, cudaMemcpyDeviceToHost, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return PINT_OK;
+}
+
+extern "C" pint_status pint_partition(int64_t mx, int32_t rank, int32_t nranks, int64_t* q_begin, int64_t* q_end) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || mx < 1 || nranks > mx)
+    return fail(PINT_ERR_ARG, "need 1 <= nranks <= mx and 0 <= rank < nranks");
+  if (q_begin) *q_begin = (rank * mx) / nranks;
+  if (q_end) *q_end = ((rank + 1) * mx) / nranks;
   return PINT_OK;
 }
 

@@ -23,7 +23,7 @@ PINT_FLAG_U0_ZERO = 1
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
     "pint_wr_solve", "pint_get_levels", "pint_get_solution", "pint_get_modal_levels",
-    "pint_modal_to_physical", "pint_get_partition", "pint_set_timing", "pint_get_timing",
+    "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
     "pint_kappa_log_rule",
 ]
@@ -65,6 +65,7 @@ def lib(path: str = LIB_PATH):
         "pint_get_solution": [P, VP, I32],
         "pint_get_modal_levels": [P, I64, I64, VP, I32],
         "pint_modal_to_physical": [P, I64, VP, VP, I32],
+        "pint_partition": [I64, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)],
         "pint_get_partition": [P, ctypes.POINTER(I64), ctypes.POINTER(I64)],
         "pint_set_timing": [P, I32],
         "pint_get_timing": [P, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(I64), ctypes.POINTER(I64)],
@@ -111,6 +112,13 @@ def _ptr(x):
     if hasattr(x, "data_ptr"):
         return _ptr(x.numpy())
     raise TypeError(f"unsupported array type {type(x)}")
+
+
+def partition(mx: int, rank: int, nranks: int) -> tuple[int, int]:
+    """Host-only x-mode slab of `rank` (pint_partition)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().pint_partition(mx, rank, nranks, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def kappa_log_rule(N: int) -> float:

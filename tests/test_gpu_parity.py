@@ -177,3 +177,31 @@ def test_state_errors_and_timing(pint):
         assert t["tpass_ms"] > 0 and t["spass_ms"] > 0
         it, u, st = p.solve(0.0, 2, raise_on_fail=False)
         assert st == P.PINT_ERR_NOT_CONVERGED and it == 2
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_xmode_slabs_reproduce_single_plan(pint, nranks):
+    """The multi-GPU partition on one GPU: each x-mode slab plan iterates independently (the WR
+    iteration has no inter-slab exchange), the gathered modal slabs map back to the single-plan
+    physical solution (bitwise up to the DST ordering: checked to 1e-14)."""
+    from paper_2007_13125_b200 import dist as pdist
+    prob = inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=12)
+    with pint.Plan.from_problem(prob) as p:
+        for _ in range(3):
+            p.iterate()
+        ref = p.get_solution()
+    slabs, bounds, plans = [], [], []
+    for r in range(nranks):
+        pl = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha,
+                       rank=r, nranks=nranks, allreduce_max=lambda x: x)
+        pl.set_problem(prob.v, prob.g, prob.phi, prob.dphi)
+        for _ in range(3):
+            pl.iterate()
+        slabs.append(pl.get_modal_levels(0, prob.N))
+        bounds.append(pl.partition())
+        plans.append(pl)
+    full = pdist.assemble_modal(slabs, bounds, prob.mx)
+    phys = plans[0].modal_to_physical(np.ascontiguousarray(full))
+    for pl in plans:
+        pl.close()
+    assert rel(phys, ref) < 1e-14
