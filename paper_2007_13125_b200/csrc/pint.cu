@@ -680,517 +680,14 @@ extern "C" pint_status pint_modal_to_physical(pint_plan p, int64_t n_count, cons
     CUDA_TRY(cudaMalloc(&stage, 2 * bytes));
     tmp = true;
   }
-  CUDA_TRY(cudaMemcpyAsync(stage, Uq_full, bytes, cudaMemcpyHostToDevice, p->stream));
+  cudaError_t e = cudaMemcpyAsync(stage, Uq_full, bytes, cudaMemcpyHostToDevice, p->stream);
   a.in = stage; a.out = stage + elems;
-  cudaError_t e = launch_dst(p->NE, a, DST_ROWS, p->stream);
+  if (e == cudaSuccess) e = launch_dst(p->NE, a, DST_ROWS, p->stream);
   ++p->launches;
   if (e == cudaSuccess) e = cudaMemcpyAsync(U, stage + elems, bytes, cudaMemcpyDeviceToHost, p->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   if (tmp) cudaFree(stage);
   if (e != cudaSuccess) return fail(PINT_ERR_CUDA, std::string("modal_to_physical: ") + cudaGetErrorString(e));
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_partition(int64_t mx, int32_t rank, int32_t nranks, int64_t* q_begin, int64_t* q_end);
-
-static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
-
-extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double kappa, double tau,
-                                        const pint_operator* op, const pint_options* opt, pint_plan* out) {
-  if (!out) return fail(PINT_ERR_ARG, "out must not be NULL");
-  *out = nullptr;
-  if (!op) return fail(PINT_ERR_ARG, "op must not be NULL");
-  if (k < 1 || k > 6) return fail(PINT_ERR_ARG, "k must be in 1..6 (BDFk, PAPER.md:278), got " + std::to_string(k));
-  if (!(kappa > 0.0 && kappa < 1.0)) return fail(PINT_ERR_ARG, "kappa must be in (0,1)");
-  if (!(tau > 0.0) || !std::isfinite(tau)) return fail(PINT_ERR_ARG, "tau must be > 0");
-  if (N < k + 1) return fail(PINT_ERR_ARG, "N must be >= k+1 (DESIGN.md reading R-Nk)");
-  const double alpha = opt ? opt->alpha : 1.0;
-  if (!(alpha > 0.0 && alpha <= 1.0)) return fail(PINT_ERR_ARG, "alpha must be in (0,1]");
-  if (op->kind != PINT_OP_FD1D_DIRICHLET && op->kind != PINT_OP_FD2D_DIRICHLET)
-    return fail(PINT_ERR_ARG, "op->kind must be PINT_OP_FD1D_DIRICHLET or PINT_OP_FD2D_DIRICHLET");
-  if (op->mx < 1 || op->my < 1) return fail(PINT_ERR_ARG, "op->mx, op->my must be >= 1");
-  if (op->kind == PINT_OP_FD1D_DIRICHLET && op->my != 1) return fail(PINT_ERR_ARG, "1D operator needs my == 1");
-  if (op->mx * op->my != M) return fail(PINT_ERR_ARG, "M must equal mx*my");
-  const int rank = opt ? opt->rank : 0, nranks = opt ? opt->nranks : 1;
-  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PINT_ERR_ARG, "need 0 <= rank < nranks");
-  if (nranks > 1 && op->kind == PINT_OP_FD1D_DIRICHLET)
-    return fail(PINT_ERR_ARG, "1D operators do not shard (replicas only): nranks must be 1");
-  if (nranks > op->mx) return fail(PINT_ERR_ARG, "nranks must be <= mx");
-  if (nranks > 1 && !(opt && opt->allreduce_max)) return fail(PINT_ERR_ARG, "nranks > 1 needs allreduce_max");
-  if (!is_pow2(N) || N < 16 || N > 4096) return fail(PINT_ERR_UNSUPPORTED, "N must be a power of two in [16, 4096]");
-  const int dim = op->kind == PINT_OP_FD1D_DIRICHLET ? 1 : 2;
-  const int64_t L = dim == 1 ? op->mx : op->my;
-  if (L > 1024) return fail(PINT_ERR_UNSUPPORTED, "line length (1D: mx, 2D: my) must be <= 1024");
-  int NE = 0;
-  if (dim == 2) {
-    NE = (int)(2 * (op->mx + 1));
-    if (!is_pow2(NE) || NE < 16 || NE > 4096) return fail(PINT_ERR_UNSUPPORTED, "2D needs 2(mx+1) a power of two in [16, 4096]");
-  }
-
-  pint_plan p = new pint_plan_s();
-  p->M = M; p->N = N; p->mx = op->mx; p->my = op->my; p->k = k; p->dim = dim;
-  p->flags = opt ? opt->flags : 0; p->rank = rank; p->nranks = nranks;
-  p->kappa = kappa; p->tau = tau; p->alpha = alpha;
-  p->allreduce = opt ? opt->allreduce_max : nullptr; p->actx = opt ? opt->allreduce_ctx : nullptr;
-  p->L = L; p->h = 1.0 / (double)(L + 1); p->NE = NE;
-  if (dim == 2) {
-    int64_t qb = 0, qe = 0;
-    pint_partition(op->mx, rank, nranks, &qb, &qe);
-    p->q0 = qb;
-    p->Qb = qe - qb;
-  } else {
-    p->q0 = 0; p->Qb = 1;
-  }
-  p->WB = (int)(TILE / N);
-  p->NB = (L + p->WB - 1) / p->WB;
-  p->ntiles = p->Qb * p->NB;
-  int C = 1;
-  while (32 * C < L) C *= 2;
-  p->C = C;
-  p->device = opt ? opt->device : 0;
-
-  auto bail = [&](pint_status s) { free_plan(p); return s; };
-  cudaError_t ce = cudaSetDevice(p->device);
-  if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce)); }
-  if (opt && opt->stream) {
-    p->stream = (cudaStream_t)opt->stream;
-    p->own_stream = false;
-  } else {
-    ce = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
-    if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(ce)); }
-    p->own_stream = true;
-  }
-
-  const size_t arr = (size_t)p->ntiles * TILE;
-  pint_status st;
-  if ((st = dalloc(p, &p->A, arr)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->B, arr)) != PINT_OK) return bail(st);
-  for (int i = 0; i < 2; ++i)
-    if ((st = dalloc(p, &p->wrap[i], (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->tw, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->gsf, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->igs, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->gsN, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->wk, k + 1)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->dh, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->dpr, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->thp, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->thm, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->sig_p, N)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->sig_q, p->Qb)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->upd, 1)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->phys, 2 * (size_t)M)) != PINT_OK) return bail(st);
-  if (dim == 2 && (st = dalloc(p, &p->twE, NE)) != PINT_OK) return bail(st);
-  ce = cudaMemsetAsync(p->A, 0, arr * sizeof(double2), p->stream);
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(p->B, 0, arr * sizeof(double2), p->stream);
-  if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
-
-  // ---- tables ----
-  const ld kap = kappa, taul = tau, al = alpha, hl = 1.0L / (ld)(L + 1), Nl = (ld)N;
-  const ld ta = powl(taul, -al);                      // tau^{-alpha}
-  std::vector<ld> w = (alpha == 1.0) ? bdf_weights(k) : cq_weights(k, al, N + 1);
-  if (alpha == 1.0) w.resize(N + 1, 0.0L);
-  std::vector<double2> tw(N), thp(N), thm(N), dh(N), dpr(N), sigp(N);
-  std::vector<double> gsf(N), igs(N), gsN(N), wk(k + 1), sigq(p->Qb);
-  for (int64_t n = 0; n < N; ++n) {
-    const ld ang = 2.0L * PI_L * (ld)n / Nl;
-    tw[n] = make_double2((double)cosl(ang), (double)-sinl(ang));
-    const ld g = powl(kap, (ld)n / Nl);                // Gamma_kappa = diag(kappa^{(n-1)/N}), 1-based n
-    gsf[n] = (double)(g * hl * hl / Nl);
-    igs[n] = (double)(1.0L / g);
-    gsN[n] = (double)(g / Nl);
-    const ld th = PI_L * (ld)n / Nl;                   // theta^n = e^{i pi n/N}
-    thp[n] = d2(cld(cosl(th), sinl(th)) / Nl);
-    thm[n] = d2(cld(cosl(th), -sinl(th)) * (-(hl * hl) * ta / (2.0L * Nl)));
-  }
-  for (int j = 0; j <= k; ++j) wk[j] = (double)(kap / taul * w[j]);
-  // eigenvalues: d_p = sum_j omega_j kappa^{j/N} e^{-2 pi i j p/N}  (Lemma 2.3 / 3.2; CQ:
-  // truncated column, reading R-CQeig); d'_p: same for C(-kappa) with (-kappa)^{j/N} = kappa^{j/N} theta^j
-  const int64_t jmax = (alpha == 1.0) ? k : N - 1;
-  std::vector<ld> cj(jmax + 1);
-  for (int64_t j = 0; j <= jmax; ++j) cj[j] = w[j] * powl(kap, (ld)j / Nl);
-  std::vector<cld> e2(2 * N);                         // e^{-i pi m/N}, m < 2N
-  for (int64_t m = 0; m < 2 * N; ++m) e2[m] = cld(cosl(PI_L * (ld)m / Nl), -sinl(PI_L * (ld)m / Nl));
-  for (int64_t pp = 0; pp < N; ++pp) {
-    cld d = 0.0L, dq = 0.0L;
-    for (int64_t j = 0; j <= jmax; ++j) {
-      d += cj[j] * e2[(2 * j * pp) % (2 * N)];
-      dq += cj[j] * e2[(j * (2 * pp - 1) % (2 * N) + 2 * N) % (2 * N)];
-    }
-    sigp[pp] = d2(d * ta * hl * hl);
-    dh[pp] = d2(d * (hl * hl) * ta / 2.0L);
-    dpr[pp] = d2(dq);
-  }
-  for (int64_t ql = 0; ql < p->Qb; ++ql) {
-    if (dim == 1) { sigq[ql] = 0.0; continue; }
-    const ld hx = 1.0L / (ld)(p->mx + 1);
-    const ld sn = sinl((ld)(p->q0 + ql + 1) * PI_L * hx / 2.0L);
-    sigq[ql] = (double)(hl * hl * 4.0L / (hx * hx) * sn * sn);   // h_y^2 lambda_q
-  }
-  if ((st = h2d(p, p->tw, tw)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->gsf, gsf)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->igs, igs)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->gsN, gsN)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->wk, wk)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->dh, dh)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->dpr, dpr)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->thp, thp)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->thm, thm)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
-  if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
-  if (dim == 2) {
-    std::vector<double2> twE(NE);
-    for (int m = 0; m < NE; ++m) {
-      const ld ang = 2.0L * PI_L * (ld)m / (ld)NE;
-      twE[m] = make_double2((double)cosl(ang), (double)-sinl(ang));
-    }
-    if ((st = h2d(p, p->twE, twE)) != PINT_OK) return bail(st);
-  }
-  *out = p;
-  return PINT_OK;
-}
-
-// ------------------------------------------------------------------------------------------
-// launches
-// ------------------------------------------------------------------------------------------
-static TPassArgs targs(pint_plan p) {
-  TPassArgs a{};
-  a.src = p->src; a.coef = p->coef; a.nhi = p->nhi; a.S = p->S;
-  a.vsrc = p->src;   // source 0 is v
-  a.tw = p->tw; a.gsf = p->gsf; a.igs = p->igs; a.gsN = p->gsN; a.wk = p->wk; a.k = p->k;
-  a.dh = p->dh; a.dpr = p->dpr; a.thp = p->thp; a.thm = p->thm; a.gsfq = p->gsf;
-  a.upd = p->upd;
-  a.nmax = p->nmax;
-  return a;
-}
-
-static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* in, double2* out,
-                         const double2* wold, double2* wnew, bool timed) {
-  TPassArgs a = targs(p);
-  a.in = in; a.out = out; a.wrap_old = wold; a.wrap_new = wnew;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timed && p->timing) {
-    CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
-    CUDA_TRY(cudaEventRecord(e0, p->stream));
-  }
-  CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
-  ++p->launches;
-  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->tev.push_back({e0, e1}); }
-  return PINT_OK;
-}
-
-static pint_status spass(pint_plan p, const double2* in, double2* out) {
-  SPassArgs a{};
-  a.in = in; a.out = out; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
-  a.N = p->N; a.NB = p->NB; a.WB = p->WB; a.L = (int)p->L;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (p->timing) {
-    CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
-    CUDA_TRY(cudaEventRecord(e0, p->stream));
-  }
-  CUDA_TRY(launch_spass(p->C, a, p->Qb, p->stream));
-  ++p->launches;
-  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
-  return PINT_OK;
-}
-
-static DstArgs dargs(pint_plan p) {
-  DstArgs a{};
-  a.mx = (int)p->mx; a.my = (int)p->my; a.WB = p->WB; a.NB = p->NB; a.N = p->N;
-  a.q0 = p->q0; a.Qb = p->Qb; a.n0 = 0; a.M = p->M;
-  a.scale = (double)sqrtl(2.0L / (ld)(p->mx + 1));
-  a.tw = p->twE;
-  return a;
-}
-
-// physical vector [M] (device) -> source slot s (tile layout [ntiles][WB]; DST-x in 2D)
-static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
-  double2* dst = p->src + (size_t)s * p->ntiles * p->WB;
-  if (p->dim == 1) {
-    CUDA_TRY(cudaMemcpyAsync(dst, phys_vec, p->M * sizeof(double2), cudaMemcpyDeviceToDevice, p->stream));
-    return PINT_OK;
-  }
-  DstArgs a = dargs(p);
-  a.in = phys_vec; a.out = dst; a.rows = p->my;
-  CUDA_TRY(launch_dst(p->NE, a, DST_PHYS_TO_SRC, p->stream));
-  ++p->launches;
-  return PINT_OK;
-}
-
-// ------------------------------------------------------------------------------------------
-// problem setup
-// ------------------------------------------------------------------------------------------
-static pint_status bootstrap(pint_plan p) {
-  // U_0^n = v (default) or 0 (PINT_FLAG_U0_ZERO): A = H_1, wrap = last-k of U_0
-  const int mi = (p->flags & PINT_FLAG_U0_ZERO) ? IN_TIME_ZERO : IN_TIME_V;
-  TRY(tpass(p, mi, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur], false));
-  p->stateA = 0;
-  p->m = 0;
-  p->last_upd = -1.0;
-  p->increases = 0;
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, int32_t R, const void* g,
-                                                  const double* phi, const double* dphi, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!v) return fail(PINT_ERR_ARG, "v must not be NULL");
-  if (R < 0 || R > 64) return fail(PINT_ERR_ARG, "R must be in 0..64");
-  if (R > 0 && (!g || !phi)) return fail(PINT_ERR_ARG, "R > 0 needs g and phi");
-  if (R > 0 && p->k > 2 && !dphi) return fail(PINT_ERR_ARG, "k > 2 with R > 0 needs dphi (d^l phi/dt^l(0), l=1..k-2)");
-  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
-  CUDA_TRY(cudaSetDevice(p->device));
-  const int64_t M = p->M, N = p->N;
-  const int k = p->k;
-  const cudaMemcpyKind kind = mem == PINT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-
-  // sources: 0 = v, 1 = A v, 2.. = g_r
-  const int S = 2 + R;
-  if (p->S != S) {
-    if (p->src) return fail(PINT_ERR_STATE, "set_problem may be called again only with the same R");
-    TRY(dalloc(p, &p->src, (size_t)S * p->ntiles * p->WB));
-    TRY(dalloc(p, &p->coef, (size_t)S * N));
-    TRY(dalloc(p, &p->nhi, S));
-    p->S = S;
-  }
-  CUDA_TRY(cudaMemsetAsync(p->src, 0, (size_t)S * p->ntiles * p->WB * sizeof(double2), p->stream));
-  CUDA_TRY(cudaMemcpyAsync(p->phys, v, M * sizeof(double2), kind, p->stream));
-  const double ihx2 = (double)((ld)(p->mx + 1) * (ld)(p->mx + 1));
-  const double ihy2 = (double)((ld)(p->my + 1) * (ld)(p->my + 1));
-  CUDA_TRY(launch_stencil(p->phys, p->phys + M, (int)p->mx, (int)p->my, ihx2, ihy2, p->stream));
-  ++p->launches;
-  TRY(to_source(p, p->phys, 0));
-  TRY(to_source(p, p->phys + M, 1));
-  for (int r = 0; r < R; ++r) {
-    CUDA_TRY(cudaMemcpyAsync(p->phys, (const double2*)g + (size_t)r * M, M * sizeof(double2), kind, p->stream));
-    TRY(to_source(p, p->phys, 2 + r));
-  }
-
-  // time coefficients of F_static_n = f̄_n + tau^-a (sum_{j<n} omega_j) v, 1-based n = row+1:
-  //   v   : tau^{-a} sum_{j=0}^{n-1} omega_j
-  //   A v : -a_n                                         (a_n (f(0) - A v))
-  //   g_r : phi_r(t_n) + a_n phi_r(0) + sum_l b_{l,n} tau^l phi_r^{(l)}(0)
-  const ld ta = powl((ld)p->tau, -(ld)p->alpha);
-  std::vector<ld> w = (p->alpha == 1.0) ? bdf_weights(k) : cq_weights(k, (ld)p->alpha, N + 1);
-  w.resize(N + 1, 0.0L);
-  std::vector<double> coef((size_t)S * N, 0.0);
-  std::vector<int> nhi(S, 0);
-  ld ps = 0.0L;
-  for (int64_t n = 1; n <= N; ++n) {
-    ps += w[n - 1];
-    // heat: sum_{j<n} omega_j vanishes exactly for n > k; keep it exact
-    if (p->alpha == 1.0 && n > k) ps = 0.0L;
-    coef[0 * N + n - 1] = (double)(ta * ps);
-    coef[1 * N + n - 1] = (double)(-table1_a(k, (int)n));
-    for (int r = 0; r < R; ++r) {
-      ld c = (ld)phi[(size_t)r * (N + 1) + n];
-      if (n < k) {
-        c += table1_a(k, (int)n) * (ld)phi[(size_t)r * (N + 1)];
-        for (int l = 1; l <= k - 2; ++l)
-          c += table1_b(k, l, (int)n) * powl((ld)p->tau, (ld)l) * (ld)dphi[(size_t)r * (k - 2) + (l - 1)];
-      }
-      coef[(size_t)(2 + r) * N + n - 1] = (double)c;
-    }
-  }
-  for (int s = 0; s < S; ++s)
-    for (int64_t n = 0; n < N; ++n)
-      if (coef[(size_t)s * N + n] != 0.0) nhi[s] = (int)(n + 1);
-  p->nmax = *std::max_element(nhi.begin(), nhi.end());
-  TRY(h2d(p, p->coef, coef));
-  TRY(h2d(p, p->nhi, nhi));
-  p->problem_set = true;
-  p->wcur = 0;
-  TRY(bootstrap(p));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
-  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
-  CUDA_TRY(cudaSetDevice(p->device));
-  if (!U0) return bootstrap(p);
-  if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "user initial guess with nranks > 1");
-  const size_t bytes = (size_t)p->N * p->M * sizeof(double2);
-  CUDA_TRY(cudaMemcpyAsync(p->B, U0, bytes, mem == PINT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, p->stream));
-  if (p->dim == 1) {
-    RemapArgs r{};
-    r.in = p->B; r.out = p->A; r.count = p->N * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
-    r.N = p->N; r.n0 = 0; r.M = p->M; r.Qb = 1;
-    CUDA_TRY(launch_remap(r, RM_1D_LEVELS_TO_INT, p->stream));
-  } else {
-    DstArgs a = dargs(p);
-    a.in = p->B; a.out = p->A; a.rows = p->N * p->my; a.n0 = 0;
-    CUDA_TRY(launch_dst(p->NE, a, DST_PHYS_LEVELS_TO_INT, p->stream));
-  }
-  ++p->launches;
-  // H_1 and the wrap state of U_0 from the time-domain array
-  TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
-  p->stateA = 0;
-  p->m = 0;
-  p->last_upd = -1.0;
-  p->increases = 0;
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return PINT_OK;
-}
-
-// ------------------------------------------------------------------------------------------
-// iteration
-// ------------------------------------------------------------------------------------------
-static pint_status iterate_async(pint_plan p) {
-  if (p->stateA == 1) {   // A holds U_m (after get_levels): re-derive H_{m+1}
-    TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
-    p->stateA = 0;
-  }
-  CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
-  TRY(spass(p, p->A, p->B));                                             // W_{m+1} = solve(H_{m+1})
-  TRY(tpass(p, IN_FREQ, OUT_H, p->B, p->A, p->wrap[p->wcur], p->wrap[1 - p->wcur], true));  // -> H_{m+2}
-  p->wcur ^= 1;
-  ++p->m;
-  return PINT_OK;
-}
-
-static pint_status read_update(pint_plan p, double* out) {
-  unsigned long long bits = 0;
-  CUDA_TRY(cudaMemcpyAsync(&bits, p->upd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  double u;
-  std::memcpy(&u, &bits, sizeof(u));
-  if (p->nranks > 1) {
-    if (p->allreduce(&u, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
-  }
-  *out = u;
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_wr_iterate(pint_plan p, double* update_inf) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
-  CUDA_TRY(cudaSetDevice(p->device));
-  TRY(iterate_async(p));
-  double u;
-  TRY(read_update(p, &u));
-  if (update_inf) *update_inf = u;
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters, int32_t* iters, double* update_inf) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
-  if (!(tol >= 0.0) || max_iters < 0) return fail(PINT_ERR_ARG, "need tol >= 0 and max_iters >= 0");
-  CUDA_TRY(cudaSetDevice(p->device));
-  int it = 0;
-  double u = INFINITY;
-  pint_status result = PINT_ERR_NOT_CONVERGED;
-  while (it < max_iters) {
-    TRY(iterate_async(p));
-    TRY(read_update(p, &u));
-    ++it;
-    if (!std::isfinite(u)) { result = PINT_ERR_DIVERGED; g_last_error = "update is not finite"; break; }
-    if (p->last_upd >= 0.0 && u > p->last_upd) {
-      if (++p->increases >= 3) { result = PINT_ERR_DIVERGED; g_last_error = "update grew 3 consecutive times"; p->last_upd = u; break; }
-    } else {
-      p->increases = 0;
-    }
-    p->last_upd = u;
-    if (u < tol) { result = PINT_OK; break; }
-  }
-  if (result == PINT_ERR_NOT_CONVERGED) g_last_error = "max_iters reached before update < tol";
-  if (iters) *iters = it;
-  if (update_inf) *update_inf = u;
-  return result;
-}
-
-// ------------------------------------------------------------------------------------------
-// output
-// ------------------------------------------------------------------------------------------
-static pint_status materialize(pint_plan p) {
-  if (p->stateA == 1) return PINT_OK;
-  // U_m = Gamma^{-1} V W_m (Step 3) from B into A (time domain)
-  TRY(tpass(p, IN_FREQ, OUT_U, p->B, p->A, nullptr, nullptr, false));
-  p->stateA = 1;
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_count, void* U, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
-  if (n_begin < 0 || n_count < 0 || n_begin + n_count > p->N) return fail(PINT_ERR_ARG, "levels out of range [0, N)");
-  if (!U && n_count > 0) return fail(PINT_ERR_ARG, "U must not be NULL");
-  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
-  if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "nranks > 1: use pint_get_modal_levels + pint_modal_to_physical");
-  CUDA_TRY(cudaSetDevice(p->device));
-  if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  TRY(materialize(p));
-  if (n_count == 0) return PINT_OK;
-  double2* dst = mem == PINT_DEVICE ? (double2*)U : p->B;   // B is free once U_m is in A
-  if (p->dim == 1) {
-    RemapArgs r{};
-    r.in = p->A; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
-    r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = 1;
-    CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
-  } else {
-    DstArgs a = dargs(p);
-    a.in = p->A; a.out = dst; a.rows = n_count * p->my; a.n0 = n_begin;
-    CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
-  }
-  ++p->launches;
-  if (mem == PINT_HOST)
-    CUDA_TRY(cudaMemcpyAsync(U, dst, n_count * p->M * sizeof(double2), cudaMemcpyDeviceToHost, p->stream));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_get_solution(pint_plan p, void* U, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  return pint_get_levels(p, 0, p->N, U, mem);
-}
-
-extern "C" pint_status pint_get_modal_levels(pint_plan p, int64_t n_begin, int64_t n_count, void* Uq, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
-  if (p->dim != 2) return fail(PINT_ERR_ARG, "modal levels exist for 2D operators only");
-  if (n_begin < 0 || n_count < 0 || n_begin + n_count > p->N) return fail(PINT_ERR_ARG, "levels out of range [0, N)");
-  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
-  if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  CUDA_TRY(cudaSetDevice(p->device));
-  TRY(materialize(p));
-  double2* dst = mem == PINT_DEVICE ? (double2*)Uq : p->B;
-  RemapArgs r{};
-  r.in = p->A; r.out = dst; r.count = n_count * p->my * p->Qb; r.WB = p->WB; r.my = (int)p->my;
-  r.NB = p->NB; r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = p->Qb;
-  CUDA_TRY(launch_remap(r, RM_INT_TO_MODAL, p->stream));
-  ++p->launches;
-  if (mem == PINT_HOST)
-    CUDA_TRY(cudaMemcpyAsync(Uq, dst, r.count * sizeof(double2), cudaMemcpyDeviceToHost, p->stream));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return PINT_OK;
-}
-
-extern "C" pint_status pint_modal_to_physical(pint_plan p, int64_t n_count, const void* Uq_full, void* U, int32_t mem) {
-  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
-  if (p->dim != 2) return fail(PINT_ERR_ARG, "2D operators only");
-  if (n_count < 0 || !Uq_full || !U) return fail(PINT_ERR_ARG, "bad n_count or NULL buffers");
-  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
-  if ((size_t)n_count * p->M > (size_t)p->ntiles * TILE / 2)
-    return fail(PINT_ERR_ARG, "n_count too large for the plan's staging buffer");
-  CUDA_TRY(cudaSetDevice(p->device));
-  TRY(materialize(p));   // B becomes scratch
-  const size_t bytes = (size_t)n_count * p->M * sizeof(double2);
-  const double2* in = (const double2*)Uq_full;
-  double2* stage_in = p->B;
-  double2* stage_out = p->B + (size_t)n_count * p->M;
-  if (mem == PINT_HOST) {
-    CUDA_TRY(cudaMemcpyAsync(stage_in, Uq_full, bytes, cudaMemcpyHostToDevice, p->stream));
-    in = stage_in;
-  }
-  DstArgs a = dargs(p);
-  a.in = in; a.out = mem == PINT_DEVICE ? (double2*)U : stage_out; a.rows = n_count * p->my;
-  CUDA_TRY(launch_dst(p->NE, a, DST_ROWS, p->stream));
-  ++p->launches;
-  if (mem == PINT_HOST) CUDA_TRY(cudaMemcpyAsync(U, stage_out, bytes, cudaMemcpyDeviceToHost, p->stream));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
   return PINT_OK;
 }
 
