@@ -59,7 +59,9 @@ typedef enum {
 enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2 };
 enum { PINT_HOST = 0, PINT_DEVICE = 1 };
 enum {
-  PINT_FLAG_U0_ZERO = 1        /* WR initial guess U_0 = 0 instead of U_0^n = v */
+  PINT_FLAG_U0_ZERO = 1,       /* WR initial guess U_0 = 0 instead of U_0^n = v */
+  PINT_FLAG_FULL_FFT = 2       /* heat: run the unpruned time FFTs every iteration (A/B, tests);
+                                  default prunes to the k window outputs / n_k nonzero inputs */
 };
 
 typedef struct {

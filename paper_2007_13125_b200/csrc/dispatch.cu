@@ -21,6 +21,16 @@ cudaError_t launch_tpass(int N, int mi, int mo, bool cq, const TPassArgs& a, lon
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  switch (N) {
+    case 512: return launch_tpass_pruned_512(a, ntiles, st);
+    case 1024: return launch_tpass_pruned_1024(a, ntiles, st);
+    case 2048: return launch_tpass_pruned_2048(a, ntiles, st);
+    case 4096: return launch_tpass_pruned_4096(a, ntiles, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st) {
   switch (NE) {
     case 16: return launch_dst_16(a, mode, st);

@@ -29,6 +29,31 @@ static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntiles, cudaStream_t st) {
+#if PINT_N >= 512
+  auto kern = tpass_heat_pruned_kernel<PINT_N>;
+  constexpr int WBp = TILE / PINT_N;
+  const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N / 256) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
+  static long resident = 0;
+  if (!resident) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
+    resident = (long)nsm * (per > 0 ? per : 1);
+  }
+  if (ntiles <= 0) return cudaSuccess;
+  const long grid = ntiles < resident ? ntiles : resident;
+  kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
+  return cudaGetLastError();
+#else
+  (void)a; (void)ntiles; (void)st;
+  return cudaErrorInvalidValue;
+#endif
+}
+
 cudaError_t PINT_CAT(launch_tpass_, PINT_N)(int mi, int mo, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st) {
   if (mo == OUT_U) return go<IN_FREQ, OUT_U, false>(a, ntiles, st);
   if (!cq) {

@@ -11,6 +11,8 @@ namespace pint {
 cudaError_t launch_tpass(int N, int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st);
 // S-pass: chunk C = ceil(L/32) rounded up to a power of two (1..32), G lines per CTA.
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st);
+// pruned heat T-pass (FREQ -> H), N in {512, 1024, 2048, 4096}
+cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st);
 // layout remaps and the FD stencil (dispatch.cu)
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);
@@ -20,7 +22,8 @@ cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st);
 #define PINT_DECLARE_N(NN)                                                                         \
   cudaError_t launch_tpass_##NN(int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, \
                                 cudaStream_t st);                                                  \
-  cudaError_t launch_dst_##NN(const DstArgs& a, int mode, cudaStream_t st);
+  cudaError_t launch_dst_##NN(const DstArgs& a, int mode, cudaStream_t st);                    \
+  cudaError_t launch_tpass_pruned_##NN(const TPassArgs& a, long ntiles, cudaStream_t st);
 PINT_DECLARE_N(16)
 PINT_DECLARE_N(32)
 PINT_DECLARE_N(64)

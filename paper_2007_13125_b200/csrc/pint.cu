@@ -360,7 +360,10 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
+  const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 512 &&
+                      std::max(p->k, p->nmax) <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT);
+  if (pruned) CUDA_TRY(launch_tpass_pruned((int)p->N, a, p->ntiles, p->stream));
+  else CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->tev.push_back({e0, e1}); }
   return PINT_OK;

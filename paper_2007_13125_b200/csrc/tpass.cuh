@@ -19,6 +19,9 @@
 
 namespace pint {
 
+#ifndef PINT_PRUNED_MINB
+#define PINT_PRUNED_MINB 3
+#endif
 #ifndef PINT_TPASS_MINB
 #define PINT_TPASS_MINB 2
 #endif
@@ -228,6 +231,124 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
     if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
     block_max_atomic(upd, a.upd);
   }
+}
+
+}  // namespace pint
+
+namespace pint {
+
+// ---------------------------------------------------------------------------------------------
+// Pruned-FFT T-pass for heat (alpha = 1), mode FREQ -> H, N >= 512 (schedule 16.16.RL, PL = 256).
+// The next iterate needs only the k window levels n in [N-k, N) of U_m, and
+// X = Gamma F vanishes for n >= nk = max(k, nmax) <= 16.  Standard FFT pruning on the same
+// Stockham passes (index maps derived in DESIGN.md "Pruned T-pass"):
+//   inverse: pass 0 (radix 16, P = 1) in full, keeping the k outputs s0 in [16-k, 16) the window
+//            needs; pass 1 only for the 16k butterflies (per tile) feeding the window, output
+//            s1 = 15 only; pass 2 only the k window outputs (s2 = RL-1).
+//   forward: with X supported on n < 16, passes 0 and 1 are broadcasts and pass 2 sees inputs
+//            X_0..X_15: H_{i + (N/16) s} = DFT16_s( X_t w_N^{t i} ).
+// ---------------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kernel(const TPassArgs a, long ntiles) {
+  static_assert(N >= 512 && N <= 4096, "3-pass schedule");
+  constexpr int WB = TILE / N;
+  constexpr int NB16 = N / 16;          // radix-16 butterflies per column
+  constexpr int RL = N / 256;
+  constexpr int NBLK = N / 256;         // pass-1 blocks per column
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const int k = a.k;
+  const int nk = max(k, a.nmax);        // X_n = 0 for n >= nk (host guarantees nk <= 16)
+  // pass-0 outputs s0 >= 16-k, slot (c, i0, j = s0-16+k): c*(9 NB16 + 1) + 9 i0 + j (k <= 8;
+  // stride 9 and the +1 column skew keep the 16-byte stores/loads bank-conflict free)
+  double2* Y0 = sm;
+  double2* Y1 = Y0 + WB * (9 * NB16 + 1);             // [WB][NBLK][16]  pass-1 window outputs
+  double2* sW = Y1 + WB * NBLK * 16;                  // [k][WB]        window of U_m
+  double2* Xs = sW + 16 * WB;                         // [WB][16]       X_0..X_15
+  const double2* tw = a.tw;
+  double upd = 0.0;
+  bool nonfinite = false;
+  const int i0 = tid / WB, c0 = tid % WB;             // FreqMap butterfly of this thread
+
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long base = tile * (long)TILE;
+    {
+      const long nt = tile + gridDim.x;
+      if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
+    }
+    // ---- inverse pass 0: DFT16 of W[i0 + (N/16) t], keep outputs s0 >= 16-k ----
+    double2 v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = a.in[base + tid + t * TPB];
+    dft16<+1>(v);
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+      if (s >= 16 - k) Y0[c0 * (9 * NB16 + 1) + 9 * i0 + s - (16 - k)] = v[s];
+    __syncthreads();
+    // ---- inverse pass 1 (window butterflies only): i1 = 16 b + k1, k1 in [16-k, 16), output s1 = 15
+    if (tid < 16 * k) {
+      const int kk = tid % k, b = (tid / k) % NBLK, c = tid / (k * NBLK);
+      const int k1 = 16 - k + kk;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t1 = 0; t1 < 16; ++t1) {
+        // input y0[i1 + (N/16) t1]: pass-0 butterfly b + NBLK t1, output k1
+        const double2 x = Y0[c * (9 * NB16 + 1) + 9 * (b + NBLK * t1) + kk];
+        double2 w = __ldg(&tw[((t1 * (k1 + 240)) & 255) * (N / 256)]);
+        w.y = -w.y;                                    // inverse: e^{+2 pi i m / 256}
+        acc = cfma(x, w, acc);
+      }
+      Y1[(c * NBLK + b) * 16 + kk] = acc;
+    }
+    __syncthreads();
+    // ---- inverse pass 2 (window outputs only): level n = N-k+j ----
+    if (tid < WB * k) {
+      const int j = tid % k, c = tid / k;
+      const int i2 = 256 - k + j;
+      double2 u = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t2 = 0; t2 < RL; ++t2) {
+        double2 w = __ldg(&tw[(t2 * (i2 + 256 * (RL - 1))) & (N - 1)]);
+        w.y = -w.y;
+        u = cfma(Y1[(c * NBLK + t2) * 16 + j], w, u);
+      }
+      const int n = N - k + j;
+      const double2 U = cscale(u, __ldg(&a.igs[n]));
+      const long wi = (tile * k + j) * WB + c;
+      const double2 o = a.wrap_old[wi];
+      const double d = sqrt(cabs2(csub(U, o)));
+      if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+      upd = fmax(upd, d);
+      a.wrap_new[wi] = U;
+      sW[j * WB + c] = U;
+    }
+    __syncthreads();
+    // ---- X_t = Gamma_t h^2/N (F_static(t) + wrap_t), t < 16 (zero for t >= nk) ----
+    if (tid < 16 * WB) {
+      const int t = tid % 16, c = tid / 16;
+      double2 F = make_double2(0.0, 0.0);
+      if (t < nk) {
+        F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, t);
+        for (int jw = t + 1; jw <= k; ++jw) F = cfmar(sW[(k + t - jw) * WB + c], __ldg(&a.wk[jw]), F);
+        F = cscale(F, __ldg(&a.gsf[t]));
+      }
+      Xs[c * 16 + t] = F;
+    }
+    __syncthreads();
+    // ---- forward pass 2 with inputs X_t: H[i0 + (N/16) s] ----
+    v[0] = Xs[c0 * 16];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      if (t < nk) v[t] = cmul(Xs[c0 * 16 + t], __ldg(&tw[t * i0]));   // w_N^{t i0}, forward
+      else v[t] = make_double2(0.0, 0.0);
+    }
+    dft16<-1>(v);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) a.out[base + tid + s * TPB] = v[s];
+    __syncthreads();   // Xs / Y0 reused by the next tile
+  }
+  if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
+  block_max_atomic(upd, a.upd);
 }
 
 }  // namespace pint

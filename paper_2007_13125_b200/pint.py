@@ -19,6 +19,7 @@ PINT_OK, PINT_ERR_ARG, PINT_ERR_ALLOC, PINT_ERR_CUDA, PINT_ERR_COMM, PINT_ERR_ST
 PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET = 1, 2
 PINT_HOST, PINT_DEVICE = 0, 1
 PINT_FLAG_U0_ZERO = 1
+PINT_FLAG_FULL_FFT = 2
 
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
@@ -130,7 +131,7 @@ class Plan:
 
     def __init__(self, mx: int, my: int, N: int, k: int, kappa: float, tau: float, alpha: float = 1.0,
                  device: int = 0, stream: int | None = None, u0_zero: bool = False,
-                 rank: int = 0, nranks: int = 1, allreduce_max=None):
+                 rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False):
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
         self.M = self.mx * self.my
@@ -144,7 +145,8 @@ class Plan:
                 except Exception:   # noqa: BLE001 - reported through PINT_ERR_COMM
                     return 1
             self._cb = ALLREDUCE_FN(_cb)
-        opt = pint_options(alpha, device, stream or 0, PINT_FLAG_U0_ZERO if u0_zero else 0, rank, nranks,
+        flags = (PINT_FLAG_U0_ZERO if u0_zero else 0) | (PINT_FLAG_FULL_FFT if full_fft else 0)
+        opt = pint_options(alpha, device, stream or 0, flags, rank, nranks,
                            self._cb, None)
         h = ctypes.c_void_p()
         _check(L.pint_plan_create(self.M, N, k, kappa, tau, ctypes.byref(op), ctypes.byref(opt), ctypes.byref(h)))

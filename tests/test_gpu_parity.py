@@ -205,3 +205,22 @@ def test_xmode_slabs_reproduce_single_plan(pint, nranks):
     for pl in plans:
         pl.close()
     assert rel(phys, ref) < 1e-14
+
+
+@pytest.mark.parametrize("N,k,mx,my", [(512, 1, 100, 1), (1024, 3, 63, 20), (2048, 6, 127, 1),
+                                       (4096, 2, 31, 9), (2048, 4, 15, 33)])
+def test_pruned_tpass_matches_full_fft_and_oracle(pint, N, k, mx, my):
+    """Heat with f = 0: the pruned-FFT T-pass (default) vs the unpruned FFT T-pass
+    (PINT_FLAG_FULL_FFT) vs the oracle, m = 1..3."""
+    prob = inputs.random_complex_problem(mx, my, N, k, 0.02, 1.0, R=0, seed=N + k)
+    res = {}
+    for full in (False, True):
+        with pint.Plan.from_problem(prob, full_fft=full) as p:
+            res[full] = []
+            for _ in range(3):
+                p.iterate()
+                res[full].append(p.get_solution())
+    o = wr.wr_naive(prob, 3, dft="fft")
+    for m in range(3):
+        assert rel(res[False][m], res[True][m]) < 1e-13
+        assert rel(res[False][m], o[m + 1]) < TOL
