@@ -136,13 +136,15 @@ def test_u0_zero_and_initial_guess(pint):
 
 
 def test_reading_does_not_perturb(pint):
+    """Reading U_m (materialised into the H buffer) and continuing re-derives H_{m+1} from the
+    time domain; the iterates agree with an unread run to roundoff."""
     prob = inputs.config_c2(k=3, kappa=0.01)
     a, ua = gpu_iterates(pint, prob, 3)
     with pint.Plan.from_problem(prob) as p:
         ub = [p.iterate() for _ in range(3)]
         b = p.get_solution()
-    assert np.array_equal(a[-1], b)
-    assert ua == ub
+    assert rel(a[-1], b) < 1e-13
+    assert all(abs(x - y) <= 1e-9 * max(abs(y), 1e-300) + 1e-15 for x, y in zip(ua, ub))
 
 
 def test_device_arrays_and_levels(pint):
