@@ -144,7 +144,7 @@ def test_reading_does_not_perturb(pint):
         ub = [p.iterate() for _ in range(3)]
         b = p.get_solution()
     assert rel(a[-1], b) < 1e-13
-    assert all(abs(x - y) <= 1e-9 * max(abs(y), 1e-300) + 1e-15 for x, y in zip(ua, ub))
+    assert all(abs(x - y) <= 1e-12 * ua[0] for x, y in zip(ua, ub))
 
 
 def test_device_arrays_and_levels(pint):
