@@ -10,6 +10,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -348,6 +349,8 @@ static TPassArgs targs(pint_plan p) {
   a.dh = p->dh; a.dpr = p->dpr; a.thp = p->thp; a.thm = p->thm; a.gsfq = p->gsf;
   a.upd = p->upd;
   a.nmax = p->nmax;
+  static const bool nopf = getenv("PINT_NO_PREFETCH") != nullptr;   // A/B switch (profiling)
+  a.prefetch = nopf ? 0 : 1;
   return a;
 }
 

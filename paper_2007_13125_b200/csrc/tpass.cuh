@@ -53,6 +53,7 @@ struct TPassArgs {
   const double* gsfq;       // [N] kappa^{n/N} h^2/N (CQ static part)
   unsigned long long* upd;  // max |update| as ordered bits
   int nmax;                 // max_s nhi[s]: F_static(n) == 0 for n >= nmax
+  int prefetch;             // 1: bulk-prefetch the next tile into L2
 };
 
 __device__ __forceinline__ void prefetch_l2_t(const void* p, unsigned bytes) {
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
   bool nonfinite = false;
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   const long base = tile * (long)TILE;
-  if (MODE_IN == IN_FREQ || MODE_IN == IN_TIME_BUF) {
+  if ((MODE_IN == IN_FREQ || MODE_IN == IN_TIME_BUF) && a.prefetch) {
     const long nt = tile + gridDim.x;
     if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
   }
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
 
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long base = tile * (long)TILE;
-    {
+    if (a.prefetch) {
       const long nt = tile + gridDim.x;
       if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
     }
@@ -301,35 +302,36 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
       Y1[(c * NBLK + b) * 16 + kk] = acc;
     }
     __syncthreads();
-    // ---- inverse pass 2 (window outputs only): level n = N-k+j ----
-    if (tid < WB * k) {
-      const int j = tid % k, c = tid / k;
-      const int i2 = 256 - k + j;
-      double2 u = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int t2 = 0; t2 < RL; ++t2) {
-        double2 w = __ldg(&tw[(t2 * (i2 + 256 * (RL - 1))) & (N - 1)]);
-        w.y = -w.y;
-        u = cfma(Y1[(c * NBLK + t2) * 16 + j], w, u);
-      }
-      const int n = N - k + j;
-      const double2 U = cscale(u, __ldg(&a.igs[n]));
-      const long wi = (tile * k + j) * WB + c;
-      const double2 o = a.wrap_old[wi];
-      const double d = sqrt(cabs2(csub(U, o)));
-      if (!(d <= 1.7976931348623157e308)) nonfinite = true;
-      upd = fmax(upd, d);
-      a.wrap_new[wi] = U;
-      sW[j * WB + c] = U;
-    }
-    __syncthreads();
-    // ---- X_t = Gamma_t h^2/N (F_static(t) + wrap_t), t < 16 (zero for t >= nk) ----
+    // ---- inverse pass 2 (window outputs, level n = N-k+j) fused with X_t, t < 16 ----
+    // thread (c, t): X_t needs U^{N+t-jw} for jw = t+1..k, i.e. window entries j = k+t-jw; it
+    // recomputes those from Y1 (RL terms each).  Threads t < k also own window entry j = t for
+    // the monitor and the wrap state.
     if (tid < 16 * WB) {
       const int t = tid % 16, c = tid / 16;
+      auto window = [&](int j) {   // U^{N-k+j} of column c
+        const int i2 = 256 - k + j;
+        double2 u = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t2 = 0; t2 < RL; ++t2) {
+          double2 w = __ldg(&tw[(t2 * (i2 + 256 * (RL - 1))) & (N - 1)]);
+          w.y = -w.y;
+          u = cfma(Y1[(c * NBLK + t2) * 16 + j], w, u);
+        }
+        return cscale(u, __ldg(&a.igs[N - k + j]));
+      };
+      if (t < k) {
+        const double2 U = window(t);
+        const long wi = (tile * k + t) * WB + c;
+        const double2 o = a.wrap_old[wi];
+        const double d = sqrt(cabs2(csub(U, o)));
+        if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+        upd = fmax(upd, d);
+        a.wrap_new[wi] = U;
+      }
       double2 F = make_double2(0.0, 0.0);
       if (t < nk) {
         F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, t);
-        for (int jw = t + 1; jw <= k; ++jw) F = cfmar(sW[(k + t - jw) * WB + c], __ldg(&a.wk[jw]), F);
+        for (int jw = t + 1; jw <= k; ++jw) F = cfmar(window(k + t - jw), __ldg(&a.wk[jw]), F);
         F = cscale(F, __ldg(&a.gsf[t]));
       }
       Xs[c * 16 + t] = F;
