@@ -373,4 +373,52 @@ __global__ void __launch_bounds__(128, 3) spass_direct_kernel(const SPassArgs a)
   }
 }
 
+// ---- pipelined variant (WB >= 2): persistent warps, one line at a time per warp; the NEXT
+// line is copied HBM -> the warp's own padded smem buffer with cp.async while the current line
+// is solved in registers, then stored with 256-bit sector stores.  Only __syncwarp is used.
+template <int C>
+__global__ void __launch_bounds__(128, 3) spass_pipe_kernel(const SPassArgs a) {
+  extern __shared__ double2 sm[];
+  constexpr int SL = 32 * (C + 1);                   // per-warp buffer, row y at y + y/C
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  double2* buf = sm + warp * SL;
+  const long N = a.N, NB = a.NB;
+  const int WB = a.WB, lwb = a.lwb, L = a.L;
+  const int Lpad = (int)NB * WB;
+  const long nlines = a.nwork;
+  const long stride = (long)gridDim.x * 4;
+  long line = (long)blockIdx.x * 4 + warp;
+  auto issue = [&](long ln) {                        // cp.async all rows of line ln into buf
+    const long q = ln / N, p = ln - q * N;
+    const double2* in = a.in + (q * NB * N + p) * WB;
+#pragma unroll 4
+    for (int i = 0; i < C; ++i) {
+      const int y = 32 * i + lane;
+      if (y < Lpad) cp_async16(&buf[y + y / C], in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)));
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (line < nlines) issue(line);
+  for (; line < nlines; line += stride) {
+    const long q = line / N, p = line - q * N;
+    const double2 sp = __ldg(&a.sig_p[p]);
+    const double2 sig = make_double2(sp.x + __ldg(&a.sig_q[q]), sp.y);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    double2 d[C];
+    const int nv = min(max(L - lane * C, 0), C);
+#pragma unroll
+    for (int r = 0; r < C; ++r) d[r] = (r < nv) ? buf[lane * (C + 1) + r] : make_double2(0.0, 0.0);
+    __syncwarp();                                    // buffer free: start the next line's copy
+    if (line + stride < nlines) issue(line + stride);
+    solve_line_regs<C>(d, sig, L, lane);
+    double2* out = a.out + (q * NB * N + p) * WB;
+#pragma unroll
+    for (int r = 0; r < C; r += 2) {
+      const int y = lane * C + r;
+      if (y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+    }
+  }
+}
+
 }  // namespace pint

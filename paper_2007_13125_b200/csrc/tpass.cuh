@@ -273,10 +273,7 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
 
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long base = tile * (long)TILE;
-    if (a.prefetch) {
-      const long nt = tile + gridDim.x;
-      if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
-    }
+    // (no L2 prefetch here: measured to evict and re-read ~45% of the tiles at this speed)
     // ---- inverse pass 0: DFT16 of W[i0 + (N/16) t], keep outputs s0 >= 16-k ----
     double2 v[16];
 #pragma unroll
