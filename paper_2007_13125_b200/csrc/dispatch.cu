@@ -89,39 +89,27 @@ static cudaError_t spass_direct_go(const SPassArgs& a, long Qb, cudaStream_t st)
 }
 
 template <int C>
-static cudaError_t spass_pipe_go(const SPassArgs& a, long Qb, cudaStream_t st) {
-  auto kern = spass_pipe_kernel<C>;
+static cudaError_t spass_pair_go(const SPassArgs& a, long Qb, cudaStream_t st) {
   SPassArgs b = a;
   int lwb = 0;
   while ((1 << lwb) < a.WB) ++lwb;
   b.lwb = lwb;
-  b.nwork = Qb * a.N;
-  const int smem = 4 * 32 * (C + 1) * (int)sizeof(double2);
-  static long resident = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 148, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
-    resident = (long)nsm * std::max(per, 1);
-  }
-  const long grid = std::min<long>((b.nwork + 3) / 4, resident);
-  kern<<<(unsigned)grid, 128, smem, st>>>(b);
+  b.nwork = Qb * a.N;                        // lines, 2 per CTA
+  const long grid = (b.nwork + 1) / 2;
+  spass_pair_kernel<C><<<(unsigned)grid, 128, 0, st>>>(b);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
   static const bool staged = getenv("PINT_SPASS_STAGED") != nullptr;   // A/B switches for profiling
   static const bool direct = getenv("PINT_SPASS_DIRECT") != nullptr;
-  if (!staged && !direct && a.WB >= 2 && C >= 2) {
+  // two warps per line (C/2 rows per lane) when the line needs C >= 4 rows per lane
+  if (!staged && !direct && a.WB >= 2 && C >= 4) {
     switch (C) {
-      case 2: return spass_pipe_go<2>(a, Qb, st);
-      case 4: return spass_pipe_go<4>(a, Qb, st);
-      case 8: return spass_pipe_go<8>(a, Qb, st);
-      case 16: return spass_pipe_go<16>(a, Qb, st);
-      case 32: return spass_pipe_go<32>(a, Qb, st);
+      case 4: return spass_pair_go<2>(a, Qb, st);
+      case 8: return spass_pair_go<4>(a, Qb, st);
+      case 16: return spass_pair_go<8>(a, Qb, st);
+      case 32: return spass_pair_go<16>(a, Qb, st);
     }
   }
   if (!staged && a.WB >= 2 && C >= 2) {

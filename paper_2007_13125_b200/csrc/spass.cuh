@@ -373,51 +373,143 @@ __global__ void __launch_bounds__(128, 3) spass_direct_kernel(const SPassArgs a)
   }
 }
 
-// ---- pipelined variant (WB >= 2): persistent warps, one line at a time per warp; the NEXT
-// line is copied HBM -> the warp's own padded smem buffer with cp.async while the current line
-// is solved in registers, then stored with 256-bit sector stores.  Only __syncwarp is used.
+// ---- two-warp variant (WB >= 2): a line of up to 64*C rows is split over 2 warps (lane gl =
+// 32*half + lane owns rows [gl*C, gl*C + C)); the warps exchange their scan totals through
+// shared memory under a pair-scoped named barrier.  Halves the recurrence chains and the
+// per-thread registers (more resident warps) relative to one warp per line.
+__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
 template <int C>
-__global__ void __launch_bounds__(128, 3) spass_pipe_kernel(const SPassArgs a) {
-  extern __shared__ double2 sm[];
-  constexpr int SL = 32 * (C + 1);                   // per-warp buffer, row y at y + y/C
+__global__ void __launch_bounds__(128, 4) spass_pair_kernel(const SPassArgs a) {
+  __shared__ double2 xch[2][4];                      // per pair: fwd total, bwd total, w0, spare
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  double2* buf = sm + warp * SL;
+  const int pair = warp >> 1, half = warp & 1;
+  const long line = (long)blockIdx.x * 2 + pair;
   const long N = a.N, NB = a.NB;
+  const bool live = line < a.nwork;
+  const long q = live ? line / N : 0, p = live ? line - q * N : 0;
   const int WB = a.WB, lwb = a.lwb, L = a.L;
   const int Lpad = (int)NB * WB;
-  const long nlines = a.nwork;
-  const long stride = (long)gridDim.x * 4;
-  long line = (long)blockIdx.x * 4 + warp;
-  auto issue = [&](long ln) {                        // cp.async all rows of line ln into buf
-    const long q = ln / N, p = ln - q * N;
-    const double2* in = a.in + (q * NB * N + p) * WB;
-#pragma unroll 4
-    for (int i = 0; i < C; ++i) {
-      const int y = 32 * i + lane;
-      if (y < Lpad) cp_async16(&buf[y + y / C], in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)));
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  if (line < nlines) issue(line);
-  for (; line < nlines; line += stride) {
-    const long q = line / N, p = line - q * N;
-    const double2 sp = __ldg(&a.sig_p[p]);
-    const double2 sig = make_double2(sp.x + __ldg(&a.sig_q[q]), sp.y);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
-    double2 d[C];
-    const int nv = min(max(L - lane * C, 0), C);
+  const int gl = half * 32 + lane;
+  const double2* in = a.in + (q * NB * N + p) * WB;
+  double2 d[C];
 #pragma unroll
-    for (int r = 0; r < C; ++r) d[r] = (r < nv) ? buf[lane * (C + 1) + r] : make_double2(0.0, 0.0);
-    __syncwarp();                                    // buffer free: start the next line's copy
-    if (line + stride < nlines) issue(line + stride);
-    solve_line_regs<C>(d, sig, L, lane);
-    double2* out = a.out + (q * NB * N + p) * WB;
+  for (int r = 0; r < C; r += 2) {
+    const int y = gl * C + r;
+    if (live && y < Lpad) ld256(in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+    else { d[r] = make_double2(0.0, 0.0); d[r + 1] = d[r]; }
+  }
+  const double2 sp = live ? __ldg(&a.sig_p[p]) : make_double2(1.0, 0.0);
+  const double2 sig = make_double2(sp.x + (live ? __ldg(&a.sig_q[q]) : 0.0), sp.y);
+  const int nv = min(max(L - gl * C, 0), C);
 #pragma unroll
-    for (int r = 0; r < C; r += 2) {
-      const int y = lane * C + r;
-      if (y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+  for (int r = 0; r < C; ++r) if (r >= nv) d[r] = make_double2(0.0, 0.0);
+
+  // ---- line setup (as in solve_line_regs) ----
+  const double2 s2 = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
+  const double2 t1 = cscale(cadd(sig, s2), 0.5), t2 = cscale(csub(sig, s2), 0.5);
+  const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
+  const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);
+  const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
+  const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
+  const double2 rr = make_double2(1.0 + tt.x, tt.y);
+  const double2 u = cdiv(tt, rr);
+  double2 uc[6];                                     // u-forms of a^{C 2^j}, j = 0..5
+  uc[0] = u;
+#pragma unroll
+  for (int c = 1; c < C; c <<= 1) uc[0] = uprod(uc[0], uc[0]);
+#pragma unroll
+  for (int i = 1; i < 6; ++i) uc[i] = uprod(uc[i - 1], uc[i - 1]);
+  // per-lane u-form of a^{C (lane+1)} and a^{C (32-lane)} (for the cross-warp carries)
+  double2 ufw = make_double2(0.0, 0.0), ubw = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    if ((lane + 1) & (1 << i)) ufw = uprod(ufw, uc[i]);
+    if ((32 - lane) & (1 << i)) ubw = uprod(ubw, uc[i]);
+  }
+
+  // ---- forward recurrence ----
+  double2 f = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int o = 1 << i;
+    double2 x;
+    x.x = __shfl_up_sync(0xffffffffu, f.x, o);
+    x.y = __shfl_up_sync(0xffffffffu, f.y, o);
+    if (lane >= o) f = cadd(f, amul(uc[i], x));
+  }
+  if (half == 0 && lane == 31) xch[pair][0] = f;     // warp-0 total (inclusive at its last row)
+  pair_bar(1 + pair);
+  if (half == 1) f = cadd(f, amul(ufw, xch[pair][0]));
+  double2 carry;
+  carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
+  carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
+  if (lane == 0) carry = half ? xch[pair][0] : make_double2(0.0, 0.0);
+  f = carry;
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    f = cadd(d[r], amul(u, f));
+    d[r] = (r < nv) ? f : make_double2(0.0, 0.0);
+  }
+  // ---- backward recurrence ----
+  double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int o = 1 << i;
+    double2 x;
+    x.x = __shfl_down_sync(0xffffffffu, w.x, o);
+    x.y = __shfl_down_sync(0xffffffffu, w.y, o);
+    if (lane + o < 32) w = cadd(w, amul(uc[i], x));
+  }
+  if (half == 1 && lane == 0) xch[pair][1] = w;      // warp-1 total (suffix from its first row)
+  pair_bar(1 + pair);
+  if (half == 0) w = cadd(w, amul(ubw, xch[pair][1]));
+  carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
+  carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
+  if (lane == 31) carry = half ? make_double2(0.0, 0.0) : xch[pair][1];
+  w = carry;
+#pragma unroll
+  for (int r = C - 1; r >= 0; --r) {
+    w = cadd(d[r], amul(u, w));
+    d[r] = w;
+  }
+  // ---- rank-1 Dirichlet correction ----
+  if (half == 0 && lane == 0) xch[pair][2] = d[0];
+  pair_bar(1 + pair);
+  const double2 w0 = xch[pair][2];
+  const double2 u2L = upow(u, 2L * L + 2);
+  const double2 K = cdiv(w0, u2L);
+  const int y0 = gl * C;
+  if (nv > 0) {
+    const double2 a1 = make_double2(1.0 - u.x, -u.y);
+    const double la = 0.5 * log(cabs2(a1));
+    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));
+    const bool needP = (y0 + 2) * la > thr;
+    const bool needQ = (2.0 * L + 2 - (y0 + nv - 1)) * la > thr;
+    if (needP) {
+      const double2 uP = upow(u, y0 + 2);
+      double2 KP = cmul(K, make_double2(1.0 - uP.x, -uP.y));
+#pragma unroll
+      for (int r = 0; r < C; ++r) { d[r] = csub(d[r], KP); KP = cmul(KP, a1); }
     }
+    if (needQ) {
+      const double2 uQ = upow(u, 2L * L + 2 - y0);
+      double2 KQ = cmul(K, make_double2(1.0 - uQ.x, -uQ.y));
+#pragma unroll
+      for (int r = 0; r < C; ++r) { d[r] = cadd(d[r], KQ); KQ = cmul(KQ, rr); }
+    }
+  }
+  double2* out = a.out + (q * NB * N + p) * WB;
+#pragma unroll
+  for (int r = 0; r < C; r += 2) {
+    const int y = gl * C + r;
+    const double2 x0 = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+    const double2 x1 = (r + 1 < nv) ? amul(u, d[r + 1]) : make_double2(0.0, 0.0);
+    if (live && y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), x0, x1);
   }
 }
 
