@@ -4,6 +4,7 @@
 // twiddles, lambda_q) are built here in 80-bit long double and rounded once to fp64.  This
 // file shares no code or tables with oracle/ (test infrastructure); Table 1 is transcribed
 // independently below.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -127,6 +128,7 @@ struct pint_plan_s {
   unsigned long long* upd = nullptr;
   int64_t dev_bytes = 0;
   std::vector<void*> allocs;
+  std::vector<VmmAlloc> vallocs;
   // state
   bool problem_set = false;
   int stateA = 0;            // 0: A holds H_{m+1} (B holds W_m); 1: A holds U_m (time domain)
@@ -141,6 +143,42 @@ struct pint_plan_s {
   double t_ms = 0, s_ms = 0;
   int64_t t_n = 0, s_n = 0;
 };
+
+// ---- driver VMM allocation with an explicit compression type (space-time buffers) ----
+struct VmmApi {
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*vfree)(CUdeviceptr, size_t) = nullptr;
+  bool ok = false;
+};
+static VmmApi& vmm() {
+  static VmmApi v;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    auto get = [](const char* n, void** f) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(n, f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    v.ok = get("cuMemCreate", (void**)&v.create) && get("cuMemAddressReserve", (void**)&v.reserve) &&
+           get("cuMemMap", (void**)&v.map) && get("cuMemSetAccess", (void**)&v.access) &&
+           get("cuMemGetAllocationGranularity", (void**)&v.gran) && get("cuMemUnmap", (void**)&v.unmap) &&
+           get("cuMemRelease", (void**)&v.release) && get("cuMemAddressFree", (void**)&v.vfree);
+  }
+  return v;
+}
+struct VmmAlloc { CUdeviceptr ptr; size_t size; CUmemGenericAllocationHandle h; };
+
+template <class T>
+static pint_status dalloc(pint_plan p, T** ptr, size_t count);
+
+// comp: 0 = CU_MEM_ALLOCATION_COMP_NONE, 1 = CU_MEM_ALLOCATION_COMP_GENERIC
+static pint_status valloc(pint_plan p, double2** ptr, size_t count, int comp);
 
 template <class T>
 static pint_status dalloc(pint_plan p, T** ptr, size_t count) {
@@ -168,10 +206,40 @@ static pint_status h2d(pint_plan p, T* dst, const std::vector<T>& v) {
 
 static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
 
+static pint_status valloc(pint_plan p, double2** ptr, size_t count, int comp) {
+  VmmApi& v = vmm();
+  if (!v.ok) return dalloc(p, ptr, count);
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = p->device;
+  prop.allocFlags.compressionType = comp ? CU_MEM_ALLOCATION_COMP_GENERIC : CU_MEM_ALLOCATION_COMP_NONE;
+  size_t g = 0;
+  if (v.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || g == 0) return dalloc(p, ptr, count);
+  const size_t bytes = ((std::max<size_t>(count, 1) * sizeof(double2) + g - 1) / g) * g;
+  VmmAlloc a{0, bytes, 0};
+  if (v.create(&a.h, bytes, &prop, 0) != CUDA_SUCCESS) return fail(PINT_ERR_ALLOC, "cuMemCreate failed");
+  if (v.reserve(&a.ptr, bytes, g, 0, 0) != CUDA_SUCCESS) { v.release(a.h); return fail(PINT_ERR_ALLOC, "cuMemAddressReserve failed"); }
+  if (v.map(a.ptr, bytes, 0, a.h, 0) != CUDA_SUCCESS) { v.vfree(a.ptr, bytes); v.release(a.h); return fail(PINT_ERR_ALLOC, "cuMemMap failed"); }
+  CUmemAccessDesc d{};
+  d.location = prop.location;
+  d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (v.access(a.ptr, bytes, &d, 1) != CUDA_SUCCESS) {
+    v.unmap(a.ptr, bytes); v.vfree(a.ptr, bytes); v.release(a.h);
+    return fail(PINT_ERR_ALLOC, "cuMemSetAccess failed");
+  }
+  p->vallocs.push_back(a);
+  p->dev_bytes += (int64_t)bytes;
+  *ptr = (double2*)a.ptr;
+  return PINT_OK;
+}
+
 static void free_plan(pint_plan p) {
   if (!p) return;
   cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
   for (void* q : p->allocs) cudaFree(q);
+  for (auto& a : p->vallocs) { vmm().unmap(a.ptr, a.size); vmm().vfree(a.ptr, a.size); vmm().release(a.h); }
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   for (auto& e : p->tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : p->sev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -251,8 +319,18 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
 
   const size_t arr = (size_t)p->ntiles * TILE;
   pint_status st;
-  if ((st = dalloc(p, &p->A, arr)) != PINT_OK) return bail(st);
-  if ((st = dalloc(p, &p->B, arr)) != PINT_OK) return bail(st);
+  {
+    // space-time buffers: PINT_ALLOC=vmm (no compression) | vmm_comp (generic compression) | default cudaMalloc
+    const char* al = getenv("PINT_ALLOC");
+    const int mode = al ? (std::string(al) == "vmm" ? 1 : (std::string(al) == "vmm_comp" ? 2 : 0)) : 0;
+    if (mode) {
+      if ((st = valloc(p, &p->A, arr, mode == 2)) != PINT_OK) return bail(st);
+      if ((st = valloc(p, &p->B, arr, mode == 2)) != PINT_OK) return bail(st);
+    } else {
+      if ((st = dalloc(p, &p->A, arr)) != PINT_OK) return bail(st);
+      if ((st = dalloc(p, &p->B, arr)) != PINT_OK) return bail(st);
+    }
+  }
   for (int i = 0; i < 2; ++i)
     if ((st = dalloc(p, &p->wrap[i], (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->tw, N)) != PINT_OK) return bail(st);
