@@ -101,6 +101,36 @@ static std::vector<ld> cq_weights(int k, ld alpha, long n) {
 // ------------------------------------------------------------------------------------------
 // plan
 // ------------------------------------------------------------------------------------------
+// ---- driver VMM allocation with an explicit compression type (space-time buffers) ----
+struct VmmApi {
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*vfree)(CUdeviceptr, size_t) = nullptr;
+  bool ok = false;
+};
+static VmmApi& vmm() {
+  static VmmApi v;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    auto get = [](const char* n, void** f) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(n, f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
+    };
+    v.ok = get("cuMemCreate", (void**)&v.create) && get("cuMemAddressReserve", (void**)&v.reserve) &&
+           get("cuMemMap", (void**)&v.map) && get("cuMemSetAccess", (void**)&v.access) &&
+           get("cuMemGetAllocationGranularity", (void**)&v.gran) && get("cuMemUnmap", (void**)&v.unmap) &&
+           get("cuMemRelease", (void**)&v.release) && get("cuMemAddressFree", (void**)&v.vfree);
+  }
+  return v;
+}
+struct VmmAlloc { CUdeviceptr ptr; size_t size; CUmemGenericAllocationHandle h; };
+
 struct pint_plan_s {
   int64_t M, N, mx, my;
   int k, dim, flags, rank, nranks;
@@ -144,35 +174,7 @@ struct pint_plan_s {
   int64_t t_n = 0, s_n = 0;
 };
 
-// ---- driver VMM allocation with an explicit compression type (space-time buffers) ----
-struct VmmApi {
-  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
-  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
-  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
-  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
-  CUresult (*gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
-  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
-  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
-  CUresult (*vfree)(CUdeviceptr, size_t) = nullptr;
-  bool ok = false;
-};
-static VmmApi& vmm() {
-  static VmmApi v;
-  static bool init = false;
-  if (!init) {
-    init = true;
-    auto get = [](const char* n, void** f) {
-      cudaDriverEntryPointQueryResult q;
-      return cudaGetDriverEntryPoint(n, f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
-    };
-    v.ok = get("cuMemCreate", (void**)&v.create) && get("cuMemAddressReserve", (void**)&v.reserve) &&
-           get("cuMemMap", (void**)&v.map) && get("cuMemSetAccess", (void**)&v.access) &&
-           get("cuMemGetAllocationGranularity", (void**)&v.gran) && get("cuMemUnmap", (void**)&v.unmap) &&
-           get("cuMemRelease", (void**)&v.release) && get("cuMemAddressFree", (void**)&v.vfree);
-  }
-  return v;
-}
-struct VmmAlloc { CUdeviceptr ptr; size_t size; CUmemGenericAllocationHandle h; };
+
 
 template <class T>
 static pint_status dalloc(pint_plan p, T** ptr, size_t count);
