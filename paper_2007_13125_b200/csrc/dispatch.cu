@@ -23,6 +23,7 @@ cudaError_t launch_tpass(int N, int mi, int mo, bool cq, const TPassArgs& a, lon
 
 cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st) {
   switch (N) {
+    case 256: return launch_tpass_pruned_256(a, ntiles, st);
     case 512: return launch_tpass_pruned_512(a, ntiles, st);
     case 1024: return launch_tpass_pruned_1024(a, ntiles, st);
     case 2048: return launch_tpass_pruned_2048(a, ntiles, st);

@@ -134,7 +134,10 @@ __device__ __forceinline__ void butterfly_pass(double2 (&v)[16], const double2* 
       const int b = tid + j * TPB, i = b / WB, k = i % P;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
-        double2 w = __ldg(&tw[t * k * (N / (P * R))]);   // global table, L1-resident
+        // volatile load: keeps the compiler from hoisting every pass's twiddles above the
+        // barriers (which blew the CQ kernel up to 255 registers + spills)
+        double2 w;
+        asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(&tw[t * k * (N / (P * R))]));
         if (DIR > 0) w.y = -w.y;
         v[j * R + t] = cmul(v[j * R + t], w);
       }

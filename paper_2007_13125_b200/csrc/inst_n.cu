@@ -30,10 +30,10 @@ static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
 }
 
 cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntiles, cudaStream_t st) {
-#if PINT_N >= 512
+#if PINT_N >= 256
   auto kern = tpass_heat_pruned_kernel<PINT_N>;
   constexpr int WBp = TILE / PINT_N;
-  const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N / 256) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
+  const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N >= 256 ? PINT_N / 256 : 1) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
   static long resident = 0;
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

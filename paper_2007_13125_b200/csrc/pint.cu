@@ -149,6 +149,10 @@ struct pint_plan_s {
   int* nhi = nullptr;        // [S]
   int S = 0;
   int nmax = 0;               // max_s nhi[s]
+  int nk = 0;                 // pruned T-pass: max(k, max sparse nhi)
+  int nsparse = 0, ndense = 0;
+  int* srclist = nullptr;     // [S]: sparse sources, then dense sources
+  double2* chat = nullptr;    // [S][N] DFTs of dense coefficient sequences
   double2 *tw = nullptr, *twE = nullptr;
   double *gsf = nullptr, *igs = nullptr, *gsN = nullptr, *wk = nullptr;
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
@@ -429,6 +433,9 @@ static TPassArgs targs(pint_plan p) {
   a.dh = p->dh; a.dpr = p->dpr; a.thp = p->thp; a.thm = p->thm; a.gsfq = p->gsf;
   a.upd = p->upd;
   a.nmax = p->nmax;
+  a.nk = p->nk;
+  a.nsparse = p->nsparse; a.spar = p->srclist;
+  a.ndense = p->ndense; a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat;
   static const bool nopf = getenv("PINT_NO_PREFETCH") != nullptr;   // A/B switch (profiling)
   a.prefetch = nopf ? 0 : 1;
   return a;
@@ -443,8 +450,8 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 512 &&
-                      std::max(p->k, p->nmax) <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT);
+  const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 256 &&
+                      p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT);
   if (pruned) CUDA_TRY(launch_tpass_pruned((int)p->N, a, p->ntiles, p->stream));
   else CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
   ++p->launches;
@@ -524,6 +531,8 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     TRY(dalloc(p, &p->src, (size_t)S * p->ntiles * p->WB));
     TRY(dalloc(p, &p->coef, (size_t)S * N));
     TRY(dalloc(p, &p->nhi, S));
+    TRY(dalloc(p, &p->srclist, S));
+    TRY(dalloc(p, &p->chat, (size_t)S * N));
     p->S = S;
   }
   CUDA_TRY(cudaMemsetAsync(p->src, 0, (size_t)S * p->ntiles * p->WB * sizeof(double2), p->stream));
@@ -569,6 +578,34 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     for (int64_t n = 0; n < N; ++n)
       if (coef[(size_t)s * N + n] != 0.0) nhi[s] = (int)(n + 1);
   p->nmax = *std::max_element(nhi.begin(), nhi.end());
+  // pruned heat T-pass: sources whose coefficients vanish for n >= 16 enter X_0..X_15; the others
+  // are synthesised from the exact DFT of Gamma h^2/N c_s(n) (long double, once per problem)
+  {
+    std::vector<int> lst;
+    int nk = p->k;
+    for (int s = 0; s < S; ++s) if (nhi[s] <= 16) { lst.push_back(s); nk = std::max(nk, nhi[s]); }
+    p->nsparse = (int)lst.size();
+    std::vector<double2> ch;
+    const ld hl = 1.0L / (ld)(p->L + 1), Nl = (ld)N;
+    for (int s = 0; s < S; ++s) {
+      if (nhi[s] <= 16) continue;
+      lst.push_back(s);
+      std::vector<ld> cg(N);
+      for (int64_t n = 0; n < N; ++n) cg[n] = (ld)coef[(size_t)s * N + n] * powl((ld)p->kappa, (ld)n / Nl) * hl * hl / Nl;
+      for (int64_t pp = 0; pp < N; ++pp) {
+        cld acc = 0.0L;
+        for (int64_t n = 0; n < nhi[s]; ++n) {
+          const ld ang = -2.0L * PI_L * (ld)((n * pp) % N) / Nl;
+          acc += cg[n] * cld(cosl(ang), sinl(ang));
+        }
+        ch.push_back(d2(acc));
+      }
+    }
+    p->ndense = S - p->nsparse;
+    p->nk = nk;
+    TRY(h2d(p, p->srclist, lst));
+    if (!ch.empty()) TRY(h2d(p, p->chat, ch));
+  }
   TRY(h2d(p, p->coef, coef));
   TRY(h2d(p, p->nhi, nhi));
   p->problem_set = true;

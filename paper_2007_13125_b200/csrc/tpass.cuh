@@ -22,6 +22,9 @@ namespace pint {
 #ifndef PINT_PRUNED_MINB
 #define PINT_PRUNED_MINB 3
 #endif
+#ifndef PINT_CQ_MINB
+#define PINT_CQ_MINB 1
+#endif
 #ifndef PINT_TPASS_MINB
 #define PINT_TPASS_MINB 2
 #endif
@@ -54,7 +57,28 @@ struct TPassArgs {
   unsigned long long* upd;  // max |update| as ordered bits
   int nmax;                 // max_s nhi[s]: F_static(n) == 0 for n >= nmax
   int prefetch;             // 1: bulk-prefetch the next tile into L2
+  // pruned heat T-pass: sources with coefficients beyond n = 15 ("dense") are synthesised in the
+  // frequency domain: H += sum_d chat[d][p] * src[dsrc[d]]; sparse sources enter X_0..X_15
+  int nsparse;              // number of sparse sources (listed first in spar[])
+  const int* spar;          // [nsparse] source indices with nhi <= 16
+  int ndense;
+  const int* dsrc;          // [ndense] source indices with nhi > 16
+  const double2* chat;      // [ndense][N]  sum_n gsf[n] coef[s][n] e^{-2 pi i n p / N}
+  int nk;                   // X_n = 0 for n >= nk (nk = max(k, max sparse nhi) <= 16)
 };
+
+// table load that the compiler may not hoist above barriers (bounds live ranges in the CQ path)
+template <class T> __device__ __forceinline__ T ldt(const T* p) { return *(volatile const T*)p; }
+__device__ __forceinline__ double2 ldt(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ldt(const double* p) {
+  double r;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
 
 __device__ __forceinline__ void prefetch_l2_t(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
@@ -79,39 +103,42 @@ __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* d
 __device__ __forceinline__ double2 static_rhs(const TPassArgs& a, const double2* srcp, long sstride, int N, int n) {
   double2 f = make_double2(0.0, 0.0);
   if (n >= a.nmax) return f;
-  for (int s = 0; s < a.S; ++s) f = cfmar(__ldg(&srcp[s * sstride]), __ldg(&a.coef[(long)s * N + n]), f);
+  for (int s = 0; s < a.S; ++s) f = cfmar(ldt(&srcp[s * sstride]), ldt(&a.coef[(long)s * N + n]), f);
   return f;
 }
 
 template <int N, int MODE_IN, int MODE_OUT, bool CQ>
-__global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPassArgs a, long ntiles) {
+__global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpass_kernel(const TPassArgs a, long ntiles) {
   using TM = TimeMap<N>;
   using FM = FreqMap<N>;
   constexpr int WB = TILE / N;
   extern __shared__ double2 sm[];
-  const int tid = threadIdx.x;
+
   const int k = a.k;
   const double2* tw = a.tw;
   const bool dense = a.nmax > TM::PL;   // F_static nonzero beyond the first PL levels
   double upd = 0.0;
   bool nonfinite = false;
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // tid re-read per tile through volatile asm: keeps the per-element table addresses (which
+  // depend only on tid) from being hoisted out of the tile loop and spilled
+  int tid;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
   const long base = tile * (long)TILE;
   if ((MODE_IN == IN_FREQ || MODE_IN == IN_TIME_BUF) && a.prefetch) {
     const long nt = tile + gridDim.x;
     if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
   }
   double2 v[16];
-  double2 dw[CQ ? 16 : 1];
+  // D W term: kept in registers only for the time-domain bootstrap (W computed in-kernel);
+  // in FREQ mode W is re-read from the (untouched, L2-resident) input tile at the end.
+  constexpr bool KEEP_DW = CQ && (MODE_IN != IN_FREQ);
+  double2 dw[KEEP_DW ? 16 : 1];
 
   // ---------------- input ----------------
   if constexpr (MODE_IN == IN_FREQ) {
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
-    if constexpr (CQ) {
-#pragma unroll
-      for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
-    }
     run_passes<N, +1, false>(v, sm, tw, tid);        // u = V W  (unnormalised inverse DFT)
   } else {
     // time-domain input U (registers in TimeMap)
@@ -129,10 +156,12 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
       for (int j = 0; j < TM::NJ; ++j)
 #pragma unroll
-        for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cscale(v[j * TM::RL + s], __ldg(&a.gsN[TM::n(j, s, tid)]));
+        for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cscale(v[j * TM::RL + s], ldt(&a.gsN[TM::n(j, s, tid)]));
       run_passes<N, -1, true>(v, sm, tw, tid);
+      if constexpr (KEEP_DW) {
 #pragma unroll
-      for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], __ldg(&a.dh[FM::p(t, tid)]));
+        for (int t = 0; t < 16; ++t) dw[t] = cmul(v[t], ldt(&a.dh[FM::p(t, tid)]));
+      }
       run_passes<N, +1, false>(v, sm, tw, tid);
     }
     // heat time modes: v holds U itself (HAVE_U_DIRECT below)
@@ -147,7 +176,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
         const int r = j * TM::RL + s;
-        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[TM::n(j, s, tid)]));
+        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], ldt(&a.igs[TM::n(j, s, tid)]));
         a.out[base + TM::e(j, s, tid)] = U;
       }
     continue;
@@ -162,7 +191,7 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
       const int n = TM::n(j, s, tid);
       if ((s == TM::RL - 1 || TM::PL < 8) && n >= N - k) {
         const int r = j * TM::RL + s, c = TM::c(j, tid), jj = n - (N - k);
-        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], __ldg(&a.igs[n]));
+        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], ldt(&a.igs[n]));
         const long wi = (tile * k + jj) * WB + c;
         if constexpr (MODE_IN == IN_FREQ) {
           const double2 o = a.wrap_old[wi];
@@ -201,11 +230,11 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
 #pragma unroll
     for (int j = 0; j < TM::NJ; ++j)
 #pragma unroll
-      for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cmul(v[j * TM::RL + s], __ldg(&a.thp[TM::n(j, s, tid)]));
+      for (int s = 0; s < TM::RL; ++s) v[j * TM::RL + s] = cmul(v[j * TM::RL + s], ldt(&a.thp[TM::n(j, s, tid)]));
     run_passes<N, -1, true>(v, sm, tw, tid);
     // s = V (D' z)
 #pragma unroll
-    for (int t = 0; t < 16; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[FM::p(t, tid)]));
+    for (int t = 0; t < 16; ++t) v[t] = cmul(v[t], ldt(&a.dpr[FM::p(t, tid)]));
     run_passes<N, +1, false>(v, sm, tw, tid);
     // X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s
 #pragma unroll
@@ -215,11 +244,16 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_kernel(const TPass
         const int n = TM::n(j, s, tid), c = TM::c(j, tid);
         const double2 F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n);
         const int r = j * TM::RL + s;
-        v[r] = cfmar(F, __ldg(&a.gsfq[n]), cmul(v[r], __ldg(&a.thm[n])));
+        v[r] = cfmar(F, ldt(&a.gsfq[n]), cmul(v[r], ldt(&a.thm[n])));
       }
     run_passes<N, -1, true>(v, sm, tw, tid);
+    if constexpr (KEEP_DW) {
 #pragma unroll
-    for (int t = 0; t < 16; ++t) v[t] = cadd(v[t], dw[t]);
+      for (int t = 0; t < 16; ++t) v[t] = cadd(v[t], dw[t]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = cfma(a.in[base + FM::e(t, tid)], ldt(&a.dh[FM::p(t, tid)]), v[t]);
+    }
   }
 
 #pragma unroll
@@ -251,7 +285,7 @@ namespace pint {
 // ---------------------------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kernel(const TPassArgs a, long ntiles) {
-  static_assert(N >= 512 && N <= 4096, "3-pass schedule");
+  static_assert(N >= 256 && N <= 4096, "16.16.RL schedule (RL = 1 for N = 256)");
   constexpr int WB = TILE / N;
   constexpr int NB16 = N / 16;          // radix-16 butterflies per column
   constexpr int RL = N / 256;
@@ -259,7 +293,7 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
   const int k = a.k;
-  const int nk = max(k, a.nmax);        // X_n = 0 for n >= nk (host guarantees nk <= 16)
+  const int nk = a.nk;                  // X_n = 0 for n >= nk (host guarantees nk <= 16)
   // pass-0 outputs s0 >= 16-k, slot (c, i0, j = s0-16+k): c*(9 NB16 + 1) + 9 i0 + j (k <= 8;
   // stride 9 and the +1 column skew keep the 16-byte stores/loads bank-conflict free)
   double2* Y0 = sm;
@@ -327,7 +361,11 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
       }
       double2 F = make_double2(0.0, 0.0);
       if (t < nk) {
-        F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, t);
+        const double2* srcp = a.src + tile * WB + c;
+        for (int i = 0; i < a.nsparse; ++i) {
+          const int s = __ldg(&a.spar[i]);
+          F = cfmar(__ldg(&srcp[(long)s * ntiles * WB]), __ldg(&a.coef[(long)s * N + t]), F);
+        }
         for (int jw = t + 1; jw <= k; ++jw) F = cfmar(window(k + t - jw), __ldg(&a.wk[jw]), F);
         F = cscale(F, __ldg(&a.gsf[t]));
       }
@@ -342,6 +380,13 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
       else v[t] = make_double2(0.0, 0.0);
     }
     dft16<-1>(v);
+    // dense static sources, synthesised in the frequency domain (precomputed DFT of their coefficients)
+    for (int dd = 0; dd < a.ndense; ++dd) {
+      const double2 g = __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * ntiles + tile) * WB + c0]);
+      const double2* ch = a.chat + (long)dd * N + i0;
+#pragma unroll
+      for (int s = 0; s < 16; ++s) v[s] = cfma(__ldg(&ch[s * (N / 16)]), g, v[s]);
+    }
 #pragma unroll
     for (int s = 0; s < 16; ++s) a.out[base + tid + s * TPB] = v[s];
     __syncthreads();   // Xs / Y0 reused by the next tile
