@@ -29,11 +29,12 @@ static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntiles, cudaStream_t st) {
 #if PINT_N >= 256
-  auto kern = tpass_heat_pruned_kernel<PINT_N>;
+template <bool DENSE>
+static cudaError_t go_pruned(const TPassArgs& a, long ntiles, cudaStream_t st) {
+  auto kern = tpass_heat_pruned_kernel<PINT_N, DENSE>;
   constexpr int WBp = TILE / PINT_N;
-  const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N >= 256 ? PINT_N / 256 : 1) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
+  const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N / 256) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
   static long resident = 0;
   if (!resident) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -48,6 +49,12 @@ cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntil
   const long grid = ntiles < resident ? ntiles : resident;
   kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
   return cudaGetLastError();
+}
+#endif
+
+cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntiles, cudaStream_t st) {
+#if PINT_N >= 256
+  return a.ndense > 0 ? go_pruned<true>(a, ntiles, st) : go_pruned<false>(a, ntiles, st);
 #else
   (void)a; (void)ntiles; (void)st;
   return cudaErrorInvalidValue;

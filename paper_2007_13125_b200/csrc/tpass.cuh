@@ -283,7 +283,7 @@ namespace pint {
 //   forward: with X supported on n < 16, passes 0 and 1 are broadcasts and pass 2 sees inputs
 //            X_0..X_15: H_{i + (N/16) s} = DFT16_s( X_t w_N^{t i} ).
 // ---------------------------------------------------------------------------------------------
-template <int N>
+template <int N, bool DENSE>
 __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kernel(const TPassArgs a, long ntiles) {
   static_assert(N >= 256 && N <= 4096, "16.16.RL schedule (RL = 1 for N = 256)");
   constexpr int WB = TILE / N;
@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
     }
     dft16<-1>(v);
     // dense static sources, synthesised in the frequency domain (precomputed DFT of their coefficients)
+    if constexpr (DENSE)
     for (int dd = 0; dd < a.ndense; ++dd) {
       const double2 g = __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * ntiles + tile) * WB + c0]);
       const double2* ch = a.chat + (long)dd * N + i0;
