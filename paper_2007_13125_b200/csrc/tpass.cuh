@@ -381,12 +381,13 @@ __global__ void __launch_bounds__(TPB, PINT_PRUNED_MINB) tpass_heat_pruned_kerne
     }
     dft16<-1>(v);
     // dense static sources, synthesised in the frequency domain (precomputed DFT of their coefficients)
-    if constexpr (DENSE)
-    for (int dd = 0; dd < a.ndense; ++dd) {
-      const double2 g = __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * ntiles + tile) * WB + c0]);
-      const double2* ch = a.chat + (long)dd * N + i0;
+    if constexpr (DENSE) {
+      for (int dd = 0; dd < a.ndense; ++dd) {
+        const double2 g = __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * ntiles + tile) * WB + c0]);
+        const double2* ch = a.chat + (long)dd * N + i0;
 #pragma unroll
-      for (int s = 0; s < 16; ++s) v[s] = cfma(__ldg(&ch[s * (N / 16)]), g, v[s]);
+        for (int s = 0; s < 16; ++s) v[s] = cfma(__ldg(&ch[s * (N / 16)]), g, v[s]);
+      }
     }
 #pragma unroll
     for (int s = 0; s < 16; ++s) a.out[base + tid + s * TPB] = v[s];

@@ -226,3 +226,45 @@ def test_pruned_tpass_matches_full_fft_and_oracle(pint, N, k, mx, my):
     for m in range(3):
         assert rel(res[False][m], res[True][m]) < 1e-13
         assert rel(res[False][m], o[m + 1]) < TOL
+
+
+UNREAD = [
+    # mx, my, N, k, kappa, R: heat cases on the pruned T-pass (N >= 256), with and without
+    # dense-in-time sources (R = 1: phi_r(t) dense; R = 0: only v and A v, sparse)
+    (200, 1, 256, 2, 0.1, 0),
+    (200, 1, 512, 3, 0.1, 0),
+    (100, 1, 1024, 1, 0.1, 0),
+    (100, 1, 2048, 6, 0.05, 1),
+    (31, 40, 256, 4, 0.05, 1),
+    (63, 20, 2048, 6, 0.01, 0),
+    (33, 1, 4096, 5, 0.02, 0),
+]
+
+
+@pytest.mark.parametrize("mx,my,N,k,kappa,R", UNREAD)
+@pytest.mark.parametrize("full_fft", [False, True])
+def test_unread_iterations(pint, mx, my, N, k, kappa, R, full_fft):
+    """m iterations without reading in between (the production loop: pruned heat T-pass, or the
+    unpruned FFTs with PINT_FLAG_FULL_FFT), then one read: equals the oracle's m-th iterate, and the
+    update norms equal the oracle's window updates."""
+    prob = inputs.random_complex_problem(mx, my, N, k, kappa, 1.0, R=R, seed=mx + N + k)
+    o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
+    for m in (1, 3):
+        with pint.Plan.from_problem(prob, full_fft=full_fft) as p:
+            ups = [p.iterate() for _ in range(m)]
+            err = rel(p.get_solution(), o[m])
+        assert err <= TOL, (m, err)
+        if my == 1:   # 2D monitors the window in the DST-x basis (a different max-norm)
+            ref_upd = np.abs(o[m][N - k:] - o[m - 1][N - k:]).max()
+            assert abs(ups[-1] - ref_upd) <= 1e-9 * ref_upd + 1e-13, (ups[-1], ref_upd)
+
+
+def test_c2_unread_matches_read(pint):
+    """C2 (k = 3, kappa = 0.01): the unread loop and the read-every-iteration loop agree."""
+    prob = inputs.config_c2(k=3, kappa=0.01)
+    with pint.Plan.from_problem(prob) as p:
+        ub = [p.iterate() for _ in range(3)]
+        b = p.get_solution()
+    o = wr.wr_naive(prob, 3)
+    assert rel(b, o[3]) < TOL
+    assert ub[1] > 0.0
