@@ -30,6 +30,19 @@ sys.path.insert(0, ROOT)
 METRIC = "space-time unknowns/sec per WR iteration (complex128) and HBM fraction, 1/2/4/8 GPU"
 UNIT = "unknowns/s"
 BYTES_PER_UNKNOWN_PASS = 32        # each pass reads 16 B and writes 16 B per unknown
+FP64_FMA_PER_CLK_SM = 64           # B200 FP64 units per SM (peak = 2 x 64 x SMs x clock)
+
+
+def fused_flops_per_unknown(k: int, nk: int) -> float:
+    """Algorithmic FP64 flops (FMA = 2) per space-time unknown of the fused heat iteration
+    (DESIGN.md §5): Step-1 synthesis ((nk-1) twiddles + DFT8 per 8 unknowns), Step-3 window
+    (DFT8 + k twiddled accumulations per 8 unknowns), Step-2 solve (4 first-order recurrence
+    sweeps + the final scaling)."""
+    dft8 = 60.0
+    synth = (6.0 * (nk - 1) + dft8) / 8.0
+    window = (dft8 + 8.0 * k) / 8.0
+    solve = 4 * 10.0 + 8.0
+    return synth + window + solve
 
 
 def peaks():
@@ -170,6 +183,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--path", default="fused", choices=["fused", "stream"],
+                    help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -196,7 +211,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
                      stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
-                     allreduce_max=allreduce_max if world > 1 else None)
+                     allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"))
     v = torch.from_numpy(prob.v).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(prob.g)).to(dev) if prob.R else None
     plan.set_problem(v, g, prob.phi if prob.R else None, prob.dphi if prob.R else None)
@@ -236,21 +251,44 @@ def main():
     hbm, peak_src = peaks()
     t_avg = tm["tpass_ms"] / max(tm["tpass_launches"], 1)
     s_avg = tm["spass_ms"] / max(tm["spass_launches"], 1)
-    bytes_launch = BYTES_PER_UNKNOWN_PASS * local_unknowns
-    dom = ("tpass", t_avg) if t_avg >= s_avg else ("spass", s_avg)
-    achieved = bytes_launch / (dom[1] / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(f"{args.config}:{dom[0]}")
-    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_launch,
-                "passes": {"tpass_ms": t_avg, "spass_ms": s_avg,
-                           "tpass_GBs": bytes_launch / (t_avg / 1e3) / 1e9,
-                           "spass_GBs": bytes_launch / (s_avg / 1e3) / 1e9,
-                           "iteration_GBs": 2 * bytes_launch / (ms_step / 1e3) / 1e9,
-                           "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm}}
+    path = plan.path()
+    if path["fused"]:
+        # one fused kernel per iteration (Steps 1-3 for every unknown) + a finish kernel on the
+        # k-level window: FP64-ALU bound (no space-time array in HBM)
+        nk = path["nk"]
+        fl = fused_flops_per_unknown(prob.k, nk)
+        smx = 1965.0
+        try:
+            smx = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        except Exception:   # noqa: BLE001
+            pass
+        peak = 2 * FP64_FMA_PER_CLK_SM * torch.cuda.get_device_properties(dev).multi_processor_count * smx * 1e6 / 1e12
+        flops_launch = fl * local_unknowns
+        achieved = flops_launch / (s_avg / 1e3) / 1e12
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(f"{args.config}:fused")
+        roofline = {"bound": "alu", "kernel": "wr_fused_kernel", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                    "peak_source": f"derived: 2 x {FP64_FMA_PER_CLK_SM} FP64 FMA/clk/SM x SMs x {smx:.0f} MHz (DESIGN.md §5)",
+                    "algorithmic_flops_per_unknown": fl, "algorithmic_flops_per_launch": flops_launch,
+                    "passes": {"fused_ms": s_avg, "finish_ms": t_avg, "chunks_per_xmode": path["chunks"],
+                               "fused_share_of_step": s_avg / ms_step}}
+    else:
+        bytes_launch = BYTES_PER_UNKNOWN_PASS * local_unknowns
+        dom = ("tpass", t_avg) if t_avg >= s_avg else ("spass", s_avg)
+        achieved = bytes_launch / (dom[1] / 1e3) / 1e9
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(f"{args.config}:{dom[0]}")
+        roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": bytes_launch,
+                    "passes": {"tpass_ms": t_avg, "spass_ms": s_avg,
+                               "tpass_GBs": bytes_launch / (t_avg / 1e3) / 1e9,
+                               "spass_GBs": bytes_launch / (s_avg / 1e3) / 1e9,
+                               "iteration_GBs": 2 * bytes_launch / (ms_step / 1e3) / 1e9,
+                               "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm}}
 
     # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host
     e2e = None
@@ -287,7 +325,11 @@ def main():
                           "grid": f"{prob.mx}x{prob.my}", "N": prob.N, "k": prob.k, "kappa": prob.kappa,
                           "alpha": prob.alpha, "unknowns": total_unknowns,
                           "parallelism": f"x-mode slabs x{world}" if world > 1 else "1 GPU",
-                          "l2": f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed"},
+                          "path": "fused" if path["fused"] else "stream",
+                          "l2": (f"fused: per-iteration working set (X, line constants, window, partials) "
+                                 f"{(16 * (8 + 3 * prob.k) * prob.M + 192 * prob.N * prob.M // prob.my) / 1e9:.2f} GB"
+                                 " > L2 126 MB, no flush needed" if path["fused"] else
+                                 f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                "clocks": clk.summary(), "last_update": upd[-1] if upd else None}
         print(json.dumps(res))

@@ -60,8 +60,10 @@ enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2 };
 enum { PINT_HOST = 0, PINT_DEVICE = 1 };
 enum {
   PINT_FLAG_U0_ZERO = 1,       /* WR initial guess U_0 = 0 instead of U_0^n = v */
-  PINT_FLAG_FULL_FFT = 2       /* heat: run the unpruned time FFTs every iteration (A/B, tests);
-                                  default prunes to the k window outputs / n_k nonzero inputs */
+  PINT_FLAG_FULL_FFT = 2,      /* heat, streaming path: run the unpruned time FFTs every iteration
+                                  (A/B, tests); default prunes to the k window outputs / n_k inputs */
+  PINT_FLAG_STREAM = 4         /* heat: use the two-pass streaming iteration (H and W arrays in HBM)
+                                  instead of the default fused one-kernel iteration (A/B, tests) */
 };
 
 typedef struct {
@@ -145,6 +147,13 @@ pint_status pint_get_partition(pint_plan plan, int64_t* q_begin, int64_t* q_end)
 pint_status pint_set_timing(pint_plan plan, int32_t enable);
 pint_status pint_get_timing(pint_plan plan, double* tpass_ms, double* spass_ms,
                             int64_t* tpass_launches, int64_t* spass_launches);
+
+/* Which iteration the plan runs for its current problem: *fused = 1 for the fused one-kernel heat
+ * iteration (fused.cuh; no space-time array per iteration), 0 for the two-pass streaming one
+ * (CQ, PINT_FLAG_STREAM, or more than 8 nonzero levels of Gamma F).  *chunks = frequency-group
+ * chunks per x-mode of the fused kernel (0 when streaming); *nk = number of nonzero leading levels
+ * of Gamma F (after pint_set_problem_separable).  Any pointer may be NULL. */
+pint_status pint_get_path(pint_plan plan, int32_t* fused, int32_t* chunks, int32_t* nk);
 
 /* Introspection: iteration count m, total kernel launches issued by this plan, device bytes. */
 pint_status pint_get_info(pint_plan plan, int64_t* m, int64_t* kernel_launches, int64_t* device_bytes);

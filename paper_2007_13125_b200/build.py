@@ -60,6 +60,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
     units = [(os.path.join(CSRC, "inst_n.cu"), os.path.join(build_dir, f"inst_{n}.o"), [f"-DPINT_N={n}", *defines])
              for n in NS]
     units += [(os.path.join(CSRC, "dispatch.cu"), os.path.join(build_dir, "dispatch.o"), defines),
+              (os.path.join(CSRC, "fused.cu"), os.path.join(build_dir, "fused.o"), defines),
               (os.path.join(CSRC, "pint.cu"), os.path.join(build_dir, "pint.o"), defines)]
     jobs = jobs or min(len(units), os.cpu_count() or 4)
     logs = []

@@ -159,7 +159,16 @@ struct pint_plan_s {
   double2* sig_p = nullptr;
   double* sig_q = nullptr;
   double2* phys = nullptr;   // [2][M] physical staging (v, A v)
+  double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
+  // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
+  bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
+  bool fused = false;         // active for the current problem (also needs nk <= 8)
+  int Cf = 0, Lf = 0, nch = 1, gpc = 1;
+  double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
+  int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
+  LineConst* lc = nullptr;    // [Qb][N]
+  double2* Pp = nullptr;      // [Qb][nch][k][Lf]
   int64_t dev_bytes = 0;
   std::vector<void*> allocs;
   std::vector<VmmAlloc> vallocs;
@@ -353,6 +362,35 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = dalloc(p, &p->upd, 1)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->phys, 2 * (size_t)M)) != PINT_OK) return bail(st);
   if (dim == 2 && (st = dalloc(p, &p->twE, NE)) != PINT_OK) return bail(st);
+  // fused heat iteration: one warp per line (C rows per lane), 8 lines + k window rows in smem
+  p->Cf = C;
+  p->Lf = 32 * C;
+  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fused_smem_bytes(C, k) <= 227u * 1024u;
+  if (p->fused_ok) {
+    const int per = std::max(fused_ctas_per_sm(C, k), 1);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+    const long slots = (long)nsm * per, NG = N / 8;
+    // chunks of frequency groups per x-mode: smallest power of two giving >= 90% wave efficiency
+    long best = 1;
+    double beff = 0.0;
+    for (long c = 1; c <= NG; c *= 2) {
+      const double waves = (double)(p->Qb * c) / (double)slots;
+      const double eff = waves / std::ceil(waves);
+      if (eff > beff + 1e-9) { beff = eff; best = c; }
+      if (eff >= 0.9) { best = c; break; }
+    }
+    p->nch = (int)best;
+    p->gpc = (int)(NG / best);
+    for (int i = 0; i < 2; ++i)
+      if ((st = dalloc(p, &p->X[i], (size_t)p->Qb * 8 * p->Lf)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->lc, (size_t)p->Qb * N)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->Pp, (size_t)p->Qb * p->nch * k * p->Lf)) != PINT_OK) return bail(st);
+    for (int i = 0; i < 2; ++i) {
+      ce = cudaMemsetAsync(p->X[i], 0, (size_t)p->Qb * 8 * p->Lf * sizeof(double2), p->stream);
+      if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
+    }
+  }
   ce = cudaMemsetAsync(p->A, 0, arr * sizeof(double2), p->stream);
   if (ce == cudaSuccess) ce = cudaMemsetAsync(p->B, 0, arr * sizeof(double2), p->stream);
   if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
@@ -410,6 +448,11 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->thm, thm)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
+  if (p->fused_ok) {
+    ce = launch_line_const(p->lc, p->sig_p, p->sig_q, N, p->Qb, p->Cf, (int)L, p->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(p->stream);
+    if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("line_const: ") + cudaGetErrorString(ce)); }
+  }
   if (dim == 2) {
     std::vector<double2> twE(NE);
     for (int m = 0; m < NE; ++m) {
@@ -474,6 +517,49 @@ static pint_status spass(pint_plan p, const double2* in, double2* out) {
   return PINT_OK;
 }
 
+static FusedArgs fargs(pint_plan p, const double2* X) {
+  FusedArgs a{};
+  a.X = X; a.lc = p->lc; a.tw = p->tw; a.src = p->src;
+  a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat; a.ndense = p->ndense;
+  a.P = p->Pp; a.W = p->B;
+  a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
+  a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
+  return a;
+}
+
+static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
+  FusedArgs a = fargs(p, X);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing && !store_w) {
+    CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, p->stream));
+  }
+  CUDA_TRY(launch_fused(p->Cf, store_w, a, p->stream));
+  ++p->launches;
+  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
+  return PINT_OK;
+}
+
+// window of U (mode: FIN_PARTIALS from the fused partial sums, FIN_FROM_WRAP / FIN_FROM_V /
+// FIN_ZERO at bootstrap) -> wrap_new, update monitor, and X for the next iteration
+static pint_status finish_pass(pint_plan p, int mode, const double2* wold, double2* wnew, double2* X) {
+  FinishArgs a{};
+  a.P = p->Pp; a.wrap_old = wold; a.wrap_new = wnew; a.X = X;
+  a.src = p->src; a.coef = p->coef; a.spar = p->srclist; a.nsparse = p->nsparse;
+  a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->upd;
+  a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
+  a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->timing && mode == FIN_PARTIALS) {
+    CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, p->stream));
+  }
+  CUDA_TRY(launch_finish(a, mode, p->stream));
+  ++p->launches;
+  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->tev.push_back({e0, e1}); }
+  return PINT_OK;
+}
+
 static DstArgs dargs(pint_plan p) {
   DstArgs a{};
   a.mx = (int)p->mx; a.my = (int)p->my; a.WB = p->WB; a.NB = p->NB; a.N = p->N;
@@ -502,8 +588,12 @@ static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
 // ------------------------------------------------------------------------------------------
 static pint_status bootstrap(pint_plan p) {
   // U_0^n = v (default) or 0 (PINT_FLAG_U0_ZERO): A = H_1, wrap = last-k of U_0
-  const int mi = (p->flags & PINT_FLAG_U0_ZERO) ? IN_TIME_ZERO : IN_TIME_V;
-  TRY(tpass(p, mi, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur], false));
+  const bool zero = (p->flags & PINT_FLAG_U0_ZERO) != 0;
+  if (p->fused) {   // window of U_0 and X_1 only
+    TRY(finish_pass(p, zero ? FIN_ZERO : FIN_FROM_V, nullptr, p->wrap[p->wcur], p->X[p->xcur]));
+  } else {
+    TRY(tpass(p, zero ? IN_TIME_ZERO : IN_TIME_V, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur], false));
+  }
   p->stateA = 0;
   p->m = 0;
   p->last_upd = -1.0;
@@ -603,6 +693,7 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     }
     p->ndense = S - p->nsparse;
     p->nk = nk;
+    p->fused = p->fused_ok && nk <= 8;
     TRY(h2d(p, p->srclist, lst));
     if (!ch.empty()) TRY(h2d(p, p->chat, ch));
   }
@@ -637,6 +728,7 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
   ++p->launches;
   // H_1 and the wrap state of U_0 from the time-domain array
   TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
+  if (p->fused) TRY(finish_pass(p, FIN_FROM_WRAP, p->wrap[p->wcur], nullptr, p->X[p->xcur]));
   p->stateA = 0;
   p->m = 0;
   p->last_upd = -1.0;
@@ -649,6 +741,16 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // iteration
 // ------------------------------------------------------------------------------------------
 static pint_status iterate_async(pint_plan p) {
+  if (p->fused) {
+    CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+    TRY(fused_pass(p, p->X[p->xcur], false));                                     // Steps 1-3
+    TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
+    p->wcur ^= 1;
+    p->xcur ^= 1;
+    p->stateA = 0;   // A no longer holds U_m
+    ++p->m;
+    return PINT_OK;
+  }
   if (p->stateA == 1) {   // A holds U_m (after get_levels): re-derive H_{m+1}
     TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
     p->stateA = 0;
@@ -717,6 +819,8 @@ extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters,
 // ------------------------------------------------------------------------------------------
 static pint_status materialize(pint_plan p) {
   if (p->stateA == 1) return PINT_OK;
+  // fused: W_m = solve(H_m) with H_m synthesised from the X that produced it, into B
+  if (p->fused) TRY(fused_pass(p, p->X[1 - p->xcur], true));
   // U_m = Gamma^{-1} V W_m (Step 3) from B into A (time domain)
   TRY(tpass(p, IN_FREQ, OUT_U, p->B, p->A, nullptr, nullptr, false));
   p->stateA = 1;
@@ -732,8 +836,28 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
   if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "nranks > 1: use pint_get_modal_levels + pint_modal_to_physical");
   CUDA_TRY(cudaSetDevice(p->device));
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  TRY(materialize(p));
   if (n_count == 0) return PINT_OK;
+  if (n_begin >= p->N - p->k && p->stateA != 1) {
+    // levels inside the window n = N-k..N-1: read from the wrap state (no materialisation)
+    if (!p->wstage) TRY(dalloc(p, &p->wstage, (size_t)p->k * p->M));
+    double2* wdst = mem == PINT_DEVICE ? (double2*)U : p->wstage;
+    if (p->dim == 1) {
+      RemapArgs r{};
+      r.in = p->wrap[p->wcur]; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
+      r.N = p->k; r.n0 = n_begin - (p->N - p->k); r.M = p->M; r.Qb = 1;
+      CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
+    } else {
+      DstArgs a = dargs(p);
+      a.in = p->wrap[p->wcur]; a.out = wdst; a.rows = n_count * p->my; a.N = p->k; a.n0 = n_begin - (p->N - p->k);
+      CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
+    }
+    ++p->launches;
+    if (mem == PINT_HOST)
+      CUDA_TRY(cudaMemcpyAsync(U, wdst, n_count * p->M * sizeof(double2), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return PINT_OK;
+  }
+  TRY(materialize(p));
   double2* dst = mem == PINT_DEVICE ? (double2*)U : p->B;   // B is free once U_m is in A
   if (p->dim == 1) {
     RemapArgs r{};
@@ -866,6 +990,14 @@ extern "C" pint_status pint_get_info(pint_plan p, int64_t* m, int64_t* launches,
   if (m) *m = p->m;
   if (launches) *launches = p->launches;
   if (dev_bytes) *dev_bytes = p->dev_bytes;
+  return PINT_OK;
+}
+
+extern "C" pint_status pint_get_path(pint_plan p, int32_t* fused, int32_t* chunks, int32_t* nk) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (fused) *fused = p->fused ? 1 : 0;
+  if (chunks) *chunks = p->fused ? p->nch : 0;
+  if (nk) *nk = p->nk;
   return PINT_OK;
 }
 

@@ -20,13 +20,14 @@ PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET = 1, 2
 PINT_HOST, PINT_DEVICE = 0, 1
 PINT_FLAG_U0_ZERO = 1
 PINT_FLAG_FULL_FFT = 2
+PINT_FLAG_STREAM = 4
 
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
     "pint_wr_solve", "pint_get_levels", "pint_get_solution", "pint_get_modal_levels",
     "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
-    "pint_kappa_log_rule",
+    "pint_kappa_log_rule", "pint_get_path",
 ]
 
 
@@ -75,6 +76,7 @@ def lib(path: str = LIB_PATH):
         "pint_status_string": [I32],
         "pint_last_error": [],
         "pint_kappa_log_rule": [I64],
+        "pint_get_path": [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -131,7 +133,8 @@ class Plan:
 
     def __init__(self, mx: int, my: int, N: int, k: int, kappa: float, tau: float, alpha: float = 1.0,
                  device: int = 0, stream: int | None = None, u0_zero: bool = False,
-                 rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False):
+                 rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False,
+                 stream_path: bool = False):
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
         self.M = self.mx * self.my
@@ -145,7 +148,8 @@ class Plan:
                 except Exception:   # noqa: BLE001 - reported through PINT_ERR_COMM
                     return 1
             self._cb = ALLREDUCE_FN(_cb)
-        flags = (PINT_FLAG_U0_ZERO if u0_zero else 0) | (PINT_FLAG_FULL_FFT if full_fft else 0)
+        flags = (PINT_FLAG_U0_ZERO if u0_zero else 0) | (PINT_FLAG_FULL_FFT if full_fft else 0) | \
+            (PINT_FLAG_STREAM if stream_path else 0)
         opt = pint_options(alpha, device, stream or 0, flags, rank, nranks,
                            self._cb, None)
         h = ctypes.c_void_p()
@@ -245,6 +249,12 @@ class Plan:
         m, l, b = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().pint_get_info(self._h, ctypes.byref(m), ctypes.byref(l), ctypes.byref(b)))
         return {"m": m.value, "kernel_launches": l.value, "device_bytes": b.value}
+
+    def path(self):
+        """{"fused": bool, "chunks": int, "nk": int} (pint_get_path)."""
+        f, c, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().pint_get_path(self._h, ctypes.byref(f), ctypes.byref(c), ctypes.byref(n)))
+        return {"fused": bool(f.value), "chunks": c.value, "nk": n.value}
 
     def close(self):
         if getattr(self, "_h", None):

@@ -212,20 +212,20 @@ def test_xmode_slabs_reproduce_single_plan(pint, nranks):
 @pytest.mark.parametrize("N,k,mx,my", [(512, 1, 100, 1), (1024, 3, 63, 20), (2048, 6, 127, 1),
                                        (4096, 2, 31, 9), (2048, 4, 15, 33)])
 def test_pruned_tpass_matches_full_fft_and_oracle(pint, N, k, mx, my):
-    """Heat with f = 0: the pruned-FFT T-pass (default) vs the unpruned FFT T-pass
-    (PINT_FLAG_FULL_FFT) vs the oracle, m = 1..3."""
+    """Heat with f = 0, reading every iterate: the fused iteration (default), the streaming one
+    with the unpruned FFT T-pass (PINT_FLAG_STREAM | PINT_FLAG_FULL_FFT) and the oracle, m = 1..3."""
     prob = inputs.random_complex_problem(mx, my, N, k, 0.02, 1.0, R=0, seed=N + k)
     res = {}
-    for full in (False, True):
-        with pint.Plan.from_problem(prob, full_fft=full) as p:
-            res[full] = []
+    for name, kw in (("fused", {}), ("full", {"stream_path": True, "full_fft": True})):
+        with pint.Plan.from_problem(prob, **kw) as p:
+            res[name] = []
             for _ in range(3):
                 p.iterate()
-                res[full].append(p.get_solution())
+                res[name].append(p.get_solution())
     o = wr.wr_naive(prob, 3, dft="fft")
     for m in range(3):
-        assert rel(res[False][m], res[True][m]) < 1e-13
-        assert rel(res[False][m], o[m + 1]) < TOL
+        assert rel(res["fused"][m], res["full"][m]) < 1e-13
+        assert rel(res["fused"][m], o[m + 1]) < TOL
 
 
 UNREAD = [
@@ -241,18 +241,25 @@ UNREAD = [
 ]
 
 
+PATHS = {"fused": {}, "stream": {"stream_path": True}, "stream_full_fft": {"stream_path": True, "full_fft": True}}
+
+
 @pytest.mark.parametrize("mx,my,N,k,kappa,R", UNREAD)
-@pytest.mark.parametrize("full_fft", [False, True])
-def test_unread_iterations(pint, mx, my, N, k, kappa, R, full_fft):
-    """m iterations without reading in between (the production loop: pruned heat T-pass, or the
-    unpruned FFTs with PINT_FLAG_FULL_FFT), then one read: equals the oracle's m-th iterate, and the
-    update norms equal the oracle's window updates."""
+@pytest.mark.parametrize("path", list(PATHS))
+def test_unread_iterations(pint, mx, my, N, k, kappa, R, path):
+    """m iterations without reading in between (the production loop: the fused one-kernel
+    iteration, the streaming two-pass one with the pruned T-pass, or with the unpruned FFTs), then
+    one read: equals the oracle's m-th iterate, and the update norms equal the oracle's window
+    updates.  The window levels read before the full array (no materialisation) agree too."""
     prob = inputs.random_complex_problem(mx, my, N, k, kappa, 1.0, R=R, seed=mx + N + k)
     o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
     for m in (1, 3):
-        with pint.Plan.from_problem(prob, full_fft=full_fft) as p:
+        with pint.Plan.from_problem(prob, **PATHS[path]) as p:
             ups = [p.iterate() for _ in range(m)]
+            win = p.get_levels(N - k, k)
             err = rel(p.get_solution(), o[m])
+            # window error over the full-array norm (the last levels have decayed by ~1e-12)
+            assert np.linalg.norm(win - o[m][N - k:]) / np.linalg.norm(o[m]) <= TOL
         assert err <= TOL, (m, err)
         if my == 1:   # 2D monitors the window in the DST-x basis (a different max-norm)
             ref_upd = np.abs(o[m][N - k:] - o[m - 1][N - k:]).max()
@@ -268,3 +275,26 @@ def test_c2_unread_matches_read(pint):
     o = wr.wr_naive(prob, 3)
     assert rel(b, o[3]) < TOL
     assert ub[1] > 0.0
+
+
+@pytest.mark.parametrize("nlev,fused", [(7, True), (12, False)])
+def test_forcing_pulse_path_selection(pint, nlev, fused):
+    """Forcing supported on the first `nlev` time levels: Gamma F has nk = nlev nonzero leading
+    levels.  nk <= 8 runs the fused iteration with nk > k; nk in 9..16 falls back to the streaming
+    iteration (pruned T-pass).  Both match the oracle, read every iterate and unread."""
+    prob = inputs.random_complex_problem(90, 1, 512, 3, 0.05, 1.0, R=1, seed=nlev)
+    phi = prob.phi.copy()
+    phi[:, nlev + 1:] = 0.0                 # phi_r(t_n) = 0 for n > nlev (1-based level n)
+    prob = prob.with_(phi=phi)
+    o = wr.wr_naive(prob, 3, dft="fft")
+    with pint.Plan.from_problem(prob) as p:
+        assert p.path()["fused"] is fused and p.path()["nk"] == nlev
+        errs = []
+        for m in range(1, 4):
+            p.iterate()
+            errs.append(rel(p.get_solution(), o[m]))
+    with pint.Plan.from_problem(prob) as p:
+        for _ in range(3):
+            p.iterate()
+        errs.append(rel(p.get_solution(), o[3]))
+    assert max(errs) <= TOL, errs
