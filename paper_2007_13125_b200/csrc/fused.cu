@@ -4,12 +4,14 @@
 
 namespace pint {
 
-size_t fused_smem_bytes(int C, int k) { return (size_t)(FG + k) * 32 * C * sizeof(double2); }
+size_t fused_smem_bytes(int lanes, int C, int k) {
+  return (size_t)(FG + k) * lanes * C * sizeof(double2) + 8 * sizeof(LineConst) + 8 * 4 * sizeof(double2);
+}
 
-template <int C, bool SW>
+template <int C, int LANES, bool SW>
 static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
-  auto kern = wr_fused_kernel<C, SW>;
-  const size_t smem = fused_smem_bytes(C, a.k);
+  auto kern = wr_fused_kernel<C, LANES, SW>;
+  const size_t smem = fused_smem_bytes(LANES, C, a.k);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -17,47 +19,57 @@ static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
     attr = smem;
   }
   if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, FT, smem, st>>>(a);
+  kern<<<(unsigned)grid, FCfg<LANES>::THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <bool SW>
-static cudaError_t fused_sw(int C, const FusedArgs& a, long grid, cudaStream_t st) {
+template <int LANES, bool SW>
+static cudaError_t fused_c(int C, const FusedArgs& a, long grid, cudaStream_t st) {
   switch (C) {
-    case 1: return fused_go<1, SW>(a, grid, st);
-    case 2: return fused_go<2, SW>(a, grid, st);
-    case 4: return fused_go<4, SW>(a, grid, st);
-    case 8: return fused_go<8, SW>(a, grid, st);
-    case 16: return fused_go<16, SW>(a, grid, st);
-    case 32: return fused_go<32, SW>(a, grid, st);
+    case 1: return fused_go<1, LANES, SW>(a, grid, st);
+    case 2: return fused_go<2, LANES, SW>(a, grid, st);
+    case 4: return fused_go<4, LANES, SW>(a, grid, st);
+    case 8: return fused_go<8, LANES, SW>(a, grid, st);
+    case 16: return fused_go<16, LANES, SW>(a, grid, st);
+    case 32: if constexpr (LANES == 32) return fused_go<32, LANES, SW>(a, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_fused(int C, bool store_w, const FusedArgs& a, cudaStream_t st) {
+cudaError_t launch_fused(int lanes, int C, bool store_w, const FusedArgs& a, cudaStream_t st) {
   const long grid = a.Qb * a.nch;
-  return store_w ? fused_sw<true>(C, a, grid, st) : fused_sw<false>(C, a, grid, st);
+  if (lanes == 64) return store_w ? fused_c<64, true>(C, a, grid, st) : fused_c<64, false>(C, a, grid, st);
+  return store_w ? fused_c<32, true>(C, a, grid, st) : fused_c<32, false>(C, a, grid, st);
 }
 
-template <int C>
+template <int C, int LANES>
 static int fused_occ(int k) {
   int per = 0;
-  const size_t smem = fused_smem_bytes(C, k);
-  cudaFuncSetAttribute(wr_fused_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wr_fused_kernel<C, false>, FT, smem) != cudaSuccess) return 0;
+  const size_t smem = fused_smem_bytes(LANES, C, k);
+  auto kern = wr_fused_kernel<C, LANES, false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FCfg<LANES>::THREADS, smem) != cudaSuccess) return 0;
   return per;
 }
 
-int fused_ctas_per_sm(int C, int k) {
+template <int LANES>
+static int fused_occ_c(int C, int k) {
   switch (C) {
-    case 1: return fused_occ<1>(k);
-    case 2: return fused_occ<2>(k);
-    case 4: return fused_occ<4>(k);
-    case 8: return fused_occ<8>(k);
-    case 16: return fused_occ<16>(k);
-    case 32: return fused_occ<32>(k);
+    case 1: return fused_occ<1, LANES>(k);
+    case 2: return fused_occ<2, LANES>(k);
+    case 4: return fused_occ<4, LANES>(k);
+    case 8: return fused_occ<8, LANES>(k);
+    case 16: return fused_occ<16, LANES>(k);
+    case 32: if constexpr (LANES == 32) return fused_occ<32, LANES>(k);
   }
   return 0;
+}
+
+int fused_ctas_per_sm(int lanes, int C, int k) { return lanes == 64 ? fused_occ_c<64>(C, k) : fused_occ_c<32>(C, k); }
+
+int fused_rows_per_subchain(int lanes, int C) {
+  const int nsmax = lanes == 32 ? 4 : 2;
+  return C / (C < nsmax ? C : nsmax);
 }
 
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st) {
@@ -68,11 +80,11 @@ cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int L,
-                              cudaStream_t st) {
+cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int CS,
+                              int L, cudaStream_t st) {
   const long total = N * Qb;
   const long blocks = std::min<long>((total + 127) / 128, 148L * 16);
-  line_const_kernel<<<(unsigned)blocks, 128, 0, st>>>(lc, sig_p, sig_q, N, Qb, C, L);
+  line_const_kernel<<<(unsigned)blocks, 128, 0, st>>>(lc, sig_p, sig_q, N, Qb, C, CS, L);
   return cudaGetLastError();
 }
 

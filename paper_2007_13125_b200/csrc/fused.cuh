@@ -22,19 +22,21 @@
 
 namespace pint {
 
-constexpr int FG = 8;      // lines per group
-constexpr int FT = 256;    // threads per CTA: warp s solves line s of the group
+constexpr int FG = 8;      // lines per group (radix of the Step-1 / Step-3 DFTs)
 
 // Per line (q, p): the iteration-invariant constants of the Toeplitz factorisation (spass.cuh),
 // computed once at plan time (line_const_kernel).
 struct LineConst {
   double2 u;        // 1 - a,  a = 1/r, r + 1/r = 2 + sigma, |r| > 1
-  double2 uc[7];    // u-forms of a^{C 2^i}
+  double2 uh;       // u-form of a^{CS}, CS = rows per sub-chain
   double2 uE;       // u-form of a^{(2L+2) mod C}
   double2 ru2L;     // 1 / (1 - a^{2L+2})
   double2 rr;       // r
+  double2 rrh;      // r^{CS}
+  double2 uc[8];    // u-forms of a^{C 2^i}
   double la, thr;   // log|a|;  log(1e-18 |1 - a^{2L+2}|)
-};
+};                  // 240 bytes
+static_assert(sizeof(LineConst) == 240, "LineConst is staged in 16-byte chunks");
 
 struct FusedArgs {
   const double2* X;        // [Qb][8][Lf]  X_t[y], zero for t >= nk and y >= L
@@ -47,6 +49,8 @@ struct FusedArgs {
   double2* W;              // STORE_W: W_m in the tile layout [q][yb][N][WB]
   long N, Qb;
   int L, Lf, Lpad, WB, NB, k, nk, ndense, nch, gpc;
+  int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
+                           // 8 u-form recurrences on every line
 };
 
 // smem row swizzle: lane l of the solve owns rows [lC, lC + C); XOR-ing the low bits with the
@@ -60,141 +64,179 @@ template <int C> __device__ __forceinline__ int swz(int y) {
 
 __device__ __forceinline__ double2 one_minus(double2 u) { return make_double2(1.0 - u.x, -u.y); }
 
-template <int C>
-__device__ __forceinline__ void fused_synth(const FusedArgs& a, double2* Hs, const double2* Xq, long q, int i) {
-  constexpr int LF = 32 * C;
-  const int NG = (int)(a.N / FG);
-  for (int y = threadIdx.x; y < LF; y += FT) {
-    double2 z[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      z[t] = make_double2(0.0, 0.0);
-      if (t < a.nk) {
-        const double2 x = Xq[t * LF + y];
-        z[t] = t == 0 ? x : cmul(x, __ldg(&a.tw[t * i]));   // X_t w_N^{t i}
-      }
-    }
-    dft8<-1>(z);                                           // H_{i + (N/8) s} = sum_t z_t e^{-2 pi i ts/8}
-    for (int d = 0; d < a.ndense; ++d) {
-      const double2 g = y < a.L ? __ldg(&a.src[((long)__ldg(&a.dsrc[d]) * a.Qb + q) * a.Lpad + y])
-                                : make_double2(0.0, 0.0);
-      const double2* ch = a.chat + (long)d * a.N + i;
-#pragma unroll
-      for (int s = 0; s < 8; ++s) z[s] = cfma(__ldg(&ch[s * NG]), g, z[s]);
-    }
-#pragma unroll
-    for (int s = 0; s < 8; ++s) Hs[s * LF + swz<C>(y)] = z[s];
-  }
+// Recurrence multipliers.  AF = false: the shift-accurate u-form (c = 1 - multiplier, every
+// product z - c z); AF = true: the plain value form, used for lines with |u| >= 1e-3,
+// where the rounding of a = 1 - u perturbs u (hence the shift) by at most 2e-13 relatively.
+template <bool AF> __device__ __forceinline__ double2 mstep(double2 c, double2 z, double2 d) {   // d + m z
+  if constexpr (AF) return cfma(c, z, d);
+  else return cadd(d, amul(c, z));
 }
-
-template <int C>
-__device__ __forceinline__ void fused_window(const FusedArgs& a, const double2* Hs, double2* acc, int i) {
-  constexpr int LF = 32 * C;
-  const int N = (int)a.N, k = a.k;
-  for (int y = threadIdx.x; y < LF; y += FT) {
-    double2 x[8];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) x[s] = Hs[s * LF + swz<C>(y)];
-    dft8<+1>(x);                                           // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int j = r - 8 + k;                             // level n = N - 8 + r = N - k + j
-      if (j >= 0) {
-        double2 w = __ldg(&a.tw[((N - 8 + r) * i) & (N - 1)]);
-        w.y = -w.y;                                        // e^{+2 pi i n i/N}
-        acc[j * LF + y] = cfma(x[r], w, acc[j * LF + y]);
-      }
-    }
-  }
+template <bool AF> __device__ __forceinline__ double2 mmul(double2 c, double2 z) {
+  if constexpr (AF) return cmul(c, z);
+  else return amul(c, z);
 }
+template <bool AF> __device__ __forceinline__ double2 mconv(double2 uform) { return AF ? one_minus(uform) : uform; }
+constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 
-// Step 2 for line (q, p) by one warp; rows lane*C .. lane*C + C - 1 (chunked warp scan, spass.cuh)
-template <int C, bool STORE_W>
-__device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, long q, long p) {
+// LANES lanes per line: 32 (one warp; default) or 64 (two warps, pair-scoped named barriers);
+// threads per CTA = 8 LANES; LF = LANES C rows per line; NS interleaved sub-chains per lane chunk.
+template <int LANES> struct FCfg {
+  static constexpr int THREADS = FG * LANES;
+  static constexpr int NSMAX = LANES == 32 ? 4 : 2;
+};
+template <int C, int LANES> constexpr int fused_ns() { return C < FCfg<LANES>::NSMAX ? C : FCfg<LANES>::NSMAX; }
+
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Step 2 for line (q, p): rows gl*C .. gl*C + C - 1 of lane gl (chunked scan, spass.cuh), each chunk
+// as NS interleaved sub-chains of CS rows (independent dependency chains).
+template <int C, int LANES, bool STORE_W, bool AF>
+__device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, const LineConst& lc, double2* xch,
+                                            long q, long p, int half, int bar) {
+  constexpr bool PAIR = LANES == 64;
+  constexpr int NS = fused_ns<C, LANES>();
+  constexpr int CS = C / NS;
   const int lane = threadIdx.x & 31;
+  const int gl = PAIR ? half * 32 + lane : lane;
   const int L = a.L;
-  const LineConst* lc = a.lc + q * a.N + p;
-  const double2 u = lc->u;
-  double2 uc[5];
+  const double2 u = mconv<AF>(lc.u);                        // a
+  const double2 uh = mconv<AF>(lc.uh);                      // a^{CS}
+  double2 uc[5];                                            // a^{C 2^i}
 #pragma unroll
-  for (int i = 0; i < 5; ++i) uc[i] = lc->uc[i];
-  const int y0 = lane * C;
+  for (int i = 0; i < 5; ++i) uc[i] = mconv<AF>(lc.uc[i]);
+  const int y0 = gl * C;
   const int nv = min(max(L - y0, 0), C);
   double2 d[C];
 #pragma unroll
   for (int r = 0; r < C; ++r) d[r] = (r < nv) ? Hl[swz<C>(y0 + r)] : make_double2(0.0, 0.0);
 
-  // forward recurrence f_y = d_y + a f_{y-1}
-  double2 f = make_double2(0.0, 0.0);
+  // ---- forward recurrence f_y = d_y + a f_{y-1} ----
+  double2 fs[NS];
 #pragma unroll
-  for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
+  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < CS; ++r)
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = mstep<AF>(u, fs[s2], d[s2 * CS + r]);
+  double2 f = fs[0];
+#pragma unroll
+  for (int s2 = 1; s2 < NS; ++s2) f = mstep<AF>(uh, f, fs[s2]);          // chunk total (zero carry)
+  if (PAIR && half == 1) {                                                 // inject warp 0's total
+    pair_sync(bar);
+    if (lane == 0) f = mstep<AF>(uc[0], xch[0], f);
+  }
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_up_sync(0xffffffffu, f.x, o);
     x.y = __shfl_up_sync(0xffffffffu, f.y, o);
-    if (lane >= o) f = cadd(f, amul(uc[i], x));
+    if (lane >= o) f = mstep<AF>(uc[i], x, f);
+  }
+  if (PAIR && half == 0) {
+    if (lane == 31) xch[0] = f;
+    pair_sync(bar);
   }
   double2 carry;
   carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
   carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
-  if (lane == 0) carry = make_double2(0.0, 0.0);
-  f = carry;
+  if (lane == 0) carry = (PAIR && half) ? xch[0] : make_double2(0.0, 0.0);
+  double2 st[NS];
+  st[0] = carry;
 #pragma unroll
-  for (int r = 0; r < C; ++r) {
-    f = cadd(d[r], amul(u, f));
-    d[r] = (r < nv) ? f : make_double2(0.0, 0.0);
+  for (int s2 = 1; s2 < NS; ++s2) st[s2] = mstep<AF>(uh, st[s2 - 1], fs[s2 - 1]);
+#pragma unroll
+  for (int r = 0; r < CS; ++r)
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) {
+      st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
+      d[s2 * CS + r] = (s2 * CS + r < nv) ? st[s2] : make_double2(0.0, 0.0);
+    }
+
+  // ---- backward recurrence w_y = f_y + a w_{y+1} ----
+#pragma unroll
+  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = CS - 1; r >= 0; --r)
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = mstep<AF>(u, fs[s2], d[s2 * CS + r]);
+  double2 w = fs[NS - 1];
+#pragma unroll
+  for (int s2 = NS - 2; s2 >= 0; --s2) w = mstep<AF>(uh, w, fs[s2]);
+  if (PAIR && half == 0) {                                                 // inject warp 1's total
+    pair_sync(bar);
+    if (lane == 31) w = mstep<AF>(uc[0], xch[1], w);
   }
-  // backward recurrence w_y = f_y + a w_{y+1}
-  double2 w = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_down_sync(0xffffffffu, w.x, o);
     x.y = __shfl_down_sync(0xffffffffu, w.y, o);
-    if (lane + o < 32) w = cadd(w, amul(uc[i], x));
+    if (lane + o < 32) w = mstep<AF>(uc[i], x, w);
+  }
+  if (PAIR && half == 1) {
+    if (lane == 0) xch[1] = w;
+    pair_sync(bar);
   }
   carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
   carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
-  if (lane == 31) carry = make_double2(0.0, 0.0);
-  w = carry;
+  if (lane == 31) carry = (PAIR && !half) ? xch[1] : make_double2(0.0, 0.0);
+  st[NS - 1] = carry;
 #pragma unroll
-  for (int r = C - 1; r >= 0; --r) {
-    w = cadd(d[r], amul(u, w));
-    d[r] = w;
-  }
-  // rank-1 Dirichlet correction x = a (w - w_0 phi), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2})
-  double2 w0;
-  w0.x = __shfl_sync(0xffffffffu, d[0].x, 0);
-  w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
-  const double2 K = cmul(w0, lc->ru2L);
-  if (nv > 0) {
-    const double la = lc->la, thr = lc->thr;
-    if ((y0 + 2) * la > thr) {                              // |a^{y+2}| is largest at y0
-      double2 ul = uprod(u, u);                             // a^2
+  for (int s2 = NS - 2; s2 >= 0; --s2) st[s2] = mstep<AF>(uh, st[s2 + 1], fs[s2 + 1]);
 #pragma unroll
-      for (int i = 0; i < 5; ++i)
-        if ((lane >> i) & 1) ul = uprod(ul, uc[i]);         // a^{C lane + 2}
-      double2 KP = cmul(K, one_minus(ul));
-      const double2 a1 = one_minus(u);
+  for (int r = CS - 1; r >= 0; --r)
 #pragma unroll
-      for (int r = 0; r < C; ++r) { d[r] = csub(d[r], KP); KP = cmul(KP, a1); }
+    for (int s2 = 0; s2 < NS; ++s2) {
+      st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
+      d[s2 * CS + r] = st[s2];
     }
-    if ((2.0 * L + 2 - (y0 + nv - 1)) * la > thr) {         // |a^{2L+2-y}| is largest at the chunk end
-      // 2L+2-y0 = e + C (m0 - lane),  e = (2L+2) mod C
-      const int m = (2 * L + 2) / C - lane;
-      double2 uq = lc->uE;
+
+  // ---- rank-1 Dirichlet correction x = a (w - w_0 phi), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2}) ----
+  double2 w0;
+  if constexpr (PAIR) {
+    if (half == 0 && lane == 0) xch[2] = d[0];
+    pair_sync(bar);
+    w0 = xch[2];
+  } else {
+    w0.x = __shfl_sync(0xffffffffu, d[0].x, 0);
+    w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
+  }
+  const double2 K = cmul(w0, lc.ru2L);
+  if (nv > 0) {
+    const double la = lc.la, thr = lc.thr;
+    if ((y0 + 2) * la > thr) {                                             // |a^{y+2}| is largest at y0
+      double2 ul = uprod(lc.u, lc.u);                                      // a^2
 #pragma unroll
-      for (int i = 0; i < 7; ++i)
-        if ((m >> i) & 1) uq = uprod(uq, lc->uc[i]);
-      double2 KQ = cmul(K, one_minus(uq));
-      const double2 rr = lc->rr;
+      for (int i = 0; i < (PAIR ? 6 : 5); ++i)
+        if ((gl >> i) & 1) ul = uprod(ul, lc.uc[i]);                      // a^{C gl + 2}
+      double2 KP[NS];
+      KP[0] = cmul(K, one_minus(ul));
 #pragma unroll
-      for (int r = 0; r < C; ++r) { d[r] = cadd(d[r], KQ); KQ = cmul(KQ, rr); }
+      for (int s2 = 1; s2 < NS; ++s2) KP[s2] = cmul(KP[s2 - 1], one_minus(lc.uh));
+      const double2 a1 = one_minus(lc.u);
+#pragma unroll
+      for (int r = 0; r < CS; ++r)
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) { d[s2 * CS + r] = csub(d[s2 * CS + r], KP[s2]); KP[s2] = cmul(KP[s2], a1); }
+    }
+    if ((2.0 * L + 2 - (y0 + nv - 1)) * la > thr) {                        // |a^{2L+2-y}| largest at the chunk end
+      const int m = (2 * L + 2) / C - gl;                                  // 2L+2-y0 = e + C m, e = (2L+2) mod C
+      double2 uq = lc.uE;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((m >> i) & 1) uq = uprod(uq, lc.uc[i]);
+      double2 KQ[NS];
+      KQ[0] = cmul(K, one_minus(uq));
+#pragma unroll
+      for (int s2 = 1; s2 < NS; ++s2) KQ[s2] = cmul(KQ[s2 - 1], lc.rrh);
+      const double2 rr = lc.rr;
+#pragma unroll
+      for (int r = 0; r < CS; ++r)
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) { d[s2 * CS + r] = cadd(d[s2 * CS + r], KQ[s2]); KQ[s2] = cmul(KQ[s2], rr); }
     }
   }
   if constexpr (STORE_W) {
@@ -202,12 +244,85 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, lon
 #pragma unroll
     for (int r = 0; r < C; ++r) {
       const int y = y0 + r;
-      if (y < a.Lpad) Wq[((long)(y / a.WB) * a.N) * a.WB + (y % a.WB)] = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+      if (y < a.Lpad) Wq[((long)(y / a.WB) * a.N) * a.WB + (y % a.WB)] = (r < nv) ? mmul<AF>(u, d[r]) : make_double2(0.0, 0.0);
     }
   } else {
 #pragma unroll
-    for (int r = 0; r < C; ++r) Hl[swz<C>(y0 + r)] = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+    for (int r = 0; r < C; ++r) Hl[swz<C>(y0 + r)] = (r < nv) ? mmul<AF>(u, d[r]) : make_double2(0.0, 0.0);
   }
+}
+
+// Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
+// next synthesis and the group's twiddles are issued first (one memory round trip), then each row
+// reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
+template <int C, int LANES, bool WINDOW>
+__device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, double2* acc, const double2* Xq,
+                                           long q, int i, bool next) {
+  constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
+  constexpr int RPT = LF >= T ? LF / T : 1;
+  const int N = (int)a.N, k = a.k, nk = a.nk;
+  const int NG = N / FG;
+  const int i1 = i + 1;
+  double2 xv[RPT][8];
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int y = threadIdx.x + T * rr;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      xv[rr][t] = (next && t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
+  }
+  double2 tws[8], tww[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    tws[t] = (next && t > 0 && t < nk) ? __ldg(&a.tw[t * i1]) : make_double2(1.0, 0.0);     // w_N^{t (i+1)}
+    const int j = t - 8 + k;                                                                 // level n = N - 8 + t
+    double2 w = (WINDOW && j >= 0) ? __ldg(&a.tw[((N - 8 + t) * i) & (N - 1)]) : make_double2(0.0, 0.0);
+    w.y = -w.y;                                                                              // e^{+2 pi i n i/N}
+    tww[t] = w;
+  }
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int y = threadIdx.x + T * rr;
+    if (LF < T && y >= LF) break;
+    if (WINDOW && !(a.dbg & 2)) {
+      double2 x[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) x[s2] = Hs[s2 * LF + swz<C>(y)];
+      dft8<+1>(x);                                       // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int j = r - 8 + k;
+        if (j >= 0) acc[j * LF + y] = cfma(x[r], tww[r], acc[j * LF + y]);
+      }
+    }
+    if (next && !(a.dbg & 4)) {
+      double2* z = xv[rr];
+#pragma unroll
+      for (int t = 1; t < 8; ++t) z[t] = cmul(z[t], tws[t]);                     // X_t w_N^{t (i+1)}
+      dft8<-1>(z);                                       // H_{i+1 + (N/8) s} = sum_t (.) e^{-2 pi i ts/8}
+      for (int dd = 0; dd < a.ndense; ++dd) {
+        const double2 g = y < a.L ? __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * a.Qb + q) * a.Lpad + y])
+                                  : make_double2(0.0, 0.0);
+        const double2* ch = a.chat + (long)dd * N + i1;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) z[s2] = cfma(__ldg(&ch[s2 * NG]), g, z[s2]);
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) Hs[s2 * LF + swz<C>(y)] = z[s2];
+    }
+  }
+}
+
+// line constants of group i (8 lines x 240 B) -> shared memory, 16-byte cp.async chunks
+__device__ __forceinline__ void fused_stage_lc(const FusedArgs& a, LineConst* slc, long q, int i) {
+  const int NG = (int)(a.N / FG);
+  const int t = threadIdx.x;
+  if (t < 8 * 15) {
+    const int line = t / 15, c = t % 15;
+    const char* src = (const char*)(a.lc + q * a.N + i + (long)NG * line) + 16 * c;
+    cp_async16((char*)(slc + line) + 16 * c, src);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
 // ---- finish: window of U_{m+1}, update monitor, X for the next iteration ----
@@ -230,34 +345,47 @@ struct FinishArgs {
 };
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
-// grid = Qb * nch CTAs; CTA (q, ch) runs groups [ch*gpc, (ch+1)*gpc) of x-mode q.
-template <int C, bool STORE_W>
-__global__ void __launch_bounds__(FT, 1) wr_fused_kernel(const FusedArgs a) {
+// grid = Qb * nch CTAs; CTA (q, ch) runs frequency groups [ch*gpc, (ch+1)*gpc) of x-mode q.
+template <int C, int LANES, bool STORE_W>
+__global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const FusedArgs a) {
   extern __shared__ double2 fsm[];
-  constexpr int LF = 32 * C;
-  double2* Hs = fsm;              // [8][LF]   H (in) / W (out) of the group's lines
-  double2* acc = fsm + 8 * LF;    // [k][LF]   window partial sums
+  constexpr int LF = LANES * C;
+  double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
+  double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums
+  LineConst* slc = (LineConst*)(acc + a.k * LF);       // [8]      line constants of the group
+  double2* xch = (double2*)(slc + 8);                  // [8][4]   pair exchange (LANES = 64)
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
   const int NG = (int)(a.N / FG);
   const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NG);
   const int warp = threadIdx.x >> 5;
+  const int line = LANES == 64 ? warp >> 1 : warp, half = LANES == 64 ? warp & 1 : 0;
   const double2* Xq = a.X + q * 8 * LF;
+  fused_stage_lc(a, slc, q, g0);
   if (!STORE_W)
-    for (int y = threadIdx.x; y < LF; y += FT)
+    for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
       for (int j = 0; j < a.k; ++j) acc[j * LF + y] = make_double2(0.0, 0.0);
-  fused_synth<C>(a, Hs, Xq, q, g0);
+  fused_rows<C, LANES, false>(a, Hs, acc, Xq, q, g0 - 1, true);   // synthesise group g0
+  cp_async_wait0();
   __syncthreads();
   for (int i = g0; i < g1; ++i) {
-    fused_solve<C, STORE_W>(a, Hs + warp * LF, q, i + (long)NG * warp);
+    if (!(a.dbg & 1)) {
+      const LineConst& lcl = slc[line];
+      if (cabs2(lcl.u) >= FUSED_AF_U2 && !(a.dbg & 8))
+        fused_solve<C, LANES, STORE_W, true>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
+      else
+        fused_solve<C, LANES, STORE_W, false>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
+    }
     __syncthreads();
-    if (!STORE_W) fused_window<C>(a, Hs, acc, i);     // rows owned by this thread: no barrier
-    if (i + 1 < g1) fused_synth<C>(a, Hs, Xq, q, i + 1);
+    const bool next = i + 1 < g1;
+    if (next) fused_stage_lc(a, slc, q, i + 1);
+    fused_rows<C, LANES, !STORE_W>(a, Hs, acc, Xq, q, i, next);
+    cp_async_wait0();
     __syncthreads();
   }
   if (!STORE_W) {
     double2* P = a.P + ((q * a.nch + ch) * a.k) * LF;
-    for (int y = threadIdx.x; y < LF; y += FT)
+    for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
       for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
   }
 }
@@ -317,7 +445,9 @@ __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int 
 }
 
 // ---- plan time: per-line constants ----
-__global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int L) {
+// C = rows per lane, CS = rows per sub-chain
+__global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int CS,
+                                  int L) {
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < N * Qb; e += (long)gridDim.x * blockDim.x) {
     const long q = e / N, p = e % N;
     const double2 sp = sig_p[p];
@@ -332,7 +462,10 @@ __global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const dou
     c.rr = make_double2(1.0 + tt.x, tt.y);                              // r = 1/a, |r| > 1
     c.u = cdiv(tt, c.rr);                                               // u = 1 - a
     c.uc[0] = upow(c.u, C);
-    for (int i = 1; i < 7; ++i) c.uc[i] = uprod(c.uc[i - 1], c.uc[i - 1]);
+    for (int i = 1; i < 8; ++i) c.uc[i] = uprod(c.uc[i - 1], c.uc[i - 1]);
+    c.uh = upow(c.u, CS);
+    c.rrh = make_double2(1.0, 0.0);
+    for (int i = 0; i < CS; ++i) c.rrh = cmul(c.rrh, c.rr);
     const double2 u2L = upow(c.u, 2L * L + 2);
     c.ru2L = cdiv(make_double2(1.0, 0.0), u2L);
     c.uE = upow(c.u, (2L * L + 2) % C);

@@ -20,13 +20,15 @@ cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);
 // DST-I rows, extended FFT length NE = 2(mx+1).
 cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st);
-// fused heat iteration (fused.cu): one CTA per (x-mode, group chunk), C = rows per lane
-size_t fused_smem_bytes(int C, int k);
-int fused_ctas_per_sm(int C, int k);
-cudaError_t launch_fused(int C, bool store_w, const FusedArgs& a, cudaStream_t st);
+// fused heat iteration (fused.cu): one CTA per (x-mode, group chunk); lanes (32 | 64) per line,
+// C rows per lane
+size_t fused_smem_bytes(int lanes, int C, int k);
+int fused_ctas_per_sm(int lanes, int C, int k);
+int fused_rows_per_subchain(int lanes, int C);
+cudaError_t launch_fused(int lanes, int C, bool store_w, const FusedArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st);
-cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int L,
-                              cudaStream_t st);
+cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int CS,
+                              int L, cudaStream_t st);
 
 #define PINT_DECLARE_N(NN)                                                                         \
   cudaError_t launch_tpass_##NN(int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, \

@@ -165,6 +165,7 @@ struct pint_plan_s {
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
+  int flanes = 32;            // fused kernel lanes per line: 32 (one warp, default) or 64 (PINT_FUSED_LANES=64)
   double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
   int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
   LineConst* lc = nullptr;    // [Qb][N]
@@ -362,12 +363,19 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = dalloc(p, &p->upd, 1)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->phys, 2 * (size_t)M)) != PINT_OK) return bail(st);
   if (dim == 2 && (st = dalloc(p, &p->twE, NE)) != PINT_OK) return bail(st);
-  // fused heat iteration: one warp per line (C rows per lane), 8 lines + k window rows in smem
-  p->Cf = C;
-  p->Lf = 32 * C;
-  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fused_smem_bytes(C, k) <= 227u * 1024u;
+  // fused heat iteration: v2 = two warps per line (64 lanes x Cf rows), v1 = one warp (32 x Cf);
+  // 8 lines + k window rows in smem
+  {
+    const char* fl = getenv("PINT_FUSED_LANES");
+    p->flanes = (fl && std::string(fl) == "64") ? 64 : 32;
+    int Cf = 1;
+    while (p->flanes * Cf < L) Cf *= 2;
+    p->Cf = Cf;
+    p->Lf = p->flanes * Cf;
+  }
+  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fused_smem_bytes(p->flanes, p->Cf, k) <= 232448u;
   if (p->fused_ok) {
-    const int per = std::max(fused_ctas_per_sm(C, k), 1);
+    const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
     const long slots = (long)nsm * per, NG = N / 8;
@@ -449,7 +457,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
   if (p->fused_ok) {
-    ce = launch_line_const(p->lc, p->sig_p, p->sig_q, N, p->Qb, p->Cf, (int)L, p->stream);
+    ce = launch_line_const(p->lc, p->sig_p, p->sig_q, N, p->Qb, p->Cf, fused_rows_per_subchain(p->flanes, p->Cf), (int)L,
+                           p->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(p->stream);
     if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("line_const: ") + cudaGetErrorString(ce)); }
   }
@@ -524,6 +533,8 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.P = p->Pp; a.W = p->B;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
+  static const int dbg = getenv("PINT_FUSED_DBG") ? atoi(getenv("PINT_FUSED_DBG")) : 0;   // profiling only
+  a.dbg = dbg;
   return a;
 }
 
@@ -534,7 +545,7 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  CUDA_TRY(launch_fused(p->Cf, store_w, a, p->stream));
+  CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, a, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
   return PINT_OK;
