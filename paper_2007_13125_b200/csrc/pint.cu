@@ -165,12 +165,14 @@ struct pint_plan_s {
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
-  int flanes = 32;            // fused kernel lanes per line: 32 (one warp, default) or 64 (PINT_FUSED_LANES=64)
+  int flanes = 32;            // fused kernel lanes per line: 32 (one warp) or 64 (PINT_FUSED_LANES=64, radix-8 only)
+  bool fws = false;           // PINT_FUSED_KERNEL=ws: warp-specialised radix-4 pipeline (experimental, slower)
   double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
   int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
   LineConst* lc = nullptr;    // [Qb][N]
   double2* Pp = nullptr;      // [Qb][nch][k][Lf]
   int64_t dev_bytes = 0;
+  unsigned long long* prof = nullptr;   // -DPINT_FUSED_PROF builds: phase cycle counters (not owned)
   std::vector<void*> allocs;
   std::vector<VmmAlloc> vallocs;
   // state
@@ -254,6 +256,16 @@ static void free_plan(pint_plan p) {
   if (!p) return;
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
+  if (p->prof) {   // profiling builds: print the phase cycle split of the fused kernel
+    unsigned long long h[36];
+    cudaMemcpy(h, p->prof, sizeof(h), cudaMemcpyDeviceToHost);
+    const double tot = (double)(h[0] + h[1] + h[2] + h[3]) + 1e-30;
+    fprintf(stderr, "[pint prof] fused phases (warp-cycles share): solve %.3f wait1 %.3f rows %.3f wait2 %.3f\n",
+            h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot);
+    for (int w = 0; w < 8; ++w)
+      fprintf(stderr, "[pint prof] warp %d: solve %.3e wait1 %.3e rows %.3e wait2 %.3e\n", w, (double)h[4 + 4 * w],
+              (double)h[5 + 4 * w], (double)h[6 + 4 * w], (double)h[7 + 4 * w]);
+  }
   for (void* q : p->allocs) cudaFree(q);
   for (auto& a : p->vallocs) { vmm().unmap(a.ptr, a.size); vmm().vfree(a.ptr, a.size); vmm().release(a.h); }
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -366,19 +378,22 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   // fused heat iteration: v2 = two warps per line (64 lanes x Cf rows), v1 = one warp (32 x Cf);
   // 8 lines + k window rows in smem
   {
+    const char* fk = getenv("PINT_FUSED_KERNEL");
+    p->fws = fk && std::string(fk) == "ws";     // experimental warp-specialised radix-4 pipeline
     const char* fl = getenv("PINT_FUSED_LANES");
-    p->flanes = (fl && std::string(fl) == "64") ? 64 : 32;
+    p->flanes = (!p->fws && fl && std::string(fl) == "64") ? 64 : 32;
     int Cf = 1;
     while (p->flanes * Cf < L) Cf *= 2;
     p->Cf = Cf;
     p->Lf = p->flanes * Cf;
   }
-  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fused_smem_bytes(p->flanes, p->Cf, k) <= 232448u;
+  const size_t fsmem = p->fws ? fused_ws_smem_bytes(p->Cf, k) : fused_smem_bytes(p->flanes, p->Cf, k);
+  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fsmem <= 232448u;
   if (p->fused_ok) {
-    const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k), 1);
+    const int per = std::max(p->fws ? fused_ws_ctas_per_sm(p->Cf, k) : fused_ctas_per_sm(p->flanes, p->Cf, k), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    const long slots = (long)nsm * per, NG = N / 8;
+    const long slots = (long)nsm * per, NG = N / (p->fws ? 4 : 8);
     // chunks of frequency groups per x-mode: smallest power of two giving >= 90% wave efficiency
     long best = 1;
     double beff = 0.0;
@@ -535,6 +550,12 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
   static const int dbg = getenv("PINT_FUSED_DBG") ? atoi(getenv("PINT_FUSED_DBG")) : 0;   // profiling only
   a.dbg = dbg;
+#ifdef PINT_FUSED_PROF
+  static unsigned long long* prof = nullptr;
+  if (!prof) { cudaMalloc(&prof, 256 * 8); cudaMemset(prof, 0, 256 * 8); }
+  a.prof = prof;
+  p->prof = prof;
+#endif
   return a;
 }
 
@@ -545,7 +566,8 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, a, p->stream));
+  if (p->fws) CUDA_TRY(launch_fused_ws(p->Cf, store_w, a, p->stream));
+  else CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, a, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
   return PINT_OK;

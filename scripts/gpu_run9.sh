@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+PINT_LIB=$PWD/paper_2007_13125_b200/libpint_prof.so timeout 300 python bench.py --no-cpu --no-e2e --steps 3 --warmup 1 > gpurun_out/bench9_prof.json 2> gpurun_out/bench9_prof.err
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:wr_fused_kernel -s 3 -c 1 -o gpurun_out/prof_fused_v5 -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --mx 127 > gpurun_out/ncu_full9.log 2>&1
