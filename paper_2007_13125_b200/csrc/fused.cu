@@ -68,7 +68,7 @@ static int fused_occ_c(int C, int k) {
 int fused_ctas_per_sm(int lanes, int C, int k) { return lanes == 64 ? fused_occ_c<64>(C, k) : fused_occ_c<32>(C, k); }
 
 int fused_rows_per_subchain(int lanes, int C) {
-  const int nsmax = lanes == 32 ? 4 : 2;
+  const int nsmax = lanes == 32 ? PINT_FUSED_NS : 2;
   return C / (C < nsmax ? C : nsmax);
 }
 

@@ -63,6 +63,20 @@ template <int C> __device__ __forceinline__ int swz(int y) {
   return y ^ (((y / C) >> SH) & (CM - 1));
 }
 
+// Row addressing of lane gl's chunk in a swizzled line (swz): y0 + (r ^ m), m constant per lane,
+// so the 8 (or C) distinct low parts are precomputed once and every row is pointer + immediate.
+template <int C> struct SwzRows {
+  static constexpr int CM = C < 8 ? C : 8;
+  double2* p[CM];
+  __device__ __forceinline__ SwzRows(double2* Hl, int gl) {
+    constexpr int SH = C >= 8 ? 0 : (C == 4 ? 1 : (C == 2 ? 2 : 3));
+    const int m = (gl >> SH) & (CM - 1);
+#pragma unroll
+    for (int i = 0; i < CM; ++i) p[i] = Hl + gl * C + (i ^ m);
+  }
+  __device__ __forceinline__ double2& operator[](int r) const { return p[r & (CM - 1)][r & ~(CM - 1)]; }
+};
+
 __device__ __forceinline__ double2 one_minus(double2 u) { return make_double2(1.0 - u.x, -u.y); }
 
 // Recurrence multipliers.  AF = false: the shift-accurate u-form (c = 1 - multiplier, every
@@ -81,9 +95,12 @@ constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 
 // LANES lanes per line: 32 (one warp; default) or 64 (two warps, pair-scoped named barriers);
 // threads per CTA = 8 LANES; LF = LANES C rows per line; NS interleaved sub-chains per lane chunk.
+#ifndef PINT_FUSED_NS
+#define PINT_FUSED_NS 4
+#endif
 template <int LANES> struct FCfg {
   static constexpr int THREADS = FG * LANES;
-  static constexpr int NSMAX = LANES == 32 ? 4 : 2;
+  static constexpr int NSMAX = LANES == 32 ? PINT_FUSED_NS : 2;
 };
 template <int C, int LANES> constexpr int fused_ns() { return C < FCfg<LANES>::NSMAX ? C : FCfg<LANES>::NSMAX; }
 
@@ -109,8 +126,10 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   const int y0 = gl * C;
   const int nv = min(max(L - y0, 0), C);
   double2 d[C];
+  // pad rows y >= L of Hl hold exact zeros (X and the sources vanish there): no load masking
+  const SwzRows<C> rows(Hl, gl);
 #pragma unroll
-  for (int r = 0; r < C; ++r) d[r] = (r < nv) ? Hl[swz<C>(y0 + r)] : make_double2(0.0, 0.0);
+  for (int r = 0; r < C; ++r) d[r] = rows[r];
 
   // ---- forward recurrence f_y = d_y + a f_{y-1} ----
   double2 fs[NS];
@@ -152,8 +171,13 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) {
       st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
-      d[s2 * CS + r] = (s2 * CS + r < nv) ? st[s2] : make_double2(0.0, 0.0);
+      d[s2 * CS + r] = st[s2];
     }
+  if (nv < C) {                                             // the lane holding row L-1: the backward
+#pragma unroll                                              // sweep starts from zero at row L
+    for (int r = 0; r < C; ++r)
+      if (r >= nv) d[r] = make_double2(0.0, 0.0);
+  }
 
   // ---- backward recurrence w_y = f_y + a w_{y+1} ----
 #pragma unroll
@@ -249,7 +273,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     }
   } else {
 #pragma unroll
-    for (int r = 0; r < C; ++r) Hl[swz<C>(y0 + r)] = (r < nv) ? mmul<AF>(u, d[r]) : make_double2(0.0, 0.0);
+    for (int r = 0; r < C; ++r) rows[r] = mmul<AF>(u, d[r]);   // pad rows: never read (finish uses y < L)
   }
 }
 
