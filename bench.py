@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--path", default="fused", choices=["fused", "stream"],
                     help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
+    ap.add_argument("--dst-per-iter", action="store_true",
+                    help="ablation (SURVEY §8(a) A6): DST-x around every S-pass instead of hoisted (streaming)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -211,7 +213,8 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
                      stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
-                     allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"))
+                     allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"),
+                     dst_per_iter=args.dst_per_iter)
     v = torch.from_numpy(prob.v).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(prob.g)).to(dev) if prob.R else None
     plan.set_problem(v, g, prob.phi if prob.R else None, prob.dphi if prob.R else None)
@@ -325,7 +328,7 @@ def main():
                           "grid": f"{prob.mx}x{prob.my}", "N": prob.N, "k": prob.k, "kappa": prob.kappa,
                           "alpha": prob.alpha, "unknowns": total_unknowns,
                           "parallelism": f"x-mode slabs x{world}" if world > 1 else "1 GPU",
-                          "path": "fused" if path["fused"] else "stream",
+                          "path": ("fused" if path["fused"] else "stream") + ("+dst-per-iter" if args.dst_per_iter else ""),
                           "l2": (f"fused: per-iteration working set (X, line constants, window, partials) "
                                  f"{(16 * (8 + 3 * prob.k) * prob.M + 192 * prob.N * prob.M // prob.my) / 1e9:.2f} GB"
                                  " > L2 126 MB, no flush needed" if path["fused"] else

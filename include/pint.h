@@ -62,8 +62,11 @@ enum {
   PINT_FLAG_U0_ZERO = 1,       /* WR initial guess U_0 = 0 instead of U_0^n = v */
   PINT_FLAG_FULL_FFT = 2,      /* heat, streaming path: run the unpruned time FFTs every iteration
                                   (A/B, tests); default prunes to the k window outputs / n_k inputs */
-  PINT_FLAG_STREAM = 4         /* heat: use the two-pass streaming iteration (H and W arrays in HBM)
+  PINT_FLAG_STREAM = 4,        /* heat: use the two-pass streaming iteration (H and W arrays in HBM)
                                   instead of the default fused one-kernel iteration (A/B, tests) */
+  PINT_FLAG_DST_PER_ITER = 8   /* 2D, one rank: ablation of the DST hoisting: keep
+                                  the arrays in physical x and apply DST-x before and after the
+                                  shifted solves every iteration (streaming path; same iterate) */
 };
 
 typedef struct {

@@ -12,7 +12,7 @@
 
 namespace pint {
 
-enum { DST_PHYS_TO_SRC = 0, DST_PHYS_LEVELS_TO_INT = 1, DST_INT_TO_PHYS_LEVELS = 2, DST_ROWS = 3 };
+enum { DST_PHYS_TO_SRC = 0, DST_PHYS_LEVELS_TO_INT = 1, DST_INT_TO_PHYS_LEVELS = 2, DST_ROWS = 3, DST_INT_TO_INT = 4 };
 
 struct DstArgs {
   const double2* in;
@@ -27,7 +27,7 @@ struct DstArgs {
 __device__ __forceinline__ long dst_in_index(const DstArgs& a, int mode, long row, int x) {
   if (mode == DST_PHYS_TO_SRC) return row * a.mx + x;
   if (mode == DST_PHYS_LEVELS_TO_INT) return (row / a.my) * a.M + (row % a.my) * a.mx + x;
-  if (mode == DST_INT_TO_PHYS_LEVELS) {
+  if (mode == DST_INT_TO_PHYS_LEVELS || mode == DST_INT_TO_INT) {
     const long nl = row / a.my, y = row % a.my;
     return (((long)x * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;
   }
@@ -47,6 +47,10 @@ __device__ __forceinline__ long dst_out_index(const DstArgs& a, int mode, long r
     return ((ql * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;
   }
   if (mode == DST_INT_TO_PHYS_LEVELS) return (row / a.my) * a.M + (row % a.my) * a.mx + q;
+  if (mode == DST_INT_TO_INT) {   // tile layout, x index -> mode index (per-iteration DST ablation)
+    const long nl = row / a.my, y = row % a.my;
+    return (((long)q * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;
+  }
   return row * a.mx + q;
 }
 
@@ -90,7 +94,9 @@ __global__ void __launch_bounds__(TPB) dst_kernel(const DstArgs a, int mode) {
 }
 
 // ---- plain gathers (1D layouts, modal slab export) ----
-enum { RM_1D_LEVELS_TO_INT = 0, RM_INT_TO_1D_LEVELS = 1, RM_INT_TO_MODAL = 2, RM_1D_TO_SRC = 3 };
+enum { RM_1D_LEVELS_TO_INT = 0, RM_INT_TO_1D_LEVELS = 1, RM_INT_TO_MODAL = 2, RM_1D_TO_SRC = 3,
+       // 2D physical-x layouts (no DST: per-iteration DST ablation, PINT_FLAG_DST_PER_ITER)
+       RM_2D_PHYS_TO_SRC = 4, RM_2D_LEVELS_TO_INT = 5, RM_INT_TO_2D_LEVELS = 6 };
 struct RemapArgs {
   const double2* in;
   double2* out;
@@ -110,6 +116,12 @@ __global__ void remap_kernel(const RemapArgs a, int mode) {
     } else if (mode == RM_INT_TO_MODAL) {
       const long ql = e % a.Qb, r = e / a.Qb, y = r % a.my, nl = r / a.my;
       a.out[e] = a.in[((ql * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB];
+    } else if (mode == RM_2D_PHYS_TO_SRC || mode == RM_2D_LEVELS_TO_INT || mode == RM_INT_TO_2D_LEVELS) {
+      const long mx = a.M / a.my;
+      const long nl = e / a.M, r = e % a.M, y = r / mx, x = r % mx;
+      if (mode == RM_2D_PHYS_TO_SRC) a.out[(x * a.NB + y / a.WB) * a.WB + y % a.WB] = a.in[e];
+      else if (mode == RM_2D_LEVELS_TO_INT) a.out[((x * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB] = a.in[e];
+      else a.out[e] = a.in[((x * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB];
     } else {  // RM_1D_TO_SRC: src tile layout [NB][WB] of one vector == identity with padding
       a.out[e] = a.in[e];
     }

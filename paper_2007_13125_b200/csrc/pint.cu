@@ -162,6 +162,7 @@ struct pint_plan_s {
   double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
   // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
+  bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
@@ -300,6 +301,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (nranks > 1 && op->kind == PINT_OP_FD1D_DIRICHLET)
     return fail(PINT_ERR_ARG, "1D operators do not shard (replicas only): nranks must be 1");
   if (nranks > op->mx) return fail(PINT_ERR_ARG, "nranks must be <= mx");
+  if (opt && (opt->flags & PINT_FLAG_DST_PER_ITER) && (op->kind != PINT_OP_FD2D_DIRICHLET || nranks != 1))
+    return fail(PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator on one rank");
   if (nranks > 1 && !(opt && opt->allreduce_max)) return fail(PINT_ERR_ARG, "nranks > 1 needs allreduce_max");
   if (!is_pow2(N) || N < 16 || N > 4096) return fail(PINT_ERR_UNSUPPORTED, "N must be a power of two in [16, 4096]");
   const int dim = op->kind == PINT_OP_FD1D_DIRICHLET ? 1 : 2;
@@ -388,7 +391,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     p->Lf = p->flanes * Cf;
   }
   const size_t fsmem = p->fws ? fused_ws_smem_bytes(p->Cf, k) : fused_smem_bytes(p->flanes, p->Cf, k);
-  p->fused_ok = alpha == 1.0 && !(p->flags & PINT_FLAG_STREAM) && fsmem <= 232448u;
+  p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
+  p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u;
   if (p->fused_ok) {
     const int per = std::max(p->fws ? fused_ws_ctas_per_sm(p->Cf, k) : fused_ctas_per_sm(p->flanes, p->Cf, k), 1);
     int nsm = 148;
@@ -609,6 +613,14 @@ static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
     CUDA_TRY(cudaMemcpyAsync(dst, phys_vec, p->M * sizeof(double2), cudaMemcpyDeviceToDevice, p->stream));
     return PINT_OK;
   }
+  if (p->dst_iter) {   // physical x: plain gather into the tile layout
+    RemapArgs r{};
+    r.in = phys_vec; r.out = dst; r.count = p->M; r.WB = p->WB; r.my = (int)p->my; r.NB = p->NB;
+    r.N = p->N; r.n0 = 0; r.M = p->M; r.Qb = p->Qb;
+    CUDA_TRY(launch_remap(r, RM_2D_PHYS_TO_SRC, p->stream));
+    ++p->launches;
+    return PINT_OK;
+  }
   DstArgs a = dargs(p);
   a.in = phys_vec; a.out = dst; a.rows = p->my;
   CUDA_TRY(launch_dst(p->NE, a, DST_PHYS_TO_SRC, p->stream));
@@ -753,6 +765,11 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
     r.in = p->B; r.out = p->A; r.count = p->N * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
     r.N = p->N; r.n0 = 0; r.M = p->M; r.Qb = 1;
     CUDA_TRY(launch_remap(r, RM_1D_LEVELS_TO_INT, p->stream));
+  } else if (p->dst_iter) {
+    RemapArgs r{};
+    r.in = p->B; r.out = p->A; r.count = p->N * p->M; r.WB = p->WB; r.my = (int)p->my; r.NB = p->NB;
+    r.N = p->N; r.n0 = 0; r.M = p->M; r.Qb = p->Qb;
+    CUDA_TRY(launch_remap(r, RM_2D_LEVELS_TO_INT, p->stream));
   } else {
     DstArgs a = dargs(p);
     a.in = p->B; a.out = p->A; a.rows = p->N * p->my; a.n0 = 0;
@@ -789,7 +806,19 @@ static pint_status iterate_async(pint_plan p) {
     p->stateA = 0;
   }
   CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
-  TRY(spass(p, p->A, p->B));                                             // W_{m+1} = solve(H_{m+1})
+  if (p->dst_iter) {
+    // ablation: H (physical x) -DST-> B, solve B -> A, W -DST-> B (physical x again)
+    DstArgs d = dargs(p);
+    d.rows = p->N * p->my; d.n0 = 0;
+    d.in = p->A; d.out = p->B;
+    CUDA_TRY(launch_dst(p->NE, d, DST_INT_TO_INT, p->stream));
+    TRY(spass(p, p->B, p->A));
+    d.in = p->A; d.out = p->B;
+    CUDA_TRY(launch_dst(p->NE, d, DST_INT_TO_INT, p->stream));
+    p->launches += 2;
+  } else {
+    TRY(spass(p, p->A, p->B));                                           // W_{m+1} = solve(H_{m+1})
+  }
   TRY(tpass(p, IN_FREQ, OUT_H, p->B, p->A, p->wrap[p->wcur], p->wrap[1 - p->wcur], true));  // -> H_{m+2}
   p->wcur ^= 1;
   ++p->m;
@@ -879,6 +908,11 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
       r.in = p->wrap[p->wcur]; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
       r.N = p->k; r.n0 = n_begin - (p->N - p->k); r.M = p->M; r.Qb = 1;
       CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
+    } else if (p->dst_iter) {
+      RemapArgs r{};
+      r.in = p->wrap[p->wcur]; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = (int)p->my;
+      r.NB = p->NB; r.N = p->k; r.n0 = n_begin - (p->N - p->k); r.M = p->M; r.Qb = p->Qb;
+      CUDA_TRY(launch_remap(r, RM_INT_TO_2D_LEVELS, p->stream));
     } else {
       DstArgs a = dargs(p);
       a.in = p->wrap[p->wcur]; a.out = wdst; a.rows = n_count * p->my; a.N = p->k; a.n0 = n_begin - (p->N - p->k);
@@ -897,6 +931,11 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
     r.in = p->A; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
     r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = 1;
     CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
+  } else if (p->dst_iter) {
+    RemapArgs r{};
+    r.in = p->A; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = (int)p->my; r.NB = p->NB;
+    r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = p->Qb;
+    CUDA_TRY(launch_remap(r, RM_INT_TO_2D_LEVELS, p->stream));
   } else {
     DstArgs a = dargs(p);
     a.in = p->A; a.out = dst; a.rows = n_count * p->my; a.n0 = n_begin;
@@ -918,6 +957,7 @@ extern "C" pint_status pint_get_modal_levels(pint_plan p, int64_t n_begin, int64
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (p->dim != 2) return fail(PINT_ERR_ARG, "modal levels exist for 2D operators only");
+  if (p->dst_iter) return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_DST_PER_ITER keeps physical x: use pint_get_levels");
   if (n_begin < 0 || n_count < 0 || n_begin + n_count > p->N) return fail(PINT_ERR_ARG, "levels out of range [0, N)");
   if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");

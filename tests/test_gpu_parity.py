@@ -298,3 +298,28 @@ def test_forcing_pulse_path_selection(pint, nlev, fused):
             p.iterate()
         errs.append(rel(p.get_solution(), o[3]))
     assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("mx,my,N,k,kappa,alpha,R", [
+    (31, 40, 64, 3, 0.1, 1.0, 1),        # heat, dense-in-time forcing
+    (63, 33, 128, 2, 0.05, 0.5, 1),      # CQ subdiffusion
+    (127, 100, 256, 6, 0.01, 1.0, 0),    # heat, BDF6
+])
+def test_dst_per_iteration_ablation(pint, mx, my, N, k, kappa, alpha, R):
+    """the DST-x applied before and after the shifted solves every iteration
+    (PINT_FLAG_DST_PER_ITER, physical-x arrays) gives the iterate of the hoisted default, read
+    after every m and unread, and both match the oracle."""
+    prob = inputs.random_complex_problem(mx, my, N, k, kappa, alpha, R=R, seed=3 * mx + my)
+    o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
+    hoisted, _ = gpu_iterates(pint, prob, 3)
+    per_iter, _ = gpu_iterates(pint, prob, 3, dst_per_iter=True)
+    for m in range(3):
+        assert rel(per_iter[m], hoisted[m]) < 1e-12
+        assert rel(per_iter[m], o[m + 1]) < TOL
+    with pint.Plan.from_problem(prob, dst_per_iter=True) as p:
+        assert not p.path()["fused"]
+        for _ in range(3):
+            p.iterate()
+        win = p.get_levels(N - k, k)
+        assert rel(p.get_solution(), o[3]) < TOL
+        assert np.linalg.norm(win - o[3][N - k:]) / np.linalg.norm(o[3]) < TOL
