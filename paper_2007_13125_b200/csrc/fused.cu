@@ -4,68 +4,70 @@
 
 namespace pint {
 
-size_t fused_smem_bytes(int lanes, int C, int k) {
-  return (size_t)(FG + k) * lanes * C * sizeof(double2) + 8 * sizeof(LineConst) + 8 * 4 * sizeof(double2);
+size_t fused_smem_bytes(int lanes, int C, int k, bool tm) {
+  return (size_t)(FG + (tm ? 0 : k)) * lanes * C * sizeof(double2) + 8 * sizeof(LineConst) + 8 * 4 * sizeof(double2);
 }
 
-template <int C, int LANES, bool SW>
+template <int C, int LANES, bool SW, bool TM>
 static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
-  auto kern = wr_fused_kernel<C, LANES, SW>;
-  const size_t smem = fused_smem_bytes(LANES, C, a.k);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  auto kern = wr_fused_kernel<C, LANES, SW, TM>;
+  const size_t smem = fused_smem_bytes(LANES, C, a.k, TM && !SW) + (a.xs ? (size_t)a.nk * LANES * C * sizeof(double2) : 0);
+  // set on every launch: the occupancy query at plan creation (fused_occ) also sets this attribute
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   if (grid <= 0) return cudaSuccess;
   kern<<<(unsigned)grid, FCfg<LANES>::THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int LANES, bool SW>
+template <int LANES, bool SW, bool TM>
 static cudaError_t fused_c(int C, const FusedArgs& a, long grid, cudaStream_t st) {
   switch (C) {
-    case 1: return fused_go<1, LANES, SW>(a, grid, st);
-    case 2: return fused_go<2, LANES, SW>(a, grid, st);
-    case 4: return fused_go<4, LANES, SW>(a, grid, st);
-    case 8: return fused_go<8, LANES, SW>(a, grid, st);
-    case 16: return fused_go<16, LANES, SW>(a, grid, st);
-    case 32: if constexpr (LANES == 32) return fused_go<32, LANES, SW>(a, grid, st);
+    case 1: return fused_go<1, LANES, SW, TM>(a, grid, st);
+    case 2: return fused_go<2, LANES, SW, TM>(a, grid, st);
+    case 4: return fused_go<4, LANES, SW, TM>(a, grid, st);
+    case 8: return fused_go<8, LANES, SW, TM>(a, grid, st);
+    case 16: return fused_go<16, LANES, SW, TM>(a, grid, st);
+    case 32: if constexpr (LANES == 32) return fused_go<32, LANES, SW, TM>(a, grid, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_fused(int lanes, int C, bool store_w, const FusedArgs& a, cudaStream_t st) {
+cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st) {
   const long grid = a.Qb * a.nch;
-  if (lanes == 64) return store_w ? fused_c<64, true>(C, a, grid, st) : fused_c<64, false>(C, a, grid, st);
-  return store_w ? fused_c<32, true>(C, a, grid, st) : fused_c<32, false>(C, a, grid, st);
+  if (store_w) return lanes == 64 ? fused_c<64, true, false>(C, a, grid, st) : fused_c<32, true, false>(C, a, grid, st);
+  if (lanes == 64) return tm ? fused_c<64, false, true>(C, a, grid, st) : fused_c<64, false, false>(C, a, grid, st);
+  return tm ? fused_c<32, false, true>(C, a, grid, st) : fused_c<32, false, false>(C, a, grid, st);
 }
 
 template <int C, int LANES>
-static int fused_occ(int k) {
+static int fused_occ(int k, bool tm) {
   int per = 0;
-  const size_t smem = fused_smem_bytes(LANES, C, k);
-  auto kern = wr_fused_kernel<C, LANES, false>;
+  const size_t smem = fused_smem_bytes(LANES, C, k, tm);
+  auto kern = tm ? wr_fused_kernel<C, LANES, false, true> : wr_fused_kernel<C, LANES, false, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FCfg<LANES>::THREADS, smem) != cudaSuccess) return 0;
   return per;
 }
 
 template <int LANES>
-static int fused_occ_c(int C, int k) {
+static int fused_occ_c(int C, int k, bool tm) {
   switch (C) {
-    case 1: return fused_occ<1, LANES>(k);
-    case 2: return fused_occ<2, LANES>(k);
-    case 4: return fused_occ<4, LANES>(k);
-    case 8: return fused_occ<8, LANES>(k);
-    case 16: return fused_occ<16, LANES>(k);
-    case 32: if constexpr (LANES == 32) return fused_occ<32, LANES>(k);
+    case 1: return fused_occ<1, LANES>(k, tm);
+    case 2: return fused_occ<2, LANES>(k, tm);
+    case 4: return fused_occ<4, LANES>(k, tm);
+    case 8: return fused_occ<8, LANES>(k, tm);
+    case 16: return fused_occ<16, LANES>(k, tm);
+    case 32: if constexpr (LANES == 32) return fused_occ<32, LANES>(k, tm);
   }
   return 0;
 }
 
-int fused_ctas_per_sm(int lanes, int C, int k) { return lanes == 64 ? fused_occ_c<64>(C, k) : fused_occ_c<32>(C, k); }
+// one CTA per SM at most when the window sums live in TMEM (each CTA allocates its columns)
+int fused_ctas_per_sm(int lanes, int C, int k, bool tm) {
+  const int per = lanes == 64 ? fused_occ_c<64>(C, k, tm) : fused_occ_c<32>(C, k, tm);
+  return tm ? (per > 1 ? 1 : per) : per;
+}
 
 int fused_rows_per_subchain(int lanes, int C) {
   const int nsmax = lanes == 32 ? PINT_FUSED_NS : 2;

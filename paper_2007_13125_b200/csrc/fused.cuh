@@ -50,6 +50,7 @@ struct FusedArgs {
   long N, Qb;
   int L, Lf, Lpad, WB, NB, k, nk, ndense, nch, gpc;
   unsigned long long* prof; // profiling builds (-DPINT_FUSED_PROF): cycles per phase, total + per warp
+  int xs;                  // 1: X of the CTA's x-mode staged once into shared memory (TMEM variant, nk small)
   int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
                            // 8 u-form recurrences on every line
 };
@@ -277,12 +278,44 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   }
 }
 
+// ---- Tensor memory (TMEM) for the window partial sums --------------------------------------
+// Each row thread keeps its acc[rr][r] (window slots r = 2..7 <-> level n = N - 8 + r) in its TMEM
+// lane: warp w reads/writes lanes 32 (w % 4) .. + 31; column block (w / 4) * RPT * 24 + rr * 24.
+// 24 32-bit columns per row = 6 complex doubles.  This frees 96 KB of shared memory bandwidth per
+// group (the RMW of 6 partial sums per row) onto the otherwise idle TMEM datapath.
+__device__ __forceinline__ void tmem_ld24(uint32_t addr, uint32_t (&w)[24]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                 "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+               : "r"(addr));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23])
+               : "r"(addr + 16));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st24(uint32_t addr, const uint32_t (&w)[24]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+               :: "r"(addr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                  "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]) : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+               :: "r"(addr + 16), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]),
+                  "r"(w[23]) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ double2 tw_get(const uint32_t (&w)[24], int s) {
+  return make_double2(__hiloint2double((int)w[4 * s + 1], (int)w[4 * s]), __hiloint2double((int)w[4 * s + 3], (int)w[4 * s + 2]));
+}
+__device__ __forceinline__ void tw_put(uint32_t (&w)[24], int s, double2 v) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(v.x), b = (unsigned long long)__double_as_longlong(v.y);
+  w[4 * s] = (uint32_t)a; w[4 * s + 1] = (uint32_t)(a >> 32); w[4 * s + 2] = (uint32_t)b; w[4 * s + 3] = (uint32_t)(b >> 32);
+}
+
 // Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
 // next synthesis and the group's twiddles are issued first (one memory round trip), then each row
 // reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
-template <int C, int LANES, bool WINDOW>
+template <int C, int LANES, bool WINDOW, bool TM = false>
 __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, double2* acc, const double2* Xq,
-                                           long q, int i, bool next) {
+                                           long q, int i, bool next, uint32_t tacc = 0) {
   constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
   constexpr int RPT = LF >= T ? LF / T : 1;
   const int N = (int)a.N, k = a.k, nk = a.nk;
@@ -314,10 +347,19 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2) x[s2] = Hs[s2 * LF + swz<C>(y)];
       dft8<+1>(x);                                       // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
+      if constexpr (TM) {
+        uint32_t w[24];                                  // slots r = 2..7 of this row
+        tmem_ld24(tacc + 24 * rr, w);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int j = r - 8 + k;
-        if (j >= 0) acc[j * LF + y] = cfma(x[r], tww[r], acc[j * LF + y]);
+        for (int r = 2; r < 8; ++r)
+          if (r - 8 + k >= 0) tw_put(w, r - 2, cfma(x[r], tww[r], tw_get(w, r - 2)));
+        tmem_st24(tacc + 24 * rr, w);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int j = r - 8 + k;
+          if (j >= 0) acc[j * LF + y] = cfma(x[r], tww[r], acc[j * LF + y]);
+        }
       }
     }
     if (next && !(a.dbg & 4)) {
@@ -509,23 +551,60 @@ __global__ void __launch_bounds__(WS_THREADS, 1) wr_fused_ws_kernel(const FusedA
   }
 }
 // grid = Qb * nch CTAs; CTA (q, ch) runs frequency groups [ch*gpc, (ch+1)*gpc) of x-mode q.
-template <int C, int LANES, bool STORE_W>
+template <int C, int LANES> struct FTmem {
+  static constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
+  static constexpr int RPT = LF >= T ? LF / T : 1;
+  static constexpr int NEED = (T / 128) * RPT * 24;          // columns
+  static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+};
+
+// TM: window partial sums in tensor memory (default) instead of shared memory.
+template <int C, int LANES, bool STORE_W, bool TM>
 __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const FusedArgs a) {
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
+  constexpr bool TMA = TM && !STORE_W;                  // TMEM accumulators in use
+  __shared__ uint32_t tbase;
   double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
-  double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums
-  LineConst* slc = (LineConst*)(acc + a.k * LF);       // [8]      line constants of the group
+  double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums (shared-memory variant)
+  LineConst* slc = (LineConst*)(acc + (TMA ? 0 : a.k * LF));   // [8] line constants of the group
   double2* xch = (double2*)(slc + 8);                  // [8][4]   pair exchange (LANES = 64)
+  double2* Xs = xch + 32;                              // [nk][LF] X of this x-mode (a.xs)
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
   const int NG = (int)(a.N / FG);
   const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NG);
   const int warp = threadIdx.x >> 5;
   const int line = LANES == 64 ? warp >> 1 : warp, half = LANES == 64 ? warp & 1 : 0;
-  const double2* Xq = a.X + q * 8 * LF;
+  const double2* Xg = a.X + q * 8 * LF;
+  const double2* Xq = Xg;
+  if (a.xs) {   // X is the same for every frequency group of this x-mode: stage it once
+    for (int e = threadIdx.x; e < a.nk * LF; e += FCfg<LANES>::THREADS) cp_async16(&Xs[e], &Xg[e]);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    cp_async_wait0();
+    __syncthreads();
+    Xq = Xs;
+  }
+  uint32_t tacc = 0;
+  if constexpr (TMA) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                   :: "r"((uint32_t)__cvta_generic_to_shared(&tbase)), "n"(FTmem<C, LANES>::COLS) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * FTmem<C, LANES>::RPT * 24);
+    uint32_t z[24];
+#pragma unroll
+    for (int j = 0; j < 24; ++j) z[j] = 0u;
+#pragma unroll
+    for (int rr = 0; rr < FTmem<C, LANES>::RPT; ++rr) tmem_st24(tacc + 24 * rr, z);
+    tmem_wait_st();
+  }
   fused_stage_lc(a, slc, q, g0);
-  if (!STORE_W)
+  if (!STORE_W && !TMA)
     for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
       for (int j = 0; j < a.k; ++j) acc[j * LF + y] = make_double2(0.0, 0.0);
   fused_rows<C, LANES, false>(a, Hs, acc, Xq, q, g0 - 1, true);   // synthesise group g0
@@ -551,7 +630,8 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     PINT_TS(t2);
     const bool next = i + 1 < g1;
     if (next) fused_stage_lc(a, slc, q, i + 1);
-    fused_rows<C, LANES, !STORE_W>(a, Hs, acc, Xq, q, i, next);
+    fused_rows<C, LANES, !STORE_W, TMA>(a, Hs, acc, Xq, q, i, next, tacc);
+    if constexpr (TMA) tmem_wait_st();
     cp_async_wait0();
     PINT_TS(t3);
     __syncthreads();
@@ -571,8 +651,28 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
 #endif
   if (!STORE_W) {
     double2* P = a.P + ((q * a.nch + ch) * a.k) * LF;
-    for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
-      for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
+    if constexpr (TMA) {
+#pragma unroll
+      for (int rr = 0; rr < FTmem<C, LANES>::RPT; ++rr) {
+        const int y = threadIdx.x + FCfg<LANES>::THREADS * rr;
+        if (LF < FCfg<LANES>::THREADS && y >= LF) break;          // warp-uniform (LF % 32 == 0)
+        uint32_t w[24];
+        tmem_ld24(tacc + 24 * rr, w);
+#pragma unroll
+        for (int r = 2; r < 8; ++r) {
+          const int j = r - 8 + a.k;
+          if (j >= 0) P[j * LF + y] = tw_get(w, r - 2);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncthreads();
+      if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n"
+                     :: "r"(tbase), "n"(FTmem<C, LANES>::COLS) : "memory");
+    } else {
+      for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
+        for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
+    }
   }
 }
 

@@ -22,10 +22,10 @@ cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double
 cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st);
 // fused heat iteration (fused.cu): one CTA per (x-mode, group chunk); lanes (32 | 64) per line,
 // C rows per lane
-size_t fused_smem_bytes(int lanes, int C, int k);
-int fused_ctas_per_sm(int lanes, int C, int k);
+size_t fused_smem_bytes(int lanes, int C, int k, bool tm);
+int fused_ctas_per_sm(int lanes, int C, int k, bool tm);
 int fused_rows_per_subchain(int lanes, int C);
-cudaError_t launch_fused(int lanes, int C, bool store_w, const FusedArgs& a, cudaStream_t st);
+cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st);
 // warp-specialised radix-4 pipeline (default): 32 lanes per line
 size_t fused_ws_smem_bytes(int C, int k);
 int fused_ws_ctas_per_sm(int C, int k);

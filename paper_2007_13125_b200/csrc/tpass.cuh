@@ -23,7 +23,7 @@ namespace pint {
 #define PINT_PRUNED_MINB 3
 #endif
 #ifndef PINT_CQ_MINB
-#define PINT_CQ_MINB 1
+#define PINT_CQ_MINB 2
 #endif
 #ifndef PINT_TPASS_MINB
 #define PINT_TPASS_MINB 2

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu18.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu18.log
+timeout 300 python bench.py --no-cpu --no-e2e --steps 10 > gpurun_out/bench18_xs.json 2> gpurun_out/bench18_xs.err
+PINT_FUSED_NO_XS=1 timeout 300 python bench.py --no-cpu --no-e2e --steps 10 > gpurun_out/bench18_noxs.json 2> gpurun_out/bench18_noxs.err
