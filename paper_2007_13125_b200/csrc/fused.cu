@@ -74,65 +74,6 @@ int fused_rows_per_subchain(int lanes, int C) {
   return C / (C < nsmax ? C : nsmax);
 }
 
-size_t fused_ws_smem_bytes(int C, int k) {
-  return (size_t)(2 * WS_LINES + k) * 32 * C * sizeof(double2) + 2 * WS_LINES * sizeof(LineConst);
-}
-
-template <int C, bool SW>
-static cudaError_t ws_go(const FusedArgs& a, long grid, cudaStream_t st) {
-  auto kern = wr_fused_ws_kernel<C, SW>;
-  const size_t smem = fused_ws_smem_bytes(C, a.k);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, WS_THREADS, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <bool SW>
-static cudaError_t ws_c(int C, const FusedArgs& a, long grid, cudaStream_t st) {
-  switch (C) {
-    case 1: return ws_go<1, SW>(a, grid, st);
-    case 2: return ws_go<2, SW>(a, grid, st);
-    case 4: return ws_go<4, SW>(a, grid, st);
-    case 8: return ws_go<8, SW>(a, grid, st);
-    case 16: return ws_go<16, SW>(a, grid, st);
-    case 32: return ws_go<32, SW>(a, grid, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_fused_ws(int C, bool store_w, const FusedArgs& a, cudaStream_t st) {
-  const long grid = a.Qb * a.nch;
-  return store_w ? ws_c<true>(C, a, grid, st) : ws_c<false>(C, a, grid, st);
-}
-
-template <int C>
-static int ws_occ(int k) {
-  int per = 0;
-  const size_t smem = fused_ws_smem_bytes(C, k);
-  auto kern = wr_fused_ws_kernel<C, false>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, WS_THREADS, smem) != cudaSuccess) return 0;
-  return per;
-}
-
-int fused_ws_ctas_per_sm(int C, int k) {
-  switch (C) {
-    case 1: return ws_occ<1>(k);
-    case 2: return ws_occ<2>(k);
-    case 4: return ws_occ<4>(k);
-    case 8: return ws_occ<8>(k);
-    case 16: return ws_occ<16>(k);
-    case 32: return ws_occ<32>(k);
-  }
-  return 0;
-}
-
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st) {
   const long total = a.Qb * a.Lf;
   const long blocks = std::min<long>((total + TPB - 1) / TPB, 148L * 8);

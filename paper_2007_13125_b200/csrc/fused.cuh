@@ -393,90 +393,6 @@ __device__ __forceinline__ void fused_stage_lc(const FusedArgs& a, LineConst* sl
 }
 
 
-// =============================================================================================
-// Warp-specialised pipeline (default): radix-4 frequency groups p = i + (N/4) s, s < 4.
-// Warps 0-3 solve the 4 lines of group i in buffer i&1 while warps 4-7 (row workers) reduce
-// group i-1 into the window and synthesise group i+1 in the other buffer; one barrier per step.
-// The solves and the row work overlap on every SM sub-partition (one solver and one row warp each).
-// =============================================================================================
-constexpr int WS_LINES = 4;                 // lines per group (radix)
-constexpr int WS_THREADS = 256;             // 4 solver warps + 4 row-worker warps
-constexpr int WS_ROWT = 128;                // row-worker threads
-
-size_t fused_ws_smem_bytes(int C, int k);
-
-// line constants of group i (4 lines, stride N/4) -> shared memory (row-worker threads)
-__device__ __forceinline__ void ws_stage_lc(const FusedArgs& a, LineConst* slc, long q, int i, int rt) {
-  const int NG = (int)(a.N / WS_LINES);
-  if (rt < WS_LINES * 15) {
-    const int line = rt / 15, c = rt % 15;
-    const char* src = (const char*)(a.lc + q * a.N + i + (long)NG * line) + 16 * c;
-    cp_async16((char*)(slc + line) + 16 * c, src);
-  }
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-
-// Row work of one step (row-worker thread rt, rows y = rt + 128 r): window of group iw (if
-// iw >= 0) then synthesis of group is (if is >= 0), in place in buffer Hb [4][LF].
-template <int C>
-__device__ __forceinline__ void ws_rows(const FusedArgs& a, double2* Hb, double2* acc, const double2* Xq, long q,
-                                        int iw, int is, int rt) {
-  constexpr int LF = 32 * C;
-  constexpr int RPT = LF >= WS_ROWT ? LF / WS_ROWT : 1;
-  const int N = (int)a.N, k = a.k, nk = a.nk;
-  const int NG = N / WS_LINES;
-  // twiddles of this step: window e^{+2 pi i n iw/N} for n = N-k+j; synthesis w_N^{t is}
-  double2 tww[6], tws[8];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    double2 w = (iw >= 0 && j < k) ? __ldg(&a.tw[((N - k + j) * iw) & (N - 1)]) : make_double2(0.0, 0.0);
-    w.y = -w.y;
-    tww[j] = w;
-  }
-#pragma unroll
-  for (int t = 0; t < 8; ++t) tws[t] = (is >= 0 && t > 0 && t < nk) ? __ldg(&a.tw[(t * is) & (N - 1)]) : make_double2(1.0, 0.0);
-#pragma unroll 2
-  for (int rr = 0; rr < RPT; ++rr) {
-    const int y = rt + WS_ROWT * rr;
-    if (LF < WS_ROWT && y >= LF) break;
-    double2 xv[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) xv[t] = (is >= 0 && t < nk) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
-    if (iw >= 0 && !(a.dbg & 2)) {
-      double2 x0 = Hb[0 * LF + swz<C>(y)], x1 = Hb[1 * LF + swz<C>(y)];
-      double2 x2 = Hb[2 * LF + swz<C>(y)], x3 = Hb[3 * LF + swz<C>(y)];
-      dft4<+1>(x0, x1, x2, x3);                          // Y_r = sum_s e^{+2 pi i rs/4} W_{iw + (N/4) s}
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        if (j < k) {
-          const int r = (j - k + 8) & 3;                 // (N - k + j) mod 4
-          const double2 Y = r == 0 ? x0 : (r == 1 ? x1 : (r == 2 ? x2 : x3));
-          acc[j * LF + y] = cfma(Y, tww[j], acc[j * LF + y]);
-        }
-      }
-    }
-    if (is >= 0 && !(a.dbg & 4)) {
-#pragma unroll
-      for (int t = 1; t < 8; ++t) xv[t] = cmul(xv[t], tws[t]);          // X_t w_N^{t is}
-      double2 z0 = cadd(xv[0], xv[4]), z1 = cadd(xv[1], xv[5]), z2 = cadd(xv[2], xv[6]), z3 = cadd(xv[3], xv[7]);
-      dft4<-1>(z0, z1, z2, z3);                          // H_{is + (N/4) s} = sum_t (.) e^{-2 pi i ts/4}
-      for (int dd = 0; dd < a.ndense; ++dd) {
-        const double2 g = y < a.L ? __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * a.Qb + q) * a.Lpad + y])
-                                  : make_double2(0.0, 0.0);
-        const double2* ch = a.chat + (long)dd * N + is;
-        z0 = cfma(__ldg(&ch[0]), g, z0);
-        z1 = cfma(__ldg(&ch[NG]), g, z1);
-        z2 = cfma(__ldg(&ch[2 * NG]), g, z2);
-        z3 = cfma(__ldg(&ch[3 * NG]), g, z3);
-      }
-      Hb[0 * LF + swz<C>(y)] = z0;
-      Hb[1 * LF + swz<C>(y)] = z1;
-      Hb[2 * LF + swz<C>(y)] = z2;
-      Hb[3 * LF + swz<C>(y)] = z3;
-    }
-  }
-}
-
 // ---- finish: window of U_{m+1}, update monitor, X for the next iteration ----
 enum { FIN_PARTIALS = 0, FIN_FROM_WRAP = 1, FIN_FROM_V = 2, FIN_ZERO = 3 };
 
@@ -498,59 +414,6 @@ struct FinishArgs {
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
 
-// grid = Qb * nch CTAs; CTA (q, ch) runs radix-4 groups [ch*gpc, (ch+1)*gpc) of x-mode q.
-template <int C, bool STORE_W>
-__global__ void __launch_bounds__(WS_THREADS, 1) wr_fused_ws_kernel(const FusedArgs a) {
-  extern __shared__ double2 fsm[];
-  constexpr int LF = 32 * C;
-  double2* Hs = fsm;                                   // [2][4][LF]  double-buffered group lines
-  double2* acc = fsm + 2 * WS_LINES * LF;              // [k][LF]     window partial sums
-  LineConst* slc = (LineConst*)(acc + a.k * LF);       // [2][4]      line constants
-  const long q = blockIdx.x / a.nch;
-  const int ch = blockIdx.x % a.nch;
-  const int NG = (int)(a.N / WS_LINES);
-  const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NG);
-  const int T = g1 - g0;
-  const int warp = threadIdx.x >> 5;
-  const bool solver = warp < WS_LINES;
-  const int rt = threadIdx.x - 32 * WS_LINES;          // row-worker thread index
-  const double2* Xq = a.X + q * 8 * LF;
-  if (!solver) {
-    if (!STORE_W)
-      for (int y = rt; y < LF; y += WS_ROWT)
-        for (int j = 0; j < a.k; ++j) acc[j * LF + y] = make_double2(0.0, 0.0);
-    ws_stage_lc(a, slc, q, g0, rt);
-    ws_rows<C>(a, Hs, acc, Xq, q, -1, g0, rt);
-    cp_async_wait0();
-  }
-  __syncthreads();
-  for (int t = 0; t <= T; ++t) {
-    if (solver) {
-      if (t < T && !(a.dbg & 1)) {
-        const int b = t & 1;
-        const LineConst& lcl = slc[b * WS_LINES + warp];
-        double2* Hl = Hs + (b * WS_LINES + warp) * LF;
-        const long p = g0 + t + (long)NG * warp;
-        if (cabs2(lcl.u) >= FUSED_AF_U2 && !(a.dbg & 8)) fused_solve<C, 32, STORE_W, true>(a, Hl, lcl, nullptr, q, p, 0, 0);
-        else fused_solve<C, 32, STORE_W, false>(a, Hl, lcl, nullptr, q, p, 0, 0);
-      }
-    } else {
-      const int b = (t + 1) & 1;                       // buffer of groups t-1 (window) and t+1 (synthesis)
-      const int iw = (t >= 1 && !STORE_W) ? g0 + t - 1 : -1;
-      const int is = (t + 1 < T) ? g0 + t + 1 : -1;
-      if (is >= 0) ws_stage_lc(a, slc + b * WS_LINES, q, is, rt);
-      if (iw >= 0 || is >= 0) ws_rows<C>(a, Hs + b * WS_LINES * LF, acc, Xq, q, iw, is, rt);
-      cp_async_wait0();
-    }
-    __syncthreads();
-  }
-  if (!STORE_W) {
-    double2* P = a.P + ((q * a.nch + ch) * a.k) * LF;
-    for (int y = threadIdx.x; y < LF; y += WS_THREADS)
-      for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
-  }
-}
-// grid = Qb * nch CTAs; CTA (q, ch) runs frequency groups [ch*gpc, (ch+1)*gpc) of x-mode q.
 template <int C, int LANES> struct FTmem {
   static constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
   static constexpr int RPT = LF >= T ? LF / T : 1;

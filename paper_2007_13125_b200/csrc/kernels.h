@@ -26,10 +26,6 @@ size_t fused_smem_bytes(int lanes, int C, int k, bool tm);
 int fused_ctas_per_sm(int lanes, int C, int k, bool tm);
 int fused_rows_per_subchain(int lanes, int C);
 cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st);
-// warp-specialised radix-4 pipeline (default): 32 lanes per line
-size_t fused_ws_smem_bytes(int C, int k);
-int fused_ws_ctas_per_sm(int C, int k);
-cudaError_t launch_fused_ws(int C, bool store_w, const FusedArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int CS,
                               int L, cudaStream_t st);

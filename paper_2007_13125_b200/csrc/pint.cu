@@ -168,7 +168,6 @@ struct pint_plan_s {
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
   int flanes = 32;            // fused kernel lanes per line: 32 (one warp) or 64 (PINT_FUSED_LANES=64, radix-8 only)
   bool ftm = true;            // window partial sums in TMEM (PINT_FUSED_TMEM=0: shared memory)
-  bool fws = false;           // PINT_FUSED_KERNEL=ws: warp-specialised radix-4 pipeline (experimental, slower)
   double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
   int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
   LineConst* lc = nullptr;    // [Qb][N]
@@ -382,10 +381,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   // fused heat iteration: v2 = two warps per line (64 lanes x Cf rows), v1 = one warp (32 x Cf);
   // 8 lines + k window rows in smem
   {
-    const char* fk = getenv("PINT_FUSED_KERNEL");
-    p->fws = fk && std::string(fk) == "ws";     // experimental warp-specialised radix-4 pipeline
     const char* fl = getenv("PINT_FUSED_LANES");
-    p->flanes = (!p->fws && fl && std::string(fl) == "64") ? 64 : 32;
+    p->flanes = (fl && std::string(fl) == "64") ? 64 : 32;
     int Cf = 1;
     while (p->flanes * Cf < L) Cf *= 2;
     p->Cf = Cf;
@@ -395,14 +392,14 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     const char* ft = getenv("PINT_FUSED_TMEM");
     p->ftm = !(ft && std::string(ft) == "0");
   }
-  const size_t fsmem = p->fws ? fused_ws_smem_bytes(p->Cf, k) : fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
+  const size_t fsmem = fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
   p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
   p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u;
   if (p->fused_ok) {
-    const int per = std::max(p->fws ? fused_ws_ctas_per_sm(p->Cf, k) : fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
+    const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    const long slots = (long)nsm * per, NG = N / (p->fws ? 4 : 8);
+    const long slots = (long)nsm * per, NG = N / 8;
     // chunks of frequency groups per x-mode: smallest power of two giving >= 90% wave efficiency
     long best = 1;
     double beff = 0.0;
@@ -559,7 +556,7 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
   // X staged in shared memory when it fits next to the lines (TMEM variant: no window sums in smem)
   static const bool noxs = getenv("PINT_FUSED_NO_XS") != nullptr;   // A/B switch
-  a.xs = (!noxs && !p->fws && p->ftm &&
+  a.xs = (!noxs && p->ftm &&
           fused_smem_bytes(p->flanes, p->Cf, p->k, true) + (size_t)p->nk * p->Lf * sizeof(double2) <= 232448u) ? 1 : 0;
   static const int dbg = getenv("PINT_FUSED_DBG") ? atoi(getenv("PINT_FUSED_DBG")) : 0;   // profiling only
   a.dbg = dbg;
@@ -580,8 +577,7 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  if (p->fws) CUDA_TRY(launch_fused_ws(p->Cf, store_w, a, p->stream));
-  else CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, p->ftm, a, p->stream));
+  CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, p->ftm, a, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
   return PINT_OK;
