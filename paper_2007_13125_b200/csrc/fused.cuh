@@ -283,7 +283,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 // lane: warp w reads/writes lanes 32 (w % 4) .. + 31; column block (w / 4) * RPT * 24 + rr * 24.
 // 24 32-bit columns per row = 6 complex doubles.  This frees 96 KB of shared memory bandwidth per
 // group (the RMW of 6 partial sums per row) onto the otherwise idle TMEM datapath.
-__device__ __forceinline__ void tmem_ld24(uint32_t addr, uint32_t (&w)[24]) {
+__device__ __forceinline__ void tmem_ld24_async(uint32_t addr, uint32_t (&w)[24]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
                  "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
@@ -291,7 +291,11 @@ __device__ __forceinline__ void tmem_ld24(uint32_t addr, uint32_t (&w)[24]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23])
                : "r"(addr + 16));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld24(uint32_t addr, uint32_t (&w)[24]) {
+  tmem_ld24_async(addr, w);
+  tmem_wait_ld();
 }
 __device__ __forceinline__ void tmem_st24(uint32_t addr, const uint32_t (&w)[24]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
@@ -321,40 +325,44 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
   const int N = (int)a.N, k = a.k, nk = a.nk;
   const int NG = N / FG;
   const int i1 = i + 1;
-  double2 xv[RPT][8];
+  // ---- Step 3 (window of group i) for all rows of this thread ----
+  if (WINDOW && !(a.dbg & 2)) {
+    double2 tww[8];
 #pragma unroll
-  for (int rr = 0; rr < RPT; ++rr) {
-    const int y = threadIdx.x + T * rr;
+    for (int t = 0; t < 8; ++t) {
+      const int j = t - 8 + k;                                                               // level n = N - 8 + t
+      double2 w = (j >= 0) ? __ldg(&a.tw[((N - 8 + t) * i) & (N - 1)]) : make_double2(0.0, 0.0);
+      w.y = -w.y;                                                                            // e^{+2 pi i n i/N}
+      tww[t] = w;
+    }
+    if constexpr (TM) {
+      uint32_t w[RPT][24];                               // slots r = 2..7 of each row: one TMEM round trip
 #pragma unroll
-    for (int t = 0; t < 8; ++t)
-      xv[rr][t] = (next && t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
-  }
-  double2 tws[8], tww[8];
+      for (int rr = 0; rr < RPT; ++rr)
+        if (!(LF < T && threadIdx.x + T * rr >= LF)) tmem_ld24_async(tacc + 24 * rr, w[rr]);
+      tmem_wait_ld();
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    tws[t] = (next && t > 0 && t < nk) ? __ldg(&a.tw[t * i1]) : make_double2(1.0, 0.0);     // w_N^{t (i+1)}
-    const int j = t - 8 + k;                                                                 // level n = N - 8 + t
-    double2 w = (WINDOW && j >= 0) ? __ldg(&a.tw[((N - 8 + t) * i) & (N - 1)]) : make_double2(0.0, 0.0);
-    w.y = -w.y;                                                                              // e^{+2 pi i n i/N}
-    tww[t] = w;
-  }
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int y = threadIdx.x + T * rr;
+        if (LF < T && y >= LF) break;                    // warp-uniform (LF % 32 == 0)
+        double2 x[8];
 #pragma unroll
-  for (int rr = 0; rr < RPT; ++rr) {
-    const int y = threadIdx.x + T * rr;
-    if (LF < T && y >= LF) break;
-    if (WINDOW && !(a.dbg & 2)) {
-      double2 x[8];
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2) x[s2] = Hs[s2 * LF + swz<C>(y)];
-      dft8<+1>(x);                                       // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
-      if constexpr (TM) {
-        uint32_t w[24];                                  // slots r = 2..7 of this row
-        tmem_ld24(tacc + 24 * rr, w);
+        for (int s2 = 0; s2 < 8; ++s2) x[s2] = Hs[s2 * LF + swz<C>(y)];
+        dft8<+1>(x);                                     // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
 #pragma unroll
         for (int r = 2; r < 8; ++r)
-          if (r - 8 + k >= 0) tw_put(w, r - 2, cfma(x[r], tww[r], tw_get(w, r - 2)));
-        tmem_st24(tacc + 24 * rr, w);
-      } else {
+          if (r - 8 + k >= 0) tw_put(w[rr], r - 2, cfma(x[r], tww[r], tw_get(w[rr], r - 2)));
+        tmem_st24(tacc + 24 * rr, w[rr]);
+      }
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int y = threadIdx.x + T * rr;
+        if (LF < T && y >= LF) break;
+        double2 x[8];
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) x[s2] = Hs[s2 * LF + swz<C>(y)];
+        dft8<+1>(x);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int j = r - 8 + k;
@@ -362,7 +370,24 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
         }
       }
     }
-    if (next && !(a.dbg & 4)) {
+  }
+  // ---- Step 1 (synthesis of group i + 1) in place ----
+  if (next && !(a.dbg & 4)) {
+    double2 xv[RPT][8];
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int y = threadIdx.x + T * rr;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        xv[rr][t] = (t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
+    }
+    double2 tws[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) tws[t] = (t > 0 && t < nk) ? __ldg(&a.tw[t * i1]) : make_double2(1.0, 0.0);   // w_N^{t (i+1)}
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int y = threadIdx.x + T * rr;
+      if (LF < T && y >= LF) break;
       double2* z = xv[rr];
 #pragma unroll
       for (int t = 1; t < 8; ++t) z[t] = cmul(z[t], tws[t]);                     // X_t w_N^{t (i+1)}
