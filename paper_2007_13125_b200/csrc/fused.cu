@@ -5,7 +5,8 @@
 namespace pint {
 
 size_t fused_smem_bytes(int lanes, int C, int k, bool tm) {
-  return (size_t)(FG + (tm ? 0 : k)) * lanes * C * sizeof(double2) + 8 * sizeof(LineConst) + 8 * 4 * sizeof(double2);
+  return (size_t)(FG + (tm ? 0 : k)) * lanes * C * sizeof(double2) + 8 * sizeof(LineConst) +
+         (lanes == 64 ? 8 * 4 * sizeof(double2) : 0);
 }
 
 template <int C, int LANES, bool SW, bool TM>

@@ -34,9 +34,11 @@ struct LineConst {
   double2 rr;       // r
   double2 rrh;      // r^{CS}
   double2 uc[8];    // u-forms of a^{C 2^i}
+  double2 ap[5];    // a^{2^i} (value form), i < 5: per-lane powers of the boundary fix-up
   double la, thr;   // log|a|;  log(1e-18 |1 - a^{2L+2}|)
-};                  // 240 bytes
-static_assert(sizeof(LineConst) == 240, "LineConst is staged in 16-byte chunks");
+};                  // 320 bytes
+constexpr int LC_CHUNKS = 20;   // 16-byte cp.async chunks per LineConst
+static_assert(sizeof(LineConst) == 16 * LC_CHUNKS, "LineConst is staged in 16-byte chunks");
 
 struct FusedArgs {
   const double2* X;        // [Qb][8][Lf]  X_t[y], zero for t >= nk and y >= L
@@ -231,9 +233,14 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
   }
   const double2 K = cmul(w0, lc.ru2L);
+  // rows y < rP carry a P term K a^{y+2} above the 1e-18 threshold: (y + 2) la > thr.  When they are
+  // few (rP <= 256: the large-shift lines) the warp fixes them up after the store, one row per lane,
+  // instead of every lane running the C-row correction loop for lane 0's sake.
+  const double rPd = lc.thr / lc.la - 2.0;                                 // la < 0, thr < 0
+  const bool fastP = !STORE_W && !PAIR && rPd <= 256.0;
   if (nv > 0) {
     const double la = lc.la, thr = lc.thr;
-    if ((y0 + 2) * la > thr) {                                             // |a^{y+2}| is largest at y0
+    if (!fastP && (y0 + 2) * la > thr) {                                   // |a^{y+2}| is largest at y0
       double2 ul = uprod(lc.u, lc.u);                                      // a^2
 #pragma unroll
       for (int i = 0; i < (PAIR ? 6 : 5); ++i)
@@ -275,6 +282,23 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   } else {
 #pragma unroll
     for (int r = 0; r < C; ++r) rows[r] = mmul<AF>(u, d[r]);   // pad rows: never read (finish uses y < L)
+    if (fastP) {
+      // x_y -= a K a^{y+2} = K a^{y+3} for y < rP (value-form powers: |a| < 0.85 here)
+      __syncwarp();
+      const int rP = min((int)ceil(rPd), L);
+      double2 al = make_double2(1.0, 0.0);                                 // a^{lane}
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+        if ((lane >> i) & 1) al = cmul(al, lc.ap[i]);
+      double2 Ka = cmul(K, cmul(lc.ap[0], lc.ap[1]));                      // K a^3
+      Ka = cmul(Ka, al);
+      const double2 a32 = cmul(lc.ap[4], lc.ap[4]);
+      for (int yy = lane; yy < rP; yy += 32) {
+        double2& xr = Hl[swz<C>(yy)];
+        xr = csub(xr, Ka);
+        Ka = cmul(Ka, a32);
+      }
+    }
   }
 }
 
@@ -409,8 +433,8 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 __device__ __forceinline__ void fused_stage_lc(const FusedArgs& a, LineConst* slc, long q, int i) {
   const int NG = (int)(a.N / FG);
   const int t = threadIdx.x;
-  if (t < 8 * 15) {
-    const int line = t / 15, c = t % 15;
+  if (t < 8 * LC_CHUNKS) {
+    const int line = t / LC_CHUNKS, c = t % LC_CHUNKS;
     const char* src = (const char*)(a.lc + q * a.N + i + (long)NG * line) + 16 * c;
     cp_async16((char*)(slc + line) + 16 * c, src);
   }
@@ -456,8 +480,8 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
   double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
   double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums (shared-memory variant)
   LineConst* slc = (LineConst*)(acc + (TMA ? 0 : a.k * LF));   // [8] line constants of the group
-  double2* xch = (double2*)(slc + 8);                  // [8][4]   pair exchange (LANES = 64)
-  double2* Xs = xch + 32;                              // [nk][LF] X of this x-mode (a.xs)
+  double2* xch = (double2*)(slc + 8);                  // [8][4]   pair exchange (LANES = 64 only)
+  double2* Xs = xch + (LANES == 64 ? 32 : 0);          // [nk][LF] X of this x-mode (a.xs)
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
   const int NG = (int)(a.N / FG);
@@ -643,6 +667,8 @@ __global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const dou
     const double2 u2L = upow(c.u, 2L * L + 2);
     c.ru2L = cdiv(make_double2(1.0, 0.0), u2L);
     c.uE = upow(c.u, (2L * L + 2) % C);
+    c.ap[0] = one_minus(c.u);
+    for (int i = 1; i < 5; ++i) c.ap[i] = cmul(c.ap[i - 1], c.ap[i - 1]);
     c.la = 0.5 * log(cabs2(one_minus(c.u)));
     c.thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));
     lc[e] = c;

@@ -394,7 +394,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   }
   const size_t fsmem = fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
   p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
-  p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u;
+  p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u - 64u;
   if (p->fused_ok) {
     const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
     int nsm = 148;
@@ -557,7 +557,7 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   // X staged in shared memory when it fits next to the lines (TMEM variant: no window sums in smem)
   static const bool noxs = getenv("PINT_FUSED_NO_XS") != nullptr;   // A/B switch
   a.xs = (!noxs && p->ftm &&
-          fused_smem_bytes(p->flanes, p->Cf, p->k, true) + (size_t)p->nk * p->Lf * sizeof(double2) <= 232448u) ? 1 : 0;
+          fused_smem_bytes(p->flanes, p->Cf, p->k, true) + (size_t)p->nk * p->Lf * sizeof(double2) <= 232448u - 64u) ? 1 : 0;
   static const int dbg = getenv("PINT_FUSED_DBG") ? atoi(getenv("PINT_FUSED_DBG")) : 0;   // profiling only
   a.dbg = dbg;
 #ifdef PINT_FUSED_PROF
