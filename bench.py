@@ -293,28 +293,42 @@ def main():
                                "iteration_GBs": 2 * bytes_launch / (ms_step / 1e3) / 1e9,
                                "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm}}
 
-    # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host
+    # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host.
+    # N > 1: every rank reads its own x-mode slab of the final level (pint_get_modal_levels); the
+    # time is the max over ranks.
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         vh = np.ascontiguousarray(prob.v)
-        out = np.empty((1, prob.M), np.complex128)
         steps, t_tot, its = args.e2e_steps, 0.0, 0
+        out_bytes = 0
         for i in range(steps + 1):
             torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             plan.set_problem(vh, np.ascontiguousarray(prob.g) if prob.R else None,
                              prob.phi if prob.R else None, prob.dphi if prob.R else None)
             it, u, st = plan.solve(prob.tol, 20, raise_on_fail=False)
-            plan.get_levels(prob.N - 1, 1, out)
+            if world > 1:
+                out = plan.get_modal_levels(prob.N - 1, 1)
+            else:
+                out = np.empty((1, prob.M), np.complex128)
+                plan.get_levels(prob.N - 1, 1, out)
             dt = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
             if i > 0:
                 t_tot += dt
                 its += it
+            out_bytes = out.nbytes
         e2e = {"value": total_unknowns * its / t_tot, "unit": UNIT,
                "h2d_bytes_per_step": int(vh.nbytes + (prob.g.nbytes if prob.R else 0)),
-               "d2h_bytes_per_step": int(out.nbytes + 8 * its // steps),
+               "d2h_bytes_per_step": int(out_bytes + 8 * its // steps),
                "what": f"set_problem(host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
-                       "final time level to host, per step; unknowns/s per WR iteration"}
+                       + ("final time level to host" if world == 1 else "each rank's modal slab of the final level to host")
+                       + ", per step (max over ranks); unknowns/s per WR iteration"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
