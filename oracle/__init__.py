@@ -22,6 +22,7 @@ Modules
   dense      O3: dense all-at-once Kronecker system (tiny sizes)
   modal      O4: per-sine-mode scalar WR (data in the span of few modes, e.g. C4)
   theory     exact per-mode WR contraction factor (pin for the paper's gamma(kappa))
+  nonlinear  O5: semilinear scheme (Newton per step) and Algorithm 3 (Newton + WR inner solves)
 
 Parity status of each function is recorded in DESIGN.md §"Oracle pins"; every
 function listed above is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py.

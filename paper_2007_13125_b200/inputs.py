@@ -184,6 +184,38 @@ def example2_fd(k: int, M: int = 999, N: int = 100, kappa: float = 0.1,
     return Problem(f"E2_k{k}", M, 1, 0.1, N, k, kappa, alpha, v, g, phi, dphi, u0="zero")
 
 
+def example4_allen_cahn(alpha: float, k: int, M: int = 999, N: int = 100, T: float = 0.4,
+                        kappa: float = 0.1, eps: float = 1.0, discrete: bool = False) -> Problem:
+    """Example 4 (Table 4): Allen-Cahn nonlinearity g(u) = (u^3 - u)/eps^2 on
+    (0,1) with the forcing that makes u = t^2/Gamma(3) sin(2 pi x) exact (continuous operators):
+      f = [t^{2-a}/Gamma(3-a) + (2 pi^2 - 1/(2 eps^2)) t^2] sin(2 pi x) + t^6/(8 eps^2) sin^3(2 pi x),
+    v = u(0) = 0.  Separable with R = 2; d^l phi/dt^l (0) = 0 for l = 1..k-2 when a < 1 (k <= 3 in
+    Table 4), and phi_1'(0) = 1 for a = 1.  The nonlinearity itself is not part of this record.
+    discrete=True replaces 4 pi^2 by the FD eigenvalue (4/h^2) sin^2(pi h) of sin(2 pi x), so that
+    the exact solution also solves the semi-discrete problem (time-discretisation error only)."""
+    x = grid1d(M)
+    t = np.arange(N + 1) * (T / N)
+    s1 = np.sin(2 * math.pi * x)
+    g = np.stack([s1, s1 ** 3]).astype(np.complex128)
+    h = 1.0 / (M + 1)
+    lam = (4.0 / h ** 2) * math.sin(math.pi * h) ** 2 if discrete else 4 * math.pi ** 2
+    phi = np.stack([t ** (2 - alpha) / math.gamma(3 - alpha) + (lam / 2 - 0.5 / eps ** 2) * t ** 2,
+                    t ** 6 / (8 * eps ** 2)])
+    nd = max(k - 2, 0)
+    dphi = np.zeros((2, nd))
+    if nd >= 1 and alpha == 1.0:
+        dphi[0, 0] = 1.0                        # d/dt t^{2-a}/Gamma(3-a) at 0 for a = 1
+    if nd >= 2:
+        dphi[0, 1] = (2.0 if alpha == 1.0 else 0.0) + 2 * (lam / 2 - 0.5 / eps ** 2)
+    return Problem(f"E4_a{alpha}_k{k}", M, 1, T, N, k, kappa, alpha, np.zeros(M, np.complex128), g, phi, dphi)
+
+
+def allen_cahn_exact(prob, n: int) -> np.ndarray:
+    """u(t_n) = t_n^2/2 sin(2 pi x) of Example 4 (for error measurement)."""
+    t = n * prob.tau
+    return (t * t / 2.0 * np.sin(2 * math.pi * grid1d(prob.mx))).astype(np.complex128)
+
+
 def random_complex_problem(mx: int, my: int, N: int, k: int, kappa: float, alpha: float,
                            R: int = 2, seed: int = 1, T: float = 1.0) -> Problem:
     """Generic complex-valued data (exercises the complex path)."""
