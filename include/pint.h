@@ -151,6 +151,34 @@ pint_status pint_set_timing(pint_plan plan, int32_t enable);
 pint_status pint_get_timing(pint_plan plan, double* tpass_ms, double* spass_ms,
                             int64_t* tpass_launches, int64_t* spass_launches);
 
+/* ---- semilinear extension: Newton's method with WR inner solves ----
+ * Problem: dbar^a u + A u + g(u) = f, u(0) = v, with the modified CQ-BDFk / BDFk scheme of
+ * eqn:BDF-CQ-m-r, g(u) = (u^3 - u)/eps^2 (Allen-Cahn, Example 4,
+ * PAPER.md:1714-1722).  Algorithm 3: U_0^n = v; Newton step l solves
+ * (dbar^a + A + g'(Ubar_{l-1})) W = fbar - (dbar^a + A) U_{l-1} - g(U_{l-1}), W^{<=0} = 0, with
+ * Ubar the mean over the N levels (reading R-NL-sign: +g'), by the WR
+ * iteration (kappa-wrap) until max_n |W_m^n - W_{m-1}^n| < inner_tol, then
+ * U_l = U_{l-1} + W.  1D operators on one rank only (g'(Ubar(x)) varies in x, so the line solves
+ * are general tridiagonal systems: shift-accurate Thomas); always the streaming path. */
+enum { PINT_NL_ALLEN_CAHN = 1 };
+
+/* Make the plan semilinear with nonlinearity `kind` and width eps > 0.  The forcing f and v are
+ * still given by pint_set_problem_separable (before or after this call); the Newton state is reset
+ * to U_0 = v by either call.  Errors: ARG (kind, eps), UNSUPPORTED (2D or nranks > 1).
+ * Afterwards pint_wr_iterate / pint_wr_solve return STATE and pint_get_levels returns U_l. */
+pint_status pint_set_nonlinearity(pint_plan plan, int32_t kind, double eps);
+
+/* Run up to max_outer Newton steps from the current U_l (inner WR: at most max_inner iterations,
+ * stop when the full-array max-norm update < inner_tol).  inner_counts[l] / outer_updates[l]
+ * (arrays of max_outer entries, may be NULL) receive the inner iteration count and
+ * max |U_l - U_{l-1}| of each step; *outer_done the number of steps run.  Returns OK when the
+ * Newton update fell below outer_tol (or outer_tol == 0 and max_outer steps ran),
+ * NOT_CONVERGED otherwise, DIVERGED on a non-finite update, STATE before set_problem/
+ * set_nonlinearity. */
+pint_status pint_newton_solve(pint_plan plan, int32_t max_outer, double outer_tol, double inner_tol,
+                              int32_t max_inner, int32_t* inner_counts, double* outer_updates,
+                              int32_t* outer_done);
+
 /* Which iteration the plan runs for its current problem: *fused = 1 for the fused one-kernel heat
  * iteration (fused.cuh; no space-time array per iteration), 0 for the two-pass streaming one
  * (CQ, PINT_FLAG_STREAM, or more than 8 nonzero levels of Gamma F).  *chunks = frequency-group

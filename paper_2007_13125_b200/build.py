@@ -61,6 +61,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
              for n in NS]
     units += [(os.path.join(CSRC, "dispatch.cu"), os.path.join(build_dir, "dispatch.o"), defines),
               (os.path.join(CSRC, "fused.cu"), os.path.join(build_dir, "fused.o"), defines),
+              (os.path.join(CSRC, "newton.cu"), os.path.join(build_dir, "newton.o"), defines),
               (os.path.join(CSRC, "pint.cu"), os.path.join(build_dir, "pint.o"), defines)]
     jobs = jobs or min(len(units), os.cpu_count() or 4)
     logs = []

@@ -5,6 +5,7 @@
 #include "spass.cuh"
 #include "dst.cuh"
 #include "fused.cuh"
+#include "newton.cuh"
 #include <algorithm>
 
 namespace pint {
@@ -27,6 +28,14 @@ int fused_ctas_per_sm(int lanes, int C, int k, bool tm);
 int fused_rows_per_subchain(int lanes, int C);
 cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st);
+// semilinear extension (newton.cu): Newton coefficient, residual, variable-coefficient line solves
+cudaError_t launch_nl_coeff(const NewtonArgs& a, cudaStream_t st);
+cudaError_t launch_nl_residual(const NewtonArgs& a, cudaStream_t st);
+cudaError_t launch_spass_vc(const VcArgs& a, cudaStream_t st);
+cudaError_t launch_nl_update(double2* U, const double2* W, long N, int L, int WB, unsigned long long* upd,
+                             cudaStream_t st);
+cudaError_t launch_nl_diffmax(const double2* A, const double2* B, long count, unsigned long long* upd,
+                              cudaStream_t st);
 cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int CS,
                               int L, cudaStream_t st);
 

@@ -1,0 +1,35 @@
+// newton.cu — launchers of the semilinear (Newton-WR) kernels (newton.cuh).
+#define PINT_DEFINE_NEWTON_KERNELS
+#include "kernels.h"
+
+namespace pint {
+
+static unsigned grid_for(long n, int tpb) {
+  const long b = (n + tpb - 1) / tpb;
+  return (unsigned)(b < 148L * 16 ? (b > 0 ? b : 1) : 148L * 16);
+}
+
+cudaError_t launch_nl_coeff(const NewtonArgs& a, cudaStream_t st) {
+  nl_coeff_kernel<<<grid_for(a.L, 128), 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_nl_residual(const NewtonArgs& a, cudaStream_t st) {
+  nl_residual_kernel<<<grid_for(a.N * a.L, 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_spass_vc(const VcArgs& a, cudaStream_t st) {
+  spass_vc_kernel<<<(unsigned)((a.N + 63) / 64), 64, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_nl_update(double2* U, const double2* W, long N, int L, int WB, unsigned long long* upd,
+                             cudaStream_t st) {
+  nl_update_kernel<<<grid_for(N * L, 256), 256, 0, st>>>(U, W, N, L, WB, upd);
+  return cudaGetLastError();
+}
+cudaError_t launch_nl_diffmax(const double2* A, const double2* B, long count, unsigned long long* upd,
+                              cudaStream_t st) {
+  nl_diffmax_kernel<<<grid_for(count, 256), 256, 0, st>>>(A, B, count, upd);
+  return cudaGetLastError();
+}
+
+}  // namespace pint

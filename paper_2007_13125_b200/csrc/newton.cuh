@@ -1,0 +1,135 @@
+// newton.cuh — the semilinear extension (Algorithm 3): Newton's method whose
+// linearised problems are solved by the WR iteration of the streaming path.  1D operator only:
+// the Newton coefficient g'(Ubar(x)) varies in x, so the DST no longer diagonalises the operator
+// and the line solves become general (non-Toeplitz) tridiagonal systems.
+//
+//   outer l:  c = g'(Ubar_{l-1}),  Ubar = (1/N) sum_n U_{l-1}^n
+//             R^n = fbar_n - dbar^a U^n - A U^n - g(U^n)                   (eqn:BDF-CQ-m-r-N rhs)
+//             inner WR: (dbar^a + A + diag(c)) W = R, W^{<=0} = 0, kappa-wrap
+//             U_l = U_{l-1} + W
+// Allen-Cahn: g(u) = (u^3 - u)/eps^2 (Example 4).
+#pragma once
+#include "spass.cuh"
+
+namespace pint {
+
+struct NewtonArgs {
+  const double2* U;      // U_{l-1}, physical [N][L] (1D)
+  double2* R;            // residual, tile layout [yb][N][WB]
+  double2* c;            // [L] h^2 g'(Ubar)  (line-solve diagonal shift)
+  const double2* src;    // [S][Lpad] separable sources (0 = v, 1 = A v, 2.. = g_r)
+  const double* coef;    // [S][N]   F_static_n = sum_s coef[s][n] src_s  (= fbar_n + tau^-a psum_n v)
+  const double* wt;      // [N]      tau^-a omega_j (heat: zero for j > k)
+  const double* anl;     // [N]      a_n of Table 1 (the -a_n g(v) part of fbar)
+  int S, L, Lpad, WB;
+  long N;
+  double ih2, h2, ieps2;
+};
+
+struct VcArgs {
+  const double2* in;      // H, tile layout [yb][N][WB]
+  double2* out;           // W
+  double2* piv;           // [N][L] scratch: 1/m_i
+  const double2* sig_p;   // [N] h^2 d_p / tau^a
+  const double2* c;       // [L]
+  long N;
+  int L, Lpad, WB;
+};
+
+#ifdef PINT_DEFINE_NEWTON_KERNELS
+
+__device__ __forceinline__ double2 nl_g(double2 u, double ieps2) {        // (u^3 - u) / eps^2
+  const double2 u3 = cmul(cmul(u, u), u);
+  return cscale(csub(u3, u), ieps2);
+}
+
+// c[y] = h^2 g'(Ubar[y]) = h^2 (3 Ubar^2 - 1) / eps^2
+__global__ void nl_coeff_kernel(const NewtonArgs a) {
+  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < a.L; y += gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (long n = 0; n < a.N; ++n) s = cadd(s, a.U[n * a.L + y]);
+    const double2 ub = cscale(s, 1.0 / (double)a.N);
+    const double2 d = cscale(make_double2(3.0 * (ub.x * ub.x - ub.y * ub.y) - 1.0, 6.0 * ub.x * ub.y), a.ieps2);
+    a.c[y] = cscale(d, a.h2);
+  }
+}
+
+// R^n = F_static_n - sum_{j=0}^{n-1} tau^-a omega_j U^{n-j} - A U^n - g(U^n) - a_n g(v)
+// (the v-terms of fbar and dbar^a cancel against the psum_n v part of F_static)
+__global__ void nl_residual_kernel(const NewtonArgs a) {
+  const long total = a.N * a.L;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long n = e / a.L;                 // 0-based level (level n+1)
+    const int y = (int)(e % a.L);
+    double2 r = make_double2(0.0, 0.0);
+    for (int s = 0; s < a.S; ++s) r = cfmar(a.src[(long)s * a.Lpad + y], a.coef[(long)s * a.N + n], r);
+    for (long j = 0; j <= n; ++j) {
+      const double w = a.wt[j];
+      if (w != 0.0) r = cfmar(a.U[(n - j) * a.L + y], -w, r);
+    }
+    const double2 u = a.U[n * a.L + y];
+    const double2 ul = y > 0 ? a.U[n * a.L + y - 1] : make_double2(0.0, 0.0);
+    const double2 ur = y < a.L - 1 ? a.U[n * a.L + y + 1] : make_double2(0.0, 0.0);
+    const double2 Au = cscale(csub(cscale(u, 2.0), cadd(ul, ur)), a.ih2);
+    r = csub(r, Au);
+    r = csub(r, nl_g(u, a.ieps2));
+    if (a.anl[n] != 0.0) r = cfmar(nl_g(a.src[y], a.ieps2), -a.anl[n], r);   // source 0 is v
+    a.R[((long)(y / a.WB) * a.N + n) * a.WB + y % a.WB] = r;
+  }
+}
+
+
+// Shifted solves with a varying diagonal, one thread per line p (1D): T x = d,
+// T = tridiag(-1, 2 + s_i, -1), s_i = h^2 (d_p / tau^a) + c_i.  Shift-accurate pivots
+// (SURVEY §8(c) E-6): m_i = 1 + e_i, e_0 = 1 + s_0, e_i = s_i + e_{i-1}/(1 + e_{i-1}) — the 2 of the
+// diagonal never meets the small shift.  Thomas: y_i = (d_i + y_{i-1})/m_i, x_i = y_i + x_{i+1}/m_i.
+__global__ void spass_vc_kernel(const VcArgs a) {
+  const long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (p >= a.N) return;
+  const double2 sp = a.sig_p[p];
+  double2* piv = a.piv + p * a.L;
+  auto idx = [&](int y) { return ((long)(y / a.WB) * a.N + p) * a.WB + y % a.WB; };
+  double2 e = make_double2(0.0, 0.0), yv = make_double2(0.0, 0.0);
+  for (int i = 0; i < a.L; ++i) {
+    const double2 s = cadd(sp, a.c[i]);
+    e = (i == 0) ? make_double2(1.0 + s.x, s.y) : cadd(s, cdiv(e, make_double2(1.0 + e.x, e.y)));
+    const double2 rm = cdiv(make_double2(1.0, 0.0), make_double2(1.0 + e.x, e.y));
+    piv[i] = rm;
+    yv = cmul(cadd(a.in[idx(i)], yv), rm);
+    a.out[idx(i)] = yv;
+  }
+  double2 x = make_double2(0.0, 0.0);
+  for (int i = a.L - 1; i >= 0; --i) {
+    x = cadd(a.out[idx(i)], cmul(x, piv[i]));
+    a.out[idx(i)] = x;
+  }
+  for (int y = a.L; y < a.Lpad; ++y) a.out[idx(y)] = make_double2(0.0, 0.0);
+}
+
+// U[n][y] += W (tile layout); max |W| -> upd (ordered bits)
+__global__ void nl_update_kernel(double2* U, const double2* W, long N, int L, int WB, unsigned long long* upd) {
+  double m = 0.0;
+  const long total = N * L;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long n = e / L;
+    const int y = (int)(e % L);
+    const double2 w = W[((long)(y / WB) * N + n) * WB + y % WB];
+    U[e] = cadd(U[e], w);
+    m = fmax(m, sqrt(cabs2(w)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
+}
+
+// max |A - B| over count elements -> upd (inner WR monitor on the full space-time array)
+__global__ void nl_diffmax_kernel(const double2* A, const double2* B, long count, unsigned long long* upd) {
+  double m = 0.0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x)
+    m = fmax(m, sqrt(cabs2(csub(A[e], B[e]))));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
+}
+
+#endif  // PINT_DEFINE_NEWTON_KERNELS
+
+}  // namespace pint

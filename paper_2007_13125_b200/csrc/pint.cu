@@ -174,6 +174,11 @@ struct pint_plan_s {
   double2* Pp = nullptr;      // [Qb][nch][k][Lf]
   int64_t dev_bytes = 0;
   unsigned long long* prof = nullptr;   // -DPINT_FUSED_PROF builds: phase cycle counters (not owned)
+  // semilinear extension (Algorithm 3; newton.cuh): 1D, streaming path
+  bool nl = false;
+  double nl_eps = 1.0;
+  double2 *nlU = nullptr, *nlR = nullptr, *nlC = nullptr, *nlPiv = nullptr, *nlT[2] = {nullptr, nullptr};
+  double *nlWt = nullptr, *nlAnl = nullptr;
   std::vector<void*> allocs;
   std::vector<VmmAlloc> vallocs;
   // state
@@ -637,6 +642,8 @@ static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
 // ------------------------------------------------------------------------------------------
 // problem setup
 // ------------------------------------------------------------------------------------------
+static pint_status nl_reset(pint_plan p);
+
 static pint_status bootstrap(pint_plan p) {
   // U_0^n = v (default) or 0 (PINT_FLAG_U0_ZERO): A = H_1, wrap = last-k of U_0
   const bool zero = (p->flags & PINT_FLAG_U0_ZERO) != 0;
@@ -649,6 +656,7 @@ static pint_status bootstrap(pint_plan p) {
   p->m = 0;
   p->last_upd = -1.0;
   p->increases = 0;
+  if (p->nl) TRY(nl_reset(p));
   return PINT_OK;
 }
 
@@ -846,6 +854,7 @@ static pint_status read_update(pint_plan p, double* out) {
 
 extern "C" pint_status pint_wr_iterate(pint_plan p, double* update_inf) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (p->nl) return fail(PINT_ERR_STATE, "semilinear plan: use pint_newton_solve");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   CUDA_TRY(cudaSetDevice(p->device));
   TRY(iterate_async(p));
@@ -857,6 +866,7 @@ extern "C" pint_status pint_wr_iterate(pint_plan p, double* update_inf) {
 
 extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters, int32_t* iters, double* update_inf) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (p->nl) return fail(PINT_ERR_STATE, "semilinear plan: use pint_newton_solve");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (!(tol >= 0.0) || max_iters < 0) return fail(PINT_ERR_ARG, "need tol >= 0 and max_iters >= 0");
   CUDA_TRY(cudaSetDevice(p->device));
@@ -883,6 +893,139 @@ extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters,
 }
 
 // ------------------------------------------------------------------------------------------
+// semilinear extension: Newton's method with WR inner solves (Algorithm 3)
+// ------------------------------------------------------------------------------------------
+static pint_status nl_reset(pint_plan p) {
+  // U_0^n = v for all n (Algorithm 3, line 1): source 0 holds v (1D tile layout == physical)
+  for (int64_t n = 0; n < p->N; ++n)
+    CUDA_TRY(cudaMemcpyAsync(p->nlU + n * p->M, p->src, p->M * sizeof(double2), cudaMemcpyDeviceToDevice, p->stream));
+  return PINT_OK;
+}
+
+extern "C" pint_status pint_set_nonlinearity(pint_plan p, int32_t kind, double eps) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (kind != PINT_NL_ALLEN_CAHN) return fail(PINT_ERR_ARG, "kind must be PINT_NL_ALLEN_CAHN");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(PINT_ERR_ARG, "eps must be > 0");
+  if (p->dim != 1 || p->nranks != 1)
+    return fail(PINT_ERR_UNSUPPORTED, "the Newton-WR extension is 1D on one rank (g'(Ubar(x)) breaks the DST)");
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->nl_eps = eps;
+  p->fused_ok = false;
+  p->fused = false;
+  if (!p->nl) {
+    const size_t arr = (size_t)p->ntiles * TILE;
+    TRY(dalloc(p, &p->nlU, (size_t)p->N * p->M));
+    TRY(dalloc(p, &p->nlR, arr));
+    TRY(dalloc(p, &p->nlT[0], arr));
+    TRY(dalloc(p, &p->nlT[1], arr));
+    TRY(dalloc(p, &p->nlC, (size_t)p->L));
+    TRY(dalloc(p, &p->nlPiv, (size_t)p->N * p->L));
+    TRY(dalloc(p, &p->nlWt, (size_t)p->N));
+    TRY(dalloc(p, &p->nlAnl, (size_t)p->N));
+    CUDA_TRY(cudaMemsetAsync(p->nlR, 0, arr * sizeof(double2), p->stream));
+    // tau^-a omega_j (j < N; heat: zero beyond k) and the Table-1 a_n (n = 1..N -> index n-1)
+    const ld ta = powl((ld)p->tau, -(ld)p->alpha);
+    std::vector<ld> w = (p->alpha == 1.0) ? bdf_weights(p->k) : cq_weights(p->k, (ld)p->alpha, p->N + 1);
+    w.resize(p->N + 1, 0.0L);
+    std::vector<double> wt(p->N), anl(p->N);
+    for (int64_t j = 0; j < p->N; ++j) wt[j] = (double)(ta * w[j]);
+    for (int64_t n = 1; n <= p->N; ++n) anl[n - 1] = (double)table1_a(p->k, (int)n);
+    TRY(h2d(p, p->nlWt, wt));
+    TRY(h2d(p, p->nlAnl, anl));
+  }
+  p->nl = true;
+  if (p->problem_set) {
+    TRY(bootstrap(p));   // streaming state + U_0 = v
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+  }
+  return PINT_OK;
+}
+
+// T-pass of the inner linear problem: W^{<=0} = 0 (no v terms), F_static = R (dense), never pruned
+static pint_status tpass_nl(pint_plan p, int mode_in, int mode_out, const double2* in, double2* out,
+                            const double2* wold, double2* wnew) {
+  TPassArgs a = targs(p);
+  a.in = in; a.out = out; a.wrap_old = wold; a.wrap_new = wnew;
+  a.S = 0; a.nmax = (int)p->N; a.nsparse = 0; a.ndense = 0;
+  a.fdense = p->nlR;
+  CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
+  ++p->launches;
+  return PINT_OK;
+}
+
+static pint_status read_upd(pint_plan p, double* out) {
+  unsigned long long bits = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bits, p->upd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  std::memcpy(out, &bits, sizeof(double));
+  return PINT_OK;
+}
+
+extern "C" pint_status pint_newton_solve(pint_plan p, int32_t max_outer, double outer_tol, double inner_tol,
+                                         int32_t max_inner, int32_t* inner_counts, double* outer_updates,
+                                         int32_t* outer_done) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (!p->nl) return fail(PINT_ERR_STATE, "call pint_set_nonlinearity first");
+  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
+  if (max_outer < 0 || max_inner < 1 || !(inner_tol >= 0.0) || !(outer_tol >= 0.0))
+    return fail(PINT_ERR_ARG, "need max_outer >= 0, max_inner >= 1, tolerances >= 0");
+  CUDA_TRY(cudaSetDevice(p->device));
+  NewtonArgs na{};
+  na.U = p->nlU; na.R = p->nlR; na.c = p->nlC; na.src = p->src; na.coef = p->coef; na.wt = p->nlWt; na.anl = p->nlAnl;
+  na.S = p->S; na.L = (int)p->L; na.Lpad = (int)(p->NB * p->WB); na.WB = p->WB; na.N = p->N;
+  const ld hl = 1.0L / (ld)(p->L + 1);
+  na.ih2 = (double)(1.0L / (hl * hl)); na.h2 = (double)(hl * hl); na.ieps2 = 1.0 / (p->nl_eps * p->nl_eps);
+  VcArgs va{};
+  va.piv = p->nlPiv; va.sig_p = p->sig_p; va.c = p->nlC; va.N = p->N; va.L = (int)p->L;
+  va.Lpad = (int)(p->NB * p->WB); va.WB = p->WB;
+  const long count = p->ntiles * TILE;
+  pint_status result = PINT_ERR_NOT_CONVERGED;
+  int32_t done = 0;
+  for (int32_t l = 0; l < max_outer; ++l) {
+    CUDA_TRY(launch_nl_coeff(na, p->stream));
+    CUDA_TRY(launch_nl_residual(na, p->stream));
+    p->launches += 2;
+    // inner WR on W: W_0 = 0 -> H_1 into A, window 0
+    TRY(tpass_nl(p, IN_TIME_ZERO, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur]));
+    CUDA_TRY(cudaMemsetAsync(p->nlT[0], 0, count * sizeof(double2), p->stream));
+    int cur = 1, m = 0;
+    double upd = INFINITY;
+    while (m < max_inner) {
+      va.in = p->A; va.out = p->B;
+      CUDA_TRY(launch_spass_vc(va, p->stream));                                             // W_m (freq)
+      TRY(tpass_nl(p, IN_FREQ, OUT_H, p->B, p->A, p->wrap[p->wcur], p->wrap[1 - p->wcur]));  // H_{m+1}
+      p->wcur ^= 1;
+      TRY(tpass_nl(p, IN_FREQ, OUT_U, p->B, p->nlT[cur], nullptr, nullptr));                // W_m (time)
+      CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+      CUDA_TRY(launch_nl_diffmax(p->nlT[cur], p->nlT[1 - cur], count, p->upd, p->stream));
+      p->launches += 2;
+      ++m;
+      TRY(read_upd(p, &upd));
+      cur ^= 1;
+      if (!std::isfinite(upd)) { g_last_error = "inner update is not finite"; return PINT_ERR_DIVERGED; }
+      if (upd < inner_tol) break;
+    }
+    // U_l = U_{l-1} + W (latest W_m is nlT[1 - cur])
+    CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+    CUDA_TRY(launch_nl_update(p->nlU, p->nlT[1 - cur], p->N, (int)p->L, p->WB, p->upd, p->stream));
+    ++p->launches;
+    double ou = 0.0;
+    TRY(read_upd(p, &ou));
+    if (inner_counts) inner_counts[l] = m;
+    if (outer_updates) outer_updates[l] = ou;
+    ++done;
+    ++p->m;
+    if (!std::isfinite(ou)) { g_last_error = "Newton update is not finite"; result = PINT_ERR_DIVERGED; break; }
+    if (ou < outer_tol) { result = PINT_OK; break; }
+  }
+  if (result == PINT_ERR_NOT_CONVERGED && done == max_outer && outer_tol == 0.0) result = PINT_OK;
+  if (result == PINT_ERR_NOT_CONVERGED) g_last_error = "max_outer reached before the Newton update < outer_tol";
+  if (outer_done) *outer_done = done;
+  p->stateA = 2;   // A/B hold inner-WR data: pint_get_levels reads U_l
+  return result;
+}
+
+// ------------------------------------------------------------------------------------------
 // output
 // ------------------------------------------------------------------------------------------
 static pint_status materialize(pint_plan p) {
@@ -903,6 +1046,13 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
   if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
   if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "nranks > 1: use pint_get_modal_levels + pint_modal_to_physical");
   CUDA_TRY(cudaSetDevice(p->device));
+  if (p->nl) {   // semilinear plans: the Newton iterate U_l (physical [N][M]; l = 0 gives v)
+    if (n_count == 0) return PINT_OK;
+    CUDA_TRY(cudaMemcpyAsync(U, p->nlU + n_begin * p->M, n_count * p->M * sizeof(double2),
+                             mem == PINT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return PINT_OK;
+  }
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
   if (n_count == 0) return PINT_OK;
   if (n_begin >= p->N - p->k && p->stateA != 1) {

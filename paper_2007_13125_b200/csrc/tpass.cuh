@@ -65,6 +65,8 @@ struct TPassArgs {
   const int* dsrc;          // [ndense] source indices with nhi > 16
   const double2* chat;      // [ndense][N]  sum_n gsf[n] coef[s][n] e^{-2 pi i n p / N}
   int nk;                   // X_n = 0 for n >= nk (nk = max(k, max sparse nhi) <= 16)
+  const double2* fdense;    // optional dense right-hand side [N][M] in the tile layout, added to
+                            // F_static (Newton inner solves: the residual R; set nmax = N)
 };
 
 // table load that the compiler may not hoist above barriers (bounds live ranges in the CQ path)
@@ -100,10 +102,12 @@ __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* d
 
 // F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]; zero for n >= nmax.
 // srcp = src + tile*WB + c, sstride = ntiles*WB (one spatial vector per source).
-__device__ __forceinline__ double2 static_rhs(const TPassArgs& a, const double2* srcp, long sstride, int N, int n) {
+__device__ __forceinline__ double2 static_rhs(const TPassArgs& a, const double2* srcp, long sstride, int N, int n,
+                                              long e) {
   double2 f = make_double2(0.0, 0.0);
   if (n >= a.nmax) return f;
   for (int s = 0; s < a.S; ++s) f = cfmar(ldt(&srcp[s * sstride]), ldt(&a.coef[(long)s * N + n]), f);
+  if (a.fdense) f = cadd(f, ldt(&a.fdense[e]));
   return f;
 }
 
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
         // F_static is zero for n >= nmax; with nmax <= PL only s == 0 slots can be nonzero
         const bool live = (s == 0) || dense || (TM::PL < 8);
         double2 F = make_double2(0.0, 0.0);
-        if (live) F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n);
+        if (live) F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
         if ((s == 0 || TM::PL < 8) && n < k) {
           // (kappa/tau) sum_{j=n+1}^{k} omega_j U_m^{N+n-j} (0-based levels), window index k+n-j
           for (int jw = n + 1; jw <= k; ++jw) F = cfmar(sW[(k + n - jw) * WB + c], __ldg(&a.wk[jw]), F);
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
         const int n = TM::n(j, s, tid), c = TM::c(j, tid);
-        const double2 F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n);
+        const double2 F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
         const int r = j * TM::RL + s;
         v[r] = cfmar(F, ldt(&a.gsfq[n]), cmul(v[r], ldt(&a.thm[n])));
       }

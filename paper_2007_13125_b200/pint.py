@@ -22,13 +22,14 @@ PINT_FLAG_U0_ZERO = 1
 PINT_FLAG_FULL_FFT = 2
 PINT_FLAG_STREAM = 4
 PINT_FLAG_DST_PER_ITER = 8
+PINT_NL_ALLEN_CAHN = 1
 
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
     "pint_wr_solve", "pint_get_levels", "pint_get_solution", "pint_get_modal_levels",
     "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
-    "pint_kappa_log_rule", "pint_get_path",
+    "pint_kappa_log_rule", "pint_get_path", "pint_set_nonlinearity", "pint_newton_solve",
 ]
 
 
@@ -78,6 +79,8 @@ def lib(path: str = LIB_PATH):
         "pint_last_error": [],
         "pint_kappa_log_rule": [I64],
         "pint_get_path": [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)],
+        "pint_set_nonlinearity": [P, I32, D],
+        "pint_newton_solve": [P, I32, D, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(I32)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -250,6 +253,21 @@ class Plan:
         m, l, b = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().pint_get_info(self._h, ctypes.byref(m), ctypes.byref(l), ctypes.byref(b)))
         return {"m": m.value, "kernel_launches": l.value, "device_bytes": b.value}
+
+    # -- semilinear extension (Newton-WR) ------------------------------------------------------
+    def set_nonlinearity(self, eps: float, kind: int = PINT_NL_ALLEN_CAHN):
+        _check(lib().pint_set_nonlinearity(self._h, kind, eps))
+
+    def newton_solve(self, max_outer: int, inner_tol: float = 1e-12, max_inner: int = 60,
+                     outer_tol: float = 0.0, raise_on_fail: bool = True):
+        """Returns (inner_counts, outer_updates, status)."""
+        cnt = (ctypes.c_int32 * max(max_outer, 1))()
+        upd = (ctypes.c_double * max(max_outer, 1))()
+        done = ctypes.c_int32()
+        st = lib().pint_newton_solve(self._h, max_outer, outer_tol, inner_tol, max_inner, cnt, upd, ctypes.byref(done))
+        if st != PINT_OK and raise_on_fail:
+            _check(st)
+        return list(cnt[:done.value]), list(upd[:done.value]), st
 
     def path(self):
         """{"fused": bool, "chunks": int, "nk": int} (pint_get_path)."""

@@ -323,3 +323,36 @@ def test_dst_per_iteration_ablation(pint, mx, my, N, k, kappa, alpha, R):
         win = p.get_levels(N - k, k)
         assert rel(p.get_solution(), o[3]) < TOL
         assert np.linalg.norm(win - o[3][N - k:]) / np.linalg.norm(o[3]) < TOL
+
+
+@pytest.mark.parametrize("alpha,k", [(0.25, 1), (0.25, 2), (0.75, 2), (0.75, 3), (1.0, 2)])
+def test_newton_wr_allen_cahn(pint, alpha, k):
+    """Semilinear extension (Algorithm 3): Example 4 at N = 128 (the library's
+    power-of-two N), h = 1/1000.  Each Newton step's iterate U_l matches the oracle's Algorithm 3 and
+    the inner WR counts are the oracle's (5, 4, 3, as in Table 4)."""
+    from oracle import nonlinear as nl
+    G, DG = nl.allen_cahn(1.0)
+    prob = inputs.example4_allen_cahn(alpha, k, N=128)
+    Us, counts = nl.newton_wr(prob, G, DG, 3)
+    with pint.Plan.from_problem(prob) as p:
+        p.set_nonlinearity(1.0)
+        assert rel(p.get_solution(), Us[0]) == 0.0 or np.linalg.norm(Us[0]) == 0.0
+        with pytest.raises(pint.PintError) as e:
+            p.iterate()
+        assert e.value.status == pint.PINT_ERR_STATE
+        for l in range(1, 4):
+            c, u, st = p.newton_solve(1)
+            assert c == [counts[l - 1]], (l, c, counts)
+            err = rel(p.get_solution(), Us[l])
+            print(f"alpha={alpha} k={k} l={l}: inner {c[0]}, rel L2 vs oracle {err:.2e}, update {u[0]:.2e}")
+            assert err < TOL, (l, err)
+    if alpha < 1.0:
+        assert counts == [5, 4, 3]      # Table 4's bracketed counts (alpha = 0.25, 0.75 columns)
+
+
+def test_newton_wr_rejects_2d(pint):
+    prob = inputs.random_complex_problem(15, 9, 64, 2, 0.1, 1.0, R=0, seed=1)
+    with pint.Plan.from_problem(prob) as p:
+        with pytest.raises(pint.PintError) as e:
+            p.set_nonlinearity(1.0)
+        assert e.value.status == pint.PINT_ERR_UNSUPPORTED
