@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--path", default="fused", choices=["fused", "stream"],
                     help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
+    ap.add_argument("--real", action="store_true",
+                    help="real-data half spectrum (SURVEY §8(f) 2b; fused path): solves p <= N/2 only")
     ap.add_argument("--dst-per-iter", action="store_true",
                     help="ablation (SURVEY §8(a) A6): DST-x around every S-pass instead of hoisted (streaming)")
     args = ap.parse_args()
@@ -214,7 +216,7 @@ def main():
     plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
                      stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
                      allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"),
-                     dst_per_iter=args.dst_per_iter)
+                     dst_per_iter=args.dst_per_iter, real_data=args.real)
     v = torch.from_numpy(prob.v).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(prob.g)).to(dev) if prob.R else None
     plan.set_problem(v, g, prob.phi if prob.R else None, prob.dphi if prob.R else None)
@@ -262,6 +264,8 @@ def main():
         # k-level window: FP64-ALU bound (no space-time array in HBM)
         nk = path["nk"]
         fl = fused_flops_per_unknown(prob.k, nk)
+        if args.real:   # half spectrum: N/16 + 1 of the N/8 frequency groups are solved
+            fl *= (prob.N // 16 + 1) / (prob.N // 8)
         smx = 1965.0
         try:
             smx = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
@@ -342,7 +346,8 @@ def main():
                           "grid": f"{prob.mx}x{prob.my}", "N": prob.N, "k": prob.k, "kappa": prob.kappa,
                           "alpha": prob.alpha, "unknowns": total_unknowns,
                           "parallelism": f"x-mode slabs x{world}" if world > 1 else "1 GPU",
-                          "path": ("fused" if path["fused"] else "stream") + ("+dst-per-iter" if args.dst_per_iter else ""),
+                          "path": ("fused" if path["fused"] else "stream") + ("+dst-per-iter" if args.dst_per_iter else "")
+                                  + ("+real-half-spectrum" if args.real else ""),
                           "l2": (f"fused: per-iteration working set (X, line constants, window, partials) "
                                  f"{(16 * (8 + 3 * prob.k) * prob.M + 192 * prob.N * prob.M // prob.my) / 1e9:.2f} GB"
                                  " > L2 126 MB, no flush needed" if path["fused"] else

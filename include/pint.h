@@ -64,9 +64,12 @@ enum {
                                   (A/B, tests); default prunes to the k window outputs / n_k inputs */
   PINT_FLAG_STREAM = 4,        /* heat: use the two-pass streaming iteration (H and W arrays in HBM)
                                   instead of the default fused one-kernel iteration (A/B, tests) */
-  PINT_FLAG_DST_PER_ITER = 8   /* 2D, one rank: ablation of the DST hoisting: keep
+  PINT_FLAG_DST_PER_ITER = 8,  /* 2D, one rank: ablation of the DST hoisting: keep
                                   the arrays in physical x and apply DST-x before and after the
                                   shifted solves every iteration (streaming path; same iterate) */
+  PINT_FLAG_REAL_DATA = 16     /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
+                                  and only the frequencies p <= N/2 are solved (SURVEY §8(f) item
+                                  2b); pint_set_problem_separable returns ARG for complex data */
 };
 
 typedef struct {

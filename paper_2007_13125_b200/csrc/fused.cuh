@@ -53,6 +53,8 @@ struct FusedArgs {
   int L, Lf, Lpad, WB, NB, k, nk, ndense, nch, gpc;
   unsigned long long* prof; // profiling builds (-DPINT_FUSED_PROF): cycles per phase, total + per warp
   int xs;                  // 1: X of the CTA's x-mode staged once into shared memory (TMEM variant, nk small)
+  int half;                // 1: real data (PINT_FLAG_REAL_DATA): W_{N-p} = conj(W_p), so only the groups
+                           //    i <= N/16 are solved and the others enter the window as conjugates
   int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
                            // 8 u-form recurrences on every line
 };
@@ -338,6 +340,14 @@ __device__ __forceinline__ void tw_put(uint32_t (&w)[24], int s, double2 v) {
   w[4 * s] = (uint32_t)a; w[4 * s + 1] = (uint32_t)(a >> 32); w[4 * s + 2] = (uint32_t)b; w[4 * s + 3] = (uint32_t)(b >> 32);
 }
 
+// Window contribution of group i: c = e^{2 pi i n i/N} Y.  Real data (half spectrum): the group's
+// conjugate partner N/8 - i (lines p <-> N - p) adds conj(c), so a pair contributes 2 Re(c); the
+// self-conjugate groups 0 and N/16 contribute Re(c).
+__device__ __forceinline__ double2 wcontrib(double2 Y, double2 w, int half, double hw) {
+  const double2 c = cmul(Y, w);
+  return half ? make_double2(hw * c.x, 0.0) : c;
+}
+
 // Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
 // next synthesis and the group's twiddles are issued first (one memory round trip), then each row
 // reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
@@ -351,6 +361,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
   const int i1 = i + 1;
   // ---- Step 3 (window of group i) for all rows of this thread ----
   if (WINDOW && !(a.dbg & 2)) {
+    const double hw = (i == 0 || 16 * i == N) ? 1.0 : 2.0;      // half spectrum: pair weight
     double2 tww[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -375,7 +386,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
         dft8<+1>(x);                                     // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
 #pragma unroll
         for (int r = 2; r < 8; ++r)
-          if (r - 8 + k >= 0) tw_put(w[rr], r - 2, cfma(x[r], tww[r], tw_get(w[rr], r - 2)));
+          if (r - 8 + k >= 0) tw_put(w[rr], r - 2, cadd(tw_get(w[rr], r - 2), wcontrib(x[r], tww[r], a.half, hw)));
         tmem_st24(tacc + 24 * rr, w[rr]);
       }
     } else {
@@ -390,7 +401,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int j = r - 8 + k;
-          if (j >= 0) acc[j * LF + y] = cfma(x[r], tww[r], acc[j * LF + y]);
+          if (j >= 0) acc[j * LF + y] = cadd(acc[j * LF + y], wcontrib(x[r], tww[r], a.half, hw));
         }
       }
     }
@@ -484,8 +495,9 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
   double2* Xs = xch + (LANES == 64 ? 32 : 0);          // [nk][LF] X of this x-mode (a.xs)
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
-  const int NG = (int)(a.N / FG);
-  const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NG);
+  const int NG = (int)(a.N / FG);                      // line stride of a group
+  const int NGL = a.half ? NG / 2 + 1 : NG;             // groups solved (half spectrum: i <= N/16)
+  const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NGL);
   const int warp = threadIdx.x >> 5;
   const int line = LANES == 64 ? warp >> 1 : warp, half = LANES == 64 ? warp & 1 : 0;
   const double2* Xg = a.X + q * 8 * LF;

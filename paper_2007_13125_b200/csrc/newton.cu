@@ -32,4 +32,9 @@ cudaError_t launch_nl_diffmax(const double2* A, const double2* B, long count, un
   return cudaGetLastError();
 }
 
+cudaError_t launch_imag_max(const double2* A, long count, unsigned long long* upd, cudaStream_t st) {
+  imag_max_kernel<<<grid_for(count, 256), 256, 0, st>>>(A, count, upd);
+  return cudaGetLastError();
+}
+
 }  // namespace pint

@@ -130,6 +130,15 @@ __global__ void nl_diffmax_kernel(const double2* A, const double2* B, long count
   if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
 }
 
+// max |Im a| over count elements -> upd (PINT_FLAG_REAL_DATA input check)
+__global__ void imag_max_kernel(const double2* A, long count, unsigned long long* upd) {
+  double m = 0.0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(A[e].y));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
+}
+
 #endif  // PINT_DEFINE_NEWTON_KERNELS
 
 }  // namespace pint

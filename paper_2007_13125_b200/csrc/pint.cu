@@ -163,6 +163,7 @@ struct pint_plan_s {
   unsigned long long* upd = nullptr;
   // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
   bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
+  bool half = false;          // PINT_FLAG_REAL_DATA: half-spectrum fused iteration
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
@@ -404,7 +405,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    const long slots = (long)nsm * per, NG = N / 8;
+    p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
+    const long slots = (long)nsm * per, NG = p->half ? N / 16 + 1 : N / 8;
     // chunks of frequency groups per x-mode: smallest power of two giving >= 90% wave efficiency
     long best = 1;
     double beff = 0.0;
@@ -415,7 +417,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       if (eff >= 0.9) { best = c; break; }
     }
     p->nch = (int)best;
-    p->gpc = (int)(NG / best);
+    p->gpc = (int)((NG + best - 1) / best);
     for (int i = 0; i < 2; ++i)
       if ((st = dalloc(p, &p->X[i], (size_t)p->Qb * 8 * p->Lf)) != PINT_OK) return bail(st);
     if ((st = dalloc(p, &p->lc, (size_t)p->Qb * N)) != PINT_OK) return bail(st);
@@ -559,6 +561,7 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.P = p->Pp; a.W = p->B;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
+  a.half = p->half ? 1 : 0;
   // X staged in shared memory when it fits next to the lines (TMEM variant: no window sums in smem)
   static const bool noxs = getenv("PINT_FUSED_NO_XS") != nullptr;   // A/B switch
   a.xs = (!noxs && p->ftm &&
@@ -576,7 +579,12 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
 
 static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
   FusedArgs a = fargs(p, X);
-  if (store_w) a.xs = 0;   // the materialising variant keeps the shared-memory layout without X
+  if (store_w) {   // materialising variant: shared-memory layout without X, every frequency group
+    a.xs = 0;
+    a.half = 0;
+    a.nch = 1;
+    a.gpc = (int)(p->N / 8);
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing && !store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
@@ -685,7 +693,10 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     p->S = S;
   }
   CUDA_TRY(cudaMemsetAsync(p->src, 0, (size_t)S * p->ntiles * p->WB * sizeof(double2), p->stream));
+  const bool chk_real = (p->flags & PINT_FLAG_REAL_DATA) != 0;
+  if (chk_real) CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
   CUDA_TRY(cudaMemcpyAsync(p->phys, v, M * sizeof(double2), kind, p->stream));
+  if (chk_real) CUDA_TRY(launch_imag_max(p->phys, M, p->upd, p->stream));
   const double ihx2 = (double)((ld)(p->mx + 1) * (ld)(p->mx + 1));
   const double ihy2 = (double)((ld)(p->my + 1) * (ld)(p->my + 1));
   CUDA_TRY(launch_stencil(p->phys, p->phys + M, (int)p->mx, (int)p->my, ihx2, ihy2, p->stream));
@@ -694,7 +705,16 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
   TRY(to_source(p, p->phys + M, 1));
   for (int r = 0; r < R; ++r) {
     CUDA_TRY(cudaMemcpyAsync(p->phys, (const double2*)g + (size_t)r * M, M * sizeof(double2), kind, p->stream));
+    if (chk_real) CUDA_TRY(launch_imag_max(p->phys, M, p->upd, p->stream));
     TRY(to_source(p, p->phys, 2 + r));
+  }
+  if (chk_real) {
+    double im = 0.0;
+    unsigned long long bits = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bits, p->upd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    std::memcpy(&im, &bits, sizeof(im));
+    if (im != 0.0) return fail(PINT_ERR_ARG, "PINT_FLAG_REAL_DATA: v or g has a nonzero imaginary part");
   }
 
   // time coefficients of F_static_n = f̄_n + tau^-a (sum_{j<n} omega_j) v, 1-based n = row+1:
@@ -774,6 +794,16 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
   if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "user initial guess with nranks > 1");
   const size_t bytes = (size_t)p->N * p->M * sizeof(double2);
   CUDA_TRY(cudaMemcpyAsync(p->B, U0, bytes, mem == PINT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, p->stream));
+  if (p->flags & PINT_FLAG_REAL_DATA) {
+    CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+    CUDA_TRY(launch_imag_max(p->B, p->N * p->M, p->upd, p->stream));
+    unsigned long long bits = 0;
+    double im = 0.0;
+    CUDA_TRY(cudaMemcpyAsync(&bits, p->upd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    std::memcpy(&im, &bits, sizeof(im));
+    if (im != 0.0) return fail(PINT_ERR_ARG, "PINT_FLAG_REAL_DATA: U0 has a nonzero imaginary part");
+  }
   if (p->dim == 1) {
     RemapArgs r{};
     r.in = p->B; r.out = p->A; r.count = p->N * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;

@@ -61,6 +61,11 @@ class Problem:
     def with_(self, **kw) -> "Problem":
         return dataclasses.replace(self, **kw)
 
+    def real_part(self) -> "Problem":
+        """The same record with real v and g (real-data variants of the random problems)."""
+        return dataclasses.replace(self, name=self.name + "_real", v=self.v.real.astype(np.complex128),
+                                   g=self.g.real.astype(np.complex128))
+
 
 def grid1d(m: int) -> np.ndarray:
     h = 1.0 / (m + 1)

@@ -356,3 +356,37 @@ def test_newton_wr_rejects_2d(pint):
         with pytest.raises(pint.PintError) as e:
             p.set_nonlinearity(1.0)
         assert e.value.status == pint.PINT_ERR_UNSUPPORTED
+
+
+REAL_CASES = [
+    ("C1", lambda: inputs.config_c1()),
+    ("C2k6", lambda: inputs.config_c2(k=6, kappa=1e-3)),
+    ("C3", lambda: inputs.config_c3()),
+    ("2D-real", lambda: inputs.random_complex_problem(63, 40, 256, 4, 0.05, 1.0, R=1, seed=5).real_part()),
+    ("1D-N16", lambda: inputs.random_complex_problem(37, 1, 16, 1, 0.3, 1.0, R=2, seed=8).real_part()),
+]
+
+
+@pytest.mark.parametrize("name,make", REAL_CASES, ids=[c[0] for c in REAL_CASES])
+def test_real_data_half_spectrum(pint, name, make):
+    """for real data W_{N-p} = conj(W_p), so the fused iteration solves only
+    p <= N/2 (PINT_FLAG_REAL_DATA).  Same iterates as the full spectrum and the oracle, read after
+    every m and unread."""
+    prob = make()
+    o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
+    half, _ = gpu_iterates(pint, prob, 3, real_data=True)
+    full, _ = gpu_iterates(pint, prob, 3)
+    for m in range(3):
+        assert rel(half[m], full[m]) < 1e-12
+        assert rel(half[m], o[m + 1]) < TOL
+    with pint.Plan.from_problem(prob, real_data=True) as p:
+        for _ in range(3):
+            p.iterate()
+        assert rel(p.get_solution(), o[3]) < TOL
+
+
+def test_real_data_rejects_complex(pint):
+    prob = inputs.random_complex_problem(31, 1, 64, 2, 0.1, 1.0, R=1, seed=2)
+    with pytest.raises(pint.PintError) as e:
+        pint.Plan.from_problem(prob, real_data=True)
+    assert e.value.status == pint.PINT_ERR_ARG
