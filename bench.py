@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--path", default="fused", choices=["fused", "stream"],
                     help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
+    ap.add_argument("--modal", action="store_true",
+                    help="fully modal variant (SURVEY §8(f) 2a; 2D heat): DST along y too, divisions instead of line solves")
     ap.add_argument("--real", action="store_true",
                     help="real-data half spectrum (SURVEY §8(f) 2b; fused path): solves p <= N/2 only")
     ap.add_argument("--dst-per-iter", action="store_true",
@@ -216,7 +218,7 @@ def main():
     plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
                      stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
                      allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"),
-                     dst_per_iter=args.dst_per_iter, real_data=args.real)
+                     dst_per_iter=args.dst_per_iter, real_data=args.real, modal=args.modal)
     v = torch.from_numpy(prob.v).to(dev)
     g = torch.from_numpy(np.ascontiguousarray(prob.g)).to(dev) if prob.R else None
     plan.set_problem(v, g, prob.phi if prob.R else None, prob.dphi if prob.R else None)
@@ -264,6 +266,8 @@ def main():
         # k-level window: FP64-ALU bound (no space-time array in HBM)
         nk = path["nk"]
         fl = fused_flops_per_unknown(prob.k, nk)
+        if args.modal:   # Step 2 is one complex division (~12 flops) instead of the 48-flop line solve
+            fl = fl - 48.0 + 12.0
         if args.real:   # half spectrum: N/16 + 1 of the N/8 frequency groups are solved
             fl *= (prob.N // 16 + 1) / (prob.N // 8)
         smx = 1965.0
@@ -276,7 +280,8 @@ def main():
         achieved = flops_launch / (s_avg / 1e3) / 1e12
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(f"{args.config}:fused")
-        roofline = {"bound": "alu", "kernel": "wr_fused_kernel", "achieved": achieved, "peak": peak,
+        roofline = {"bound": "alu", "kernel": "wr_modal_kernel" if args.modal else "wr_fused_kernel",
+                    "achieved": achieved, "peak": peak,
                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                     "peak_source": f"derived: 2 x {FP64_FMA_PER_CLK_SM} FP64 FMA/clk/SM x SMs x {smx:.0f} MHz (DESIGN.md §5)",
                     "algorithmic_flops_per_unknown": fl, "algorithmic_flops_per_launch": flops_launch,
@@ -347,7 +352,7 @@ def main():
                           "alpha": prob.alpha, "unknowns": total_unknowns,
                           "parallelism": f"x-mode slabs x{world}" if world > 1 else "1 GPU",
                           "path": ("fused" if path["fused"] else "stream") + ("+dst-per-iter" if args.dst_per_iter else "")
-                                  + ("+real-half-spectrum" if args.real else ""),
+                                  + ("+real-half-spectrum" if args.real else "") + ("+fully-modal" if args.modal else ""),
                           "l2": (f"fused: per-iteration working set (X, line constants, window, partials) "
                                  f"{(16 * (8 + 3 * prob.k) * prob.M + 192 * prob.N * prob.M // prob.my) / 1e9:.2f} GB"
                                  " > L2 126 MB, no flush needed" if path["fused"] else

@@ -67,9 +67,14 @@ enum {
   PINT_FLAG_DST_PER_ITER = 8,  /* 2D, one rank: ablation of the DST hoisting: keep
                                   the arrays in physical x and apply DST-x before and after the
                                   shifted solves every iteration (streaming path; same iterate) */
-  PINT_FLAG_REAL_DATA = 16     /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
+  PINT_FLAG_REAL_DATA = 16,    /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
                                   and only the frequencies p <= N/2 are solved (SURVEY §8(f) item
                                   2b); pint_set_problem_separable returns ARG for complex data */
+  PINT_FLAG_MODAL = 32         /* 2D heat: fully modal variant — the DST is
+                                  applied along y as well (hoisted), every (x-mode, y-mode) is a
+                                  scalar problem and the shifted solves are divisions; needs
+                                  2(my+1) a power of two (UNSUPPORTED otherwise), excludes
+                                  PINT_FLAG_STREAM / PINT_FLAG_DST_PER_ITER (ARG) */
 };
 
 typedef struct {

@@ -12,7 +12,10 @@
 
 namespace pint {
 
-enum { DST_PHYS_TO_SRC = 0, DST_PHYS_LEVELS_TO_INT = 1, DST_INT_TO_PHYS_LEVELS = 2, DST_ROWS = 3, DST_INT_TO_INT = 4 };
+enum { DST_PHYS_TO_SRC = 0, DST_PHYS_LEVELS_TO_INT = 1, DST_INT_TO_PHYS_LEVELS = 2, DST_ROWS = 3, DST_INT_TO_INT = 4,
+       // along y inside the tile layout [q][yb][N][WB] (fully modal path): row = q * N + level,
+       // element y (transform length a.mx := my)
+       DST_TILE_Y = 5 };
 
 struct DstArgs {
   const double2* in;
@@ -27,6 +30,10 @@ struct DstArgs {
 __device__ __forceinline__ long dst_in_index(const DstArgs& a, int mode, long row, int x) {
   if (mode == DST_PHYS_TO_SRC) return row * a.mx + x;
   if (mode == DST_PHYS_LEVELS_TO_INT) return (row / a.my) * a.M + (row % a.my) * a.mx + x;
+  if (mode == DST_TILE_Y) {
+    const long qq = row / a.N, nl = row % a.N;
+    return ((qq * a.NB + x / a.WB) * a.N + nl) * a.WB + x % a.WB;
+  }
   if (mode == DST_INT_TO_PHYS_LEVELS || mode == DST_INT_TO_INT) {
     const long nl = row / a.my, y = row % a.my;
     return (((long)x * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;
@@ -47,6 +54,10 @@ __device__ __forceinline__ long dst_out_index(const DstArgs& a, int mode, long r
     return ((ql * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;
   }
   if (mode == DST_INT_TO_PHYS_LEVELS) return (row / a.my) * a.M + (row % a.my) * a.mx + q;
+  if (mode == DST_TILE_Y) {
+    const long qq = row / a.N, nl = row % a.N;
+    return ((qq * a.NB + q / a.WB) * a.N + nl) * a.WB + q % a.WB;
+  }
   if (mode == DST_INT_TO_INT) {   // tile layout, x index -> mode index (per-iteration DST ablation)
     const long nl = row / a.my, y = row % a.my;
     return (((long)q * a.NB + y / a.WB) * a.N + a.n0 + nl) * a.WB + y % a.WB;

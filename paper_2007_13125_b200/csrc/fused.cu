@@ -75,6 +75,15 @@ int fused_rows_per_subchain(int lanes, int C) {
   return C / (C < nsmax ? C : nsmax);
 }
 
+cudaError_t launch_modal(bool store_w, const FusedArgs& a, cudaStream_t st) {
+  const long warps = a.Qb * (long)a.L;
+  const long blocks = (warps * 32 + 255) / 256;
+  if (blocks <= 0) return cudaSuccess;
+  if (store_w) wr_modal_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else wr_modal_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st) {
   const long total = a.Qb * a.Lf;
   const long blocks = std::min<long>((total + TPB - 1) / TPB, 148L * 8);

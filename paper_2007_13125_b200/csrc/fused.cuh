@@ -55,6 +55,9 @@ struct FusedArgs {
   int xs;                  // 1: X of the CTA's x-mode staged once into shared memory (TMEM variant, nk small)
   int half;                // 1: real data (PINT_FLAG_REAL_DATA): W_{N-p} = conj(W_p), so only the groups
                            //    i <= N/16 are solved and the others enter the window as conjugates
+  const double* mu;        // fully modal path (PINT_FLAG_MODAL): [L] mu_j = 4 sin^2(j pi h_y / 2)
+  const double2* sig_p;    // modal path: [N] h^2 d_p / tau^a
+  const double* sig_q;     // modal path: [Qb] h^2 lambda_q
   int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
                            // 8 u-form recurrences on every line
 };
@@ -596,6 +599,89 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     } else {
       for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
         for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Fully modal variant (PINT_FLAG_MODAL): with the DST applied along y as well
+// (hoisted like the DST-x), every (x-mode q, y-mode j) is a scalar problem and Step 2 is a division,
+// W_p = H_p / (sigma_{p,q} + mu_j), mu_j = 2 - 2 cos(j pi h_y) (eigenvalues of tridiag(-1, 2, -1)):
+// the shift is never added to 2, so the division is shift-accurate by construction.  One warp per
+// mode; lane l takes the frequency groups i = l, l + 32, ...: synthesis (twiddle + DFT8), division,
+// window (DFT8 + k twiddled accumulations) in registers; a warp reduction of the k window sums.
+// No shared memory, no barriers; the finish kernel is the line path's (y index = mode j).
+// STORE_W: write W (every p) into the tile layout [q][jb][N][WB] for materialisation.
+#ifndef PINT_MODAL_MINB
+#define PINT_MODAL_MINB 2
+#endif
+template <bool STORE_W>
+__global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const FusedArgs a) {
+  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.Qb * (long)a.L) return;                       // warp-uniform
+  const long q = gw / a.L;
+  const int j = (int)(gw % a.L);
+  const int N = (int)a.N, k = a.k, nk = a.nk;
+  const int NG = N / FG;
+  const int NGL = (a.half && !STORE_W) ? NG / 2 + 1 : NG;
+  double2 X[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) X[t] = (t < nk) ? a.X[(q * 8 + t) * a.Lf + j] : make_double2(0.0, 0.0);
+  const double cm = __ldg(&a.sig_q[q]) + __ldg(&a.mu[j]);
+  double2 acc[6];
+#pragma unroll
+  for (int l = 0; l < 6; ++l) acc[l] = make_double2(0.0, 0.0);
+  for (int i = lane; i < NGL; i += 32) {
+    double2 z[8];
+    z[0] = X[0];
+#pragma unroll
+    for (int t = 1; t < 8; ++t) z[t] = (t < nk) ? cmul(X[t], __ldg(&a.tw[t * i])) : make_double2(0.0, 0.0);
+    dft8<-1>(z);                                            // H_{i + (N/8) s}
+    for (int dd = 0; dd < a.ndense; ++dd) {
+      const double2 g = __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * a.Qb + q) * a.Lpad + j]);
+      const double2* ch = a.chat + (long)dd * N + i;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) z[s2] = cfma(__ldg(&ch[s2 * NG]), g, z[s2]);
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) {                        // Step 2: W_p = H_p / (sigma_p + c)
+      const double2 sp = __ldg(&a.sig_p[i + s2 * NG]);
+      z[s2] = cdiv(z[s2], make_double2(sp.x + cm, sp.y));
+    }
+    if constexpr (STORE_W) {
+      double2* Wq = a.W + ((q * a.NB + j / a.WB) * a.N) * a.WB + j % a.WB;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) Wq[(long)(i + s2 * NG) * a.WB] = z[s2];
+    } else {
+      dft8<+1>(z);                                          // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
+      const double hw = (i == 0 || 16 * i == N) ? 1.0 : 2.0;
+#pragma unroll
+      for (int r = 2; r < 8; ++r) {
+        const int l = r - 8 + k;                            // window level N - 8 + r = N - k + l
+        if (l >= 0) {
+          double2 w = __ldg(&a.tw[((N - 8 + r) * i) & (N - 1)]);
+          w.y = -w.y;
+          acc[r - 2] = cadd(acc[r - 2], wcontrib(z[r], w, a.half, hw));
+        }
+      }
+    }
+  }
+  if constexpr (!STORE_W) {
+#pragma unroll
+    for (int r = 2; r < 8; ++r)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[r - 2].x += __shfl_xor_sync(0xffffffffu, acc[r - 2].x, o);
+        acc[r - 2].y += __shfl_xor_sync(0xffffffffu, acc[r - 2].y, o);
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 2; r < 8; ++r) {
+        const int l = r - 8 + k;
+        if (l >= 0) a.P[(q * k + l) * a.Lf + j] = acc[r - 2];
+      }
     }
   }
 }

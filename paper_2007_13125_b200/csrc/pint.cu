@@ -164,6 +164,11 @@ struct pint_plan_s {
   // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
   bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
   bool half = false;          // PINT_FLAG_REAL_DATA: half-spectrum fused iteration
+  bool modal = false;         // PINT_FLAG_MODAL: DST along y too, one warp per (q, j) mode
+  int NEy = 0;
+  double2* twEy = nullptr;    // [NEy] DST-y twiddles
+  double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
+  double2* wtmp = nullptr;    // [ntiles][k][WB] modal window -> (q, y) staging
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
@@ -309,6 +314,14 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (nranks > op->mx) return fail(PINT_ERR_ARG, "nranks must be <= mx");
   if (opt && (opt->flags & PINT_FLAG_DST_PER_ITER) && (op->kind != PINT_OP_FD2D_DIRICHLET || nranks != 1))
     return fail(PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator on one rank");
+  if (opt && (opt->flags & PINT_FLAG_MODAL)) {
+    if (op->kind != PINT_OP_FD2D_DIRICHLET || (opt->alpha != 1.0))
+      return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL needs a 2D heat problem (alpha = 1)");
+    if (opt->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER))
+      return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL excludes PINT_FLAG_STREAM and PINT_FLAG_DST_PER_ITER");
+    if (!is_pow2(2 * (op->my + 1)) || 2 * (op->my + 1) < 16 || 2 * (op->my + 1) > 4096)
+      return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_MODAL needs 2(my+1) a power of two in [16, 4096]");
+  }
   if (nranks > 1 && !(opt && opt->allreduce_max)) return fail(PINT_ERR_ARG, "nranks > 1 needs allreduce_max");
   if (!is_pow2(N) || N < 16 || N > 4096) return fail(PINT_ERR_UNSUPPORTED, "N must be a power of two in [16, 4096]");
   const int dim = op->kind == PINT_OP_FD1D_DIRICHLET ? 1 : 2;
@@ -401,7 +414,25 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   const size_t fsmem = fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
   p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
   p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u - 64u;
-  if (p->fused_ok) {
+  p->modal = (p->flags & PINT_FLAG_MODAL) != 0;
+  if (p->modal) {
+    p->Lf = (int)(p->NB * p->WB);    // X / partials indexed by the y-mode j < my
+    p->NEy = (int)(2 * (op->my + 1));
+  }
+  if (p->fused_ok && p->modal) {
+    p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
+    p->nch = 1;
+    p->gpc = (int)(N / 8);
+    for (int i = 0; i < 2; ++i)
+      if ((st = dalloc(p, &p->X[i], (size_t)p->Qb * 8 * p->Lf)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->Pp, (size_t)p->Qb * k * p->Lf)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->twEy, p->NEy)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->mu, (size_t)op->my)) != PINT_OK) return bail(st);
+    for (int i = 0; i < 2; ++i) {
+      ce = cudaMemsetAsync(p->X[i], 0, (size_t)p->Qb * 8 * p->Lf * sizeof(double2), p->stream);
+      if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
+    }
+  } else if (p->fused_ok) {
     const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
@@ -484,7 +515,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->thm, thm)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
-  if (p->fused_ok) {
+  if (p->fused_ok && !p->modal) {
     ce = launch_line_const(p->lc, p->sig_p, p->sig_q, N, p->Qb, p->Cf, fused_rows_per_subchain(p->flanes, p->Cf), (int)L,
                            p->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(p->stream);
@@ -497,6 +528,20 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       twE[m] = make_double2((double)cosl(ang), (double)-sinl(ang));
     }
     if ((st = h2d(p, p->twE, twE)) != PINT_OK) return bail(st);
+  }
+  if (p->modal && p->fused_ok) {
+    std::vector<double2> twEy(p->NEy);
+    for (int m = 0; m < p->NEy; ++m) {
+      const ld ang = 2.0L * PI_L * (ld)m / (ld)p->NEy;
+      twEy[m] = make_double2((double)cosl(ang), (double)-sinl(ang));
+    }
+    if ((st = h2d(p, p->twEy, twEy)) != PINT_OK) return bail(st);
+    std::vector<double> mu(p->my);
+    for (int64_t jj = 0; jj < p->my; ++jj) {
+      const ld sn = sinl((ld)(jj + 1) * PI_L / (2.0L * (ld)(p->my + 1)));
+      mu[jj] = (double)(4.0L * sn * sn);
+    }
+    if ((st = h2d(p, p->mu, mu)) != PINT_OK) return bail(st);
   }
   *out = p;
   return PINT_OK;
@@ -562,6 +607,7 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
   a.half = p->half ? 1 : 0;
+  a.mu = p->mu; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
   // X staged in shared memory when it fits next to the lines (TMEM variant: no window sums in smem)
   static const bool noxs = getenv("PINT_FUSED_NO_XS") != nullptr;   // A/B switch
   a.xs = (!noxs && p->ftm &&
@@ -590,7 +636,8 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
-  CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, p->ftm, a, p->stream));
+  if (p->modal) CUDA_TRY(launch_modal(store_w, a, p->stream));
+  else CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, p->ftm, a, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
   return PINT_OK;
@@ -623,6 +670,19 @@ static DstArgs dargs(pint_plan p) {
   a.scale = (double)sqrtl(2.0L / (ld)(p->mx + 1));
   a.tw = p->twE;
   return a;
+}
+
+// DST along y inside the tile layout (fully modal path): rows = nq x-modes x `levels` levels
+static pint_status dst_y(pint_plan p, const double2* in, double2* out, long levels, long nq) {
+  DstArgs a{};
+  a.in = in; a.out = out; a.rows = nq * levels;
+  a.mx = (int)p->my; a.my = 1; a.WB = p->WB; a.NB = p->NB; a.N = levels; a.n0 = 0;
+  a.q0 = 0; a.Qb = nq; a.M = p->M;
+  a.scale = (double)sqrtl(2.0L / (ld)(p->my + 1));
+  a.tw = p->twEy;
+  CUDA_TRY(launch_dst(p->NEy, a, DST_TILE_Y, p->stream));
+  ++p->launches;
+  return PINT_OK;
 }
 
 // physical vector [M] (device) -> source slot s (tile layout [ntiles][WB]; DST-x in 2D)
@@ -708,6 +768,7 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     if (chk_real) CUDA_TRY(launch_imag_max(p->phys, M, p->upd, p->stream));
     TRY(to_source(p, p->phys, 2 + r));
   }
+  if (p->modal && p->fused_ok) TRY(dst_y(p, p->src, p->src, 1, (long)S * p->Qb));   // sources -> (q, j) modes
   if (chk_real) {
     double im = 0.0;
     unsigned long long bits = 0;
@@ -821,7 +882,12 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
   }
   ++p->launches;
   // H_1 and the wrap state of U_0 from the time-domain array
-  TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
+  if (p->fused && p->modal) {   // fully modal: the window lives in (q, j) space
+    TRY(dst_y(p, p->A, p->B, p->N, p->Qb));
+    TRY(tpass(p, IN_TIME_BUF, OUT_H, p->B, p->A, nullptr, p->wrap[p->wcur], false));
+  } else {
+    TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
+  }
   if (p->fused) TRY(finish_pass(p, FIN_FROM_WRAP, p->wrap[p->wcur], nullptr, p->X[p->xcur]));
   p->stateA = 0;
   p->m = 0;
@@ -1060,6 +1126,17 @@ extern "C" pint_status pint_newton_solve(pint_plan p, int32_t max_outer, double 
 // ------------------------------------------------------------------------------------------
 static pint_status materialize(pint_plan p) {
   if (p->stateA == 1) return PINT_OK;
+  if (p->fused && p->modal) {
+    // W_m per (q, j) mode into A, U_m = Gamma^{-1} V W_m into B, DST-y back to (q, y) into A
+    FusedArgs a = fargs(p, p->X[1 - p->xcur]);
+    a.W = p->A; a.half = 0;
+    CUDA_TRY(launch_modal(true, a, p->stream));
+    ++p->launches;
+    TRY(tpass(p, IN_FREQ, OUT_U, p->A, p->B, nullptr, nullptr, false));
+    TRY(dst_y(p, p->B, p->A, p->N, p->Qb));
+    p->stateA = 1;
+    return PINT_OK;
+  }
   // fused: W_m = solve(H_m) with H_m synthesised from the X that produced it, into B
   if (p->fused) TRY(fused_pass(p, p->X[1 - p->xcur], true));
   // U_m = Gamma^{-1} V W_m (Step 3) from B into A (time domain)
@@ -1089,6 +1166,12 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
     // levels inside the window n = N-k..N-1: read from the wrap state (no materialisation)
     if (!p->wstage) TRY(dalloc(p, &p->wstage, (size_t)p->k * p->M));
     double2* wdst = mem == PINT_DEVICE ? (double2*)U : p->wstage;
+    const double2* wsrc = p->wrap[p->wcur];
+    if (p->fused && p->modal) {   // window levels are (q, j)-modal: DST-y back first
+      if (!p->wtmp) TRY(dalloc(p, &p->wtmp, (size_t)p->ntiles * p->k * p->WB));
+      TRY(dst_y(p, p->wrap[p->wcur], p->wtmp, p->k, p->Qb));
+      wsrc = p->wtmp;
+    }
     if (p->dim == 1) {
       RemapArgs r{};
       r.in = p->wrap[p->wcur]; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
@@ -1101,7 +1184,7 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
       CUDA_TRY(launch_remap(r, RM_INT_TO_2D_LEVELS, p->stream));
     } else {
       DstArgs a = dargs(p);
-      a.in = p->wrap[p->wcur]; a.out = wdst; a.rows = n_count * p->my; a.N = p->k; a.n0 = n_begin - (p->N - p->k);
+      a.in = wsrc; a.out = wdst; a.rows = n_count * p->my; a.N = p->k; a.n0 = n_begin - (p->N - p->k);
       CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
     }
     ++p->launches;

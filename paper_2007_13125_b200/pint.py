@@ -24,6 +24,7 @@ PINT_FLAG_STREAM = 4
 PINT_FLAG_DST_PER_ITER = 8
 PINT_NL_ALLEN_CAHN = 1
 PINT_FLAG_REAL_DATA = 16
+PINT_FLAG_MODAL = 32
 
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
@@ -139,7 +140,8 @@ class Plan:
     def __init__(self, mx: int, my: int, N: int, k: int, kappa: float, tau: float, alpha: float = 1.0,
                  device: int = 0, stream: int | None = None, u0_zero: bool = False,
                  rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False,
-                 stream_path: bool = False, dst_per_iter: bool = False, real_data: bool = False):
+                 stream_path: bool = False, dst_per_iter: bool = False, real_data: bool = False,
+                 modal: bool = False):
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
         self.M = self.mx * self.my
@@ -155,7 +157,7 @@ class Plan:
             self._cb = ALLREDUCE_FN(_cb)
         flags = (PINT_FLAG_U0_ZERO if u0_zero else 0) | (PINT_FLAG_FULL_FFT if full_fft else 0) | \
             (PINT_FLAG_STREAM if stream_path else 0) | (PINT_FLAG_DST_PER_ITER if dst_per_iter else 0) | \
-            (PINT_FLAG_REAL_DATA if real_data else 0)
+            (PINT_FLAG_REAL_DATA if real_data else 0) | (PINT_FLAG_MODAL if modal else 0)
         opt = pint_options(alpha, device, stream or 0, flags, rank, nranks,
                            self._cb, None)
         h = ctypes.c_void_p()

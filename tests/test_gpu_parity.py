@@ -390,3 +390,37 @@ def test_real_data_rejects_complex(pint):
     with pytest.raises(pint.PintError) as e:
         pint.Plan.from_problem(prob, real_data=True)
     assert e.value.status == pint.PINT_ERR_ARG
+
+
+MODAL_CASES = [
+    ("C3", lambda: inputs.config_c3(), {}),
+    ("2D-c", lambda: inputs.random_complex_problem(63, 31, 256, 4, 0.05, 1.0, R=1, seed=6), {}),
+    ("2D-N2048", lambda: inputs.random_complex_problem(31, 63, 2048, 6, 0.01, 1.0, R=0, seed=7), {}),
+    ("2D-real-half", lambda: inputs.random_complex_problem(63, 15, 128, 2, 0.1, 1.0, R=2, seed=9).real_part(),
+     {"real_data": True}),
+]
+
+
+@pytest.mark.parametrize("name,make,kw", MODAL_CASES, ids=[c[0] for c in MODAL_CASES])
+def test_fully_modal_variant(pint, name, make, kw):
+    """SURVEY §8(f) item 2a (PINT_FLAG_MODAL): DST along y too, the shifted solves become divisions
+    per (x-mode, y-mode).  Same iterates as the line-solve path and the oracle, read after every m
+    and unread; window levels and a user initial guess go through the y-mode space correctly."""
+    prob = make()
+    o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
+    modal, _ = gpu_iterates(pint, prob, 3, modal=True, **kw)
+    lines, _ = gpu_iterates(pint, prob, 3, **kw)
+    for m in range(3):
+        assert rel(modal[m], lines[m]) < 1e-12
+        assert rel(modal[m], o[m + 1]) < TOL
+    N, k = prob.N, prob.k
+    with pint.Plan.from_problem(prob, modal=True, **kw) as p:
+        for _ in range(3):
+            p.iterate()
+        win = p.get_levels(N - k, k)
+        assert np.linalg.norm(win - o[3][N - k:]) / np.linalg.norm(o[3]) < TOL
+        assert rel(p.get_solution(), o[3]) < TOL
+        U0 = o[3].real.astype(np.complex128) if kw.get("real_data") else o[3]   # oracle roundoff in Im
+        p.set_initial_guess(np.ascontiguousarray(U0))
+        p.iterate()
+        assert rel(p.get_solution(), wr.wr_naive(prob, 1, U0=U0, dft="fft", wrap="fft")[1]) < TOL
