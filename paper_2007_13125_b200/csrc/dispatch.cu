@@ -54,12 +54,8 @@ static cudaError_t spass_go(const SPassArgs& a, long Qb, cudaStream_t st) {
   auto kern = spass_kernel<C, SG>;
   const int off = (a.WB >= 8) ? 0 : (a.WB > 8 / SG ? a.WB : 8 / SG);
   const int smem = SG * (32 * (C + 1) + off) * (int)sizeof(double2);
-  static int attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
   SPassArgs b = a;
   int lwb = 0;
   while ((1 << lwb) < a.WB) ++lwb;

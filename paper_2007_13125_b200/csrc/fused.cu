@@ -11,7 +11,7 @@ size_t fused_smem_bytes(int lanes, int C, int k, bool tm) {
 
 template <int C, int LANES, bool SW, bool TM>
 static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
-  auto kern = wr_fused_kernel<C, LANES, SW, TM>;
+  auto kern = (TM && !SW && a.half) ? wr_fused_kernel<C, LANES, SW, TM, TM && !SW> : wr_fused_kernel<C, LANES, SW, TM>;
   const size_t smem = fused_smem_bytes(LANES, C, a.k, TM && !SW) + (a.xs ? (size_t)a.nk * LANES * C * sizeof(double2) : 0);
   // set on every launch: the occupancy query at plan creation (fused_occ) also sets this attribute
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -354,7 +354,7 @@ __device__ __forceinline__ double2 wcontrib(double2 Y, double2 w, int half, doub
 // Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
 // next synthesis and the group's twiddles are issued first (one memory round trip), then each row
 // reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
-template <int C, int LANES, bool WINDOW, bool TM = false>
+template <int C, int LANES, bool WINDOW, bool TM = false, bool HALF = false>
 __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, double2* acc, const double2* Xq,
                                            long q, int i, bool next, uint32_t tacc = 0) {
   constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
@@ -389,7 +389,9 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
         dft8<+1>(x);                                     // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
 #pragma unroll
         for (int r = 2; r < 8; ++r)
-          if (r - 8 + k >= 0) tw_put(w[rr], r - 2, cadd(tw_get(w[rr], r - 2), wcontrib(x[r], tww[r], a.half, hw)));
+          if (r - 8 + k >= 0)
+            tw_put(w[rr], r - 2, HALF ? cadd(tw_get(w[rr], r - 2), wcontrib(x[r], tww[r], 1, hw))
+                                        : cfma(x[r], tww[r], tw_get(w[rr], r - 2)));
         tmem_st24(tacc + 24 * rr, w[rr]);
       }
     } else {
@@ -404,7 +406,9 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int j = r - 8 + k;
-          if (j >= 0) acc[j * LF + y] = cadd(acc[j * LF + y], wcontrib(x[r], tww[r], a.half, hw));
+          if (j >= 0)
+            acc[j * LF + y] = HALF ? cadd(acc[j * LF + y], wcontrib(x[r], tww[r], 1, hw))
+                                     : cfma(x[r], tww[r], acc[j * LF + y]);
         }
       }
     }
@@ -485,7 +489,8 @@ template <int C, int LANES> struct FTmem {
 };
 
 // TM: window partial sums in tensor memory (default) instead of shared memory.
-template <int C, int LANES, bool STORE_W, bool TM>
+// HALF: real-data half spectrum (PINT_FLAG_REAL_DATA; instantiated with TM only).
+template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false>
 __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const FusedArgs a) {
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
@@ -499,7 +504,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
   const int NG = (int)(a.N / FG);                      // line stride of a group
-  const int NGL = a.half ? NG / 2 + 1 : NG;             // groups solved (half spectrum: i <= N/16)
+  const int NGL = HALF ? NG / 2 + 1 : NG;               // groups solved (half spectrum: i <= N/16)
   const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NGL);
   const int warp = threadIdx.x >> 5;
   const int line = LANES == 64 ? warp >> 1 : warp, half = LANES == 64 ? warp & 1 : 0;
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     PINT_TS(t2);
     const bool next = i + 1 < g1;
     if (next) fused_stage_lc(a, slc, q, i + 1);
-    fused_rows<C, LANES, !STORE_W, TMA>(a, Hs, acc, Xq, q, i, next, tacc);
+    fused_rows<C, LANES, !STORE_W, TMA, HALF>(a, Hs, acc, Xq, q, i, next, tacc);
     if constexpr (TMA) tmem_wait_st();
     cp_async_wait0();
     PINT_TS(t3);

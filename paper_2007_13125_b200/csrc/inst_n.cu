@@ -9,20 +9,23 @@
 
 namespace pint {
 
+// opt in to `smem` bytes of dynamic shared memory and return SMs x resident CTAs (0 on error)
+static long persistent_grid(const void* kern, int smem) {
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
+  int dev = 0, nsm = 148, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
+  return (long)nsm * (per > 0 ? per : 1);
+}
+
 template <int MI, int MO, bool CQ>
 static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
   auto kern = tpass_kernel<PINT_N, MI, MO, CQ>;
   const int smem = phys_size(TILE) * (int)sizeof(double2);
-  static long resident = 0;   // persistent grid: SMs x resident CTAs per SM
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 148, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
-    resident = (long)nsm * (per > 0 ? per : 1);
-  }
+  // persistent grid: SMs x resident CTAs per SM (thread-safe one-time init; one device per process)
+  static const long resident = persistent_grid((const void*)kern, smem);
+  if (resident <= 0) return cudaErrorInvalidValue;
   if (ntiles <= 0) return cudaSuccess;
   const long grid = ntiles < resident ? ntiles : resident;
   kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
@@ -35,16 +38,8 @@ static cudaError_t go_pruned(const TPassArgs& a, long ntiles, cudaStream_t st) {
   auto kern = tpass_heat_pruned_kernel<PINT_N, DENSE>;
   constexpr int WBp = TILE / PINT_N;
   const int smem = (WBp * (9 * (PINT_N / 16) + 1) + WBp * (PINT_N / 256) * 16 + 16 * WBp + WBp * 16) * (int)sizeof(double2);
-  static long resident = 0;
-  if (!resident) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 148, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
-    resident = (long)nsm * (per > 0 ? per : 1);
-  }
+  static const long resident = persistent_grid((const void*)kern, smem);
+  if (resident <= 0) return cudaErrorInvalidValue;
   if (ntiles <= 0) return cudaSuccess;
   const long grid = ntiles < resident ? ntiles : resident;
   kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
@@ -82,12 +77,8 @@ cudaError_t PINT_CAT(launch_tpass_, PINT_N)(int mi, int mo, bool cq, const TPass
 cudaError_t PINT_CAT(launch_dst_, PINT_N)(const DstArgs& a, int mode, cudaStream_t st) {
   auto kern = dst_kernel<PINT_N>;
   const int smem = phys_size(TILE) * (int)sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static const long ok = persistent_grid((const void*)kern, smem);   // sets the smem attribute once
+  if (ok <= 0) return cudaErrorInvalidValue;
   const long rb = TILE / PINT_N;
   const long blocks = (a.rows + rb - 1) / rb;
   if (blocks <= 0) return cudaSuccess;

@@ -436,7 +436,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     const int per = std::max(fused_ctas_per_sm(p->flanes, p->Cf, k, p->ftm), 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
+    p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0 && p->ftm;   // the half-spectrum kernel keeps its sums in TMEM
     const long slots = (long)nsm * per, NG = p->half ? N / 16 + 1 : N / 8;
     // chunks of frequency groups per x-mode: smallest power of two giving >= 90% wave efficiency
     long best = 1;
@@ -817,17 +817,22 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
     p->nsparse = (int)lst.size();
     std::vector<double2> ch;
     const ld hl = 1.0L / (ld)(p->L + 1), Nl = (ld)N;
+    std::vector<cld> eN;                               // e^{-2 pi i m/N}, m < N (long double, built once)
     for (int s = 0; s < S; ++s) {
       if (nhi[s] <= 16) continue;
       lst.push_back(s);
+      if (eN.empty()) {
+        eN.resize(N);
+        for (int64_t m = 0; m < N; ++m) {
+          const ld ang = -2.0L * PI_L * (ld)m / Nl;
+          eN[m] = cld(cosl(ang), sinl(ang));
+        }
+      }
       std::vector<ld> cg(N);
       for (int64_t n = 0; n < N; ++n) cg[n] = (ld)coef[(size_t)s * N + n] * powl((ld)p->kappa, (ld)n / Nl) * hl * hl / Nl;
       for (int64_t pp = 0; pp < N; ++pp) {
         cld acc = 0.0L;
-        for (int64_t n = 0; n < nhi[s]; ++n) {
-          const ld ang = -2.0L * PI_L * (ld)((n * pp) % N) / Nl;
-          acc += cg[n] * cld(cosl(ang), sinl(ang));
-        }
+        for (int64_t n = 0; n < nhi[s]; ++n) acc += cg[n] * eN[(n * pp) % N];
         ch.push_back(d2(acc));
       }
     }

@@ -85,6 +85,8 @@ def lib(path: str = LIB_PATH):
         "pint_newton_solve": [P, I32, D, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(I32)],
     }
     for name, args in sig.items():
+        if not hasattr(L, name) and "PINT_LIB" in os.environ:
+            continue          # older variant library (A/B timing via PINT_LIB): extension symbols may be absent
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int

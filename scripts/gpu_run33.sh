@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+for i in 1 2; do
+PINT_LIB=$PWD/paper_2007_13125_b200/libpint_pre.so timeout 300 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/bench33_pre_$i.json 2> gpurun_out/bench33_pre_$i.err
+timeout 300 python bench.py --no-cpu --no-e2e --steps 20 > gpurun_out/bench33_cur_$i.json 2> gpurun_out/bench33_cur_$i.err
+done
