@@ -358,6 +358,9 @@ def main():
                                  " > L2 126 MB, no flush needed" if path["fused"] else
                                  f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+               "comm": ({"collective": "NCCL all_reduce(max) of the update norm, one double per iteration",
+                         "data_path_bytes_per_step": 0, "allreduce_bytes_per_step": 8,
+                         "partition": f"x-mode slabs (rank 0: q in [{q0}, {q1}))"} if world > 1 else None),
                "clocks": clk.summary(), "last_update": upd[-1] if upd else None}
         print(json.dumps(res))
     plan.close()
