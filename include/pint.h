@@ -117,6 +117,20 @@ pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double kappa, doub
 pint_status pint_set_problem_separable(pint_plan plan, const void* v, int32_t R, const void* g,
                                        const double* phi, const double* dphi, int32_t mem);
 
+/* Problem data with a dense (non-separable) forcing:
+ *   v      [M] complex: u(0)
+ *   f      [N][M] complex: f(t_n), n = 1..N (row n-1)
+ *   f0     [M] complex: f(0) for the starting correction a_n f(0) (Table 1); NULL = 0
+ *   fderiv [max(k-2,0)][M] complex: d^l f/dt^l (0), l = 1..k-2 (b_{l,n} corrections); NULL = 0
+ * in memory space mem.  The corrections become separable sources; f(t_n) is stored as a dense
+ * right-hand side (16 B per unknown, DST-x applied per level in 2D) that the streaming T-pass adds to
+ * F_static, so the plan runs the streaming path (unpruned T-pass) afterwards.  One rank only
+ * (UNSUPPORTED otherwise, and with PINT_FLAG_MODAL / PINT_FLAG_DST_PER_ITER).  A plan cannot switch
+ * between the separable form with another R and this form (STATE).  Bootstraps like
+ * pint_set_problem_separable. */
+pint_status pint_set_problem(pint_plan plan, const void* v, const void* f, const void* f0, const void* fderiv,
+                             int32_t mem);
+
 /* Replace the WR initial guess by a full space-time array U0 [N][M] (this is U_0^1..U_0^N;
  * requires a prior pint_set_problem_separable).  Resets m to 0. */
 pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);

@@ -21,6 +21,7 @@ struct NewtonArgs {
   const double* coef;    // [S][N]   F_static_n = sum_s coef[s][n] src_s  (= fbar_n + tau^-a psum_n v)
   const double* wt;      // [N]      tau^-a omega_j (heat: zero for j > k)
   const double* anl;     // [N]      a_n of Table 1 (the -a_n g(v) part of fbar)
+  const double2* fd;     // dense forcing f(t_n) (tile layout) or NULL (pint_set_problem)
   int S, L, Lpad, WB;
   long N;
   double ih2, h2, ieps2;
@@ -74,6 +75,7 @@ __global__ void nl_residual_kernel(const NewtonArgs a) {
     r = csub(r, Au);
     r = csub(r, nl_g(u, a.ieps2));
     if (a.anl[n] != 0.0) r = cfmar(nl_g(a.src[y], a.ieps2), -a.anl[n], r);   // source 0 is v
+    if (a.fd) r = cadd(r, a.fd[((long)(y / a.WB) * a.N + n) * a.WB + y % a.WB]);
     a.R[((long)(y / a.WB) * a.N + n) * a.WB + y % a.WB] = r;
   }
 }

@@ -169,6 +169,8 @@ struct pint_plan_s {
   double2* twEy = nullptr;    // [NEy] DST-y twiddles
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
   double2* wtmp = nullptr;    // [ntiles][k][WB] modal window -> (q, y) staging
+  double2* fd = nullptr;      // dense forcing f(t_1..t_N) in the tile layout (pint_set_problem)
+  bool has_fd = false;
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
@@ -563,6 +565,11 @@ static TPassArgs targs(pint_plan p) {
   a.ndense = p->ndense; a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat;
   static const bool nopf = getenv("PINT_NO_PREFETCH") != nullptr;   // A/B switch (profiling)
   a.prefetch = nopf ? 0 : 1;
+  if (p->has_fd) {   // dense forcing: F_static += f(t_n) at every level (streaming path, unpruned)
+    a.fdense = p->fd;
+    a.nmax = (int)p->N;
+    a.nk = (int)p->N;
+  }
   return a;
 }
 
@@ -576,7 +583,7 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
   const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 256 &&
-                      p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT);
+                      p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT) && !p->has_fd;
   if (pruned) CUDA_TRY(launch_tpass_pruned((int)p->N, a, p->ntiles, p->stream));
   else CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
   ++p->launches;
@@ -728,8 +735,18 @@ static pint_status bootstrap(pint_plan p) {
   return PINT_OK;
 }
 
+static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const void* g, const double* phi,
+                                    const double* dphi, int32_t mem, bool boot);
+
 extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, int32_t R, const void* g,
                                                   const double* phi, const double* dphi, int32_t mem) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  p->has_fd = false;
+  return set_problem_impl(p, v, R, g, phi, dphi, mem, true);
+}
+
+static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const void* g, const double* phi,
+                                    const double* dphi, int32_t mem, bool boot) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (!v) return fail(PINT_ERR_ARG, "v must not be NULL");
   if (R < 0 || R > 64) return fail(PINT_ERR_ARG, "R must be in 0..64");
@@ -846,6 +863,65 @@ extern "C" pint_status pint_set_problem_separable(pint_plan p, const void* v, in
   TRY(h2d(p, p->nhi, nhi));
   p->problem_set = true;
   p->wcur = 0;
+  if (boot) TRY(bootstrap(p));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return PINT_OK;
+}
+
+extern "C" pint_status pint_set_problem(pint_plan p, const void* v, const void* f, const void* f0, const void* fderiv,
+                                        int32_t mem) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (!v || !f) return fail(PINT_ERR_ARG, "v and f must not be NULL");
+  if (mem != PINT_HOST && mem != PINT_DEVICE) return fail(PINT_ERR_ARG, "mem must be PINT_HOST or PINT_DEVICE");
+  if (p->nranks > 1) return fail(PINT_ERR_UNSUPPORTED, "dense forcing on several ranks: use the separable form");
+  if (p->modal || p->dst_iter) return fail(PINT_ERR_UNSUPPORTED, "dense forcing with PINT_FLAG_MODAL / DST_PER_ITER");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int64_t M = p->M, N = p->N;
+  const int k = p->k;
+  // the starting corrections a_n f(0) and b_{l,n} tau^l f^(l)(0) are separable sources:
+  //   g_0 = f(0) with phi_0(t_n) = [n = 0]  ->  coefficient a_n;   g_l = f^(l)(0), dphi_l = e_l -> b_{l,n} tau^l
+  const int32_t R = 1 + std::max(k - 2, 0);
+  std::vector<double> phi((size_t)R * (N + 1), 0.0), dphi((size_t)R * std::max(k - 2, 0), 0.0);
+  phi[0] = 1.0;
+  for (int l = 1; l <= k - 2; ++l) dphi[(size_t)l * (k - 2) + (l - 1)] = 1.0;
+  const size_t vb = (size_t)M * sizeof(double2);
+  double2* gtmp = nullptr;
+  std::vector<double2> gh;
+  const void* gptr = nullptr;
+  if (mem == PINT_HOST) {
+    gh.assign((size_t)R * M, make_double2(0.0, 0.0));
+    if (f0) std::memcpy(gh.data(), f0, vb);
+    if (fderiv && k > 2) std::memcpy(gh.data() + M, fderiv, (size_t)(k - 2) * vb);
+    gptr = gh.data();
+  } else {
+    CUDA_TRY(cudaMalloc(&gtmp, (size_t)R * vb));
+    cudaError_t e = cudaMemsetAsync(gtmp, 0, (size_t)R * vb, p->stream);
+    if (e == cudaSuccess && f0) e = cudaMemcpyAsync(gtmp, f0, vb, cudaMemcpyDeviceToDevice, p->stream);
+    if (e == cudaSuccess && fderiv && k > 2)
+      e = cudaMemcpyAsync(gtmp + M, fderiv, (size_t)(k - 2) * vb, cudaMemcpyDeviceToDevice, p->stream);
+    if (e != cudaSuccess) { cudaFree(gtmp); return fail(PINT_ERR_CUDA, std::string("set_problem: ") + cudaGetErrorString(e)); }
+    gptr = gtmp;
+  }
+  pint_status st = set_problem_impl(p, v, R, gptr, phi.data(), k > 2 ? dphi.data() : nullptr, mem, false);
+  if (gtmp) { cudaStreamSynchronize(p->stream); cudaFree(gtmp); }
+  if (st != PINT_OK) return st;
+  // f(t_1..t_N) -> tile layout (DST-x per level in 2D), staged through B
+  if (!p->fd) TRY(dalloc(p, &p->fd, (size_t)p->ntiles * TILE));
+  CUDA_TRY(cudaMemcpyAsync(p->B, f, (size_t)N * vb, mem == PINT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                           p->stream));
+  if (p->dim == 1) {
+    RemapArgs r{};
+    r.in = p->B; r.out = p->fd; r.count = N * M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
+    r.N = N; r.n0 = 0; r.M = M; r.Qb = 1;
+    CUDA_TRY(launch_remap(r, RM_1D_LEVELS_TO_INT, p->stream));
+  } else {
+    DstArgs a = dargs(p);
+    a.in = p->B; a.out = p->fd; a.rows = N * p->my; a.n0 = 0;
+    CUDA_TRY(launch_dst(p->NE, a, DST_PHYS_LEVELS_TO_INT, p->stream));
+  }
+  ++p->launches;
+  p->has_fd = true;
+  p->fused = false;            // X is dense in time: streaming path, unpruned T-pass
   TRY(bootstrap(p));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   return PINT_OK;
@@ -1073,6 +1149,7 @@ extern "C" pint_status pint_newton_solve(pint_plan p, int32_t max_outer, double 
   CUDA_TRY(cudaSetDevice(p->device));
   NewtonArgs na{};
   na.U = p->nlU; na.R = p->nlR; na.c = p->nlC; na.src = p->src; na.coef = p->coef; na.wt = p->nlWt; na.anl = p->nlAnl;
+  na.fd = p->has_fd ? p->fd : nullptr;
   na.S = p->S; na.L = (int)p->L; na.Lpad = (int)(p->NB * p->WB); na.WB = p->WB; na.N = p->N;
   const ld hl = 1.0L / (ld)(p->L + 1);
   na.ih2 = (double)(1.0L / (hl * hl)); na.h2 = (double)(hl * hl); na.ieps2 = 1.0 / (p->nl_eps * p->nl_eps);

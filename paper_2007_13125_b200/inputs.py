@@ -238,6 +238,29 @@ def random_complex_problem(mx: int, my: int, N: int, k: int, kappa: float, alpha
                    v.astype(np.complex128), g.astype(np.complex128), phi, dphi)
 
 
+def random_dense_forcing(mx: int, my: int, N: int, k: int, kappa: float, alpha: float, seed: int = 3,
+                         T: float = 1.0):
+    """A non-separable forcing f(t_n, x) (random, complex) for pint_set_problem, and the same data as
+    a separable record for the oracle: g_r = f(t_r), phi_r(t_n) = [n = r] (r = 0..N), plus one source
+    per derivative d^l f/dt^l (0) (l = 1..k-2) with phi = 0, dphi = e_l.
+    Returns (problem, f [N][M] = f(t_1..t_N), f0 = f(0), fderiv [k-2][M])."""
+    rng = np.random.default_rng(seed)
+    M = mx * my
+    F = rng.standard_normal((N + 1, M)) + 1j * rng.standard_normal((N + 1, M))
+    nd = max(k - 2, 0)
+    D = rng.standard_normal((nd, M)) + 1j * rng.standard_normal((nd, M))
+    v = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    g = np.concatenate([F, D]).astype(np.complex128)
+    R = N + 1 + nd
+    phi = np.zeros((R, N + 1))
+    phi[np.arange(N + 1), np.arange(N + 1)] = 1.0
+    dphi = np.zeros((R, nd))
+    for l in range(nd):
+        dphi[N + 1 + l, l] = 1.0
+    prob = Problem(f"dense_{mx}x{my}_N{N}_k{k}", mx, my, T, N, k, kappa, alpha, v.astype(np.complex128), g, phi, dphi)
+    return prob, np.ascontiguousarray(F[1:]), np.ascontiguousarray(F[0]), np.ascontiguousarray(D)
+
+
 CONFIGS = {
     "C1": config_c1,
     "C2": config_c2,

@@ -31,7 +31,7 @@ EXPORTED = [
     "pint_wr_solve", "pint_get_levels", "pint_get_solution", "pint_get_modal_levels",
     "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
-    "pint_kappa_log_rule", "pint_get_path", "pint_set_nonlinearity", "pint_newton_solve",
+    "pint_kappa_log_rule", "pint_get_path", "pint_set_nonlinearity", "pint_newton_solve", "pint_set_problem",
 ]
 
 
@@ -82,6 +82,7 @@ def lib(path: str = LIB_PATH):
         "pint_kappa_log_rule": [I64],
         "pint_get_path": [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)],
         "pint_set_nonlinearity": [P, I32, D],
+        "pint_set_problem": [P, VP, VP, VP, VP, I32],
         "pint_newton_solve": [P, I32, D, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(I32)],
     }
     for name, args in sig.items():
@@ -179,6 +180,16 @@ class Plan:
         _check(lib().pint_set_problem_separable(
             self._h, vp, R, gp, None if phi_a is None else phi_a.ctypes.data,
             None if dphi_a is None else dphi_a.ctypes.data, mem))
+
+    def set_problem_dense(self, v, f, f0=None, fderiv=None):
+        """v [M]; f [N][M] = f(t_1..t_N); f0 [M] = f(0); fderiv [k-2][M] (pint_set_problem)."""
+        vp, mem = _ptr(v)
+        fp, fm = _ptr(f)
+        f0p, m0 = _ptr(f0) if f0 is not None else (None, mem)
+        fdp, md = _ptr(fderiv) if fderiv is not None else (None, mem)
+        if len({mem, fm, m0, md}) != 1:
+            raise ValueError("all arrays must live in the same memory space")
+        _check(lib().pint_set_problem(self._h, vp, fp, f0p, fdp, mem))
 
     @classmethod
     def from_problem(cls, prob, device_arrays: bool = False, **kw) -> "Plan":

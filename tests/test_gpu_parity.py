@@ -424,3 +424,49 @@ def test_fully_modal_variant(pint, name, make, kw):
         p.set_initial_guess(np.ascontiguousarray(U0))
         p.iterate()
         assert rel(p.get_solution(), wr.wr_naive(prob, 1, U0=U0, dft="fft", wrap="fft")[1]) < TOL
+
+
+@pytest.mark.parametrize("mx,my,N,k,kappa,alpha", [
+    (63, 1, 64, 2, 0.1, 1.0),
+    (100, 1, 256, 6, 0.05, 1.0),     # heat, dense in time: streaming unpruned T-pass
+    (15, 9, 32, 4, 0.2, 1.0),        # 2D: DST-x per level of f
+    (63, 1, 128, 3, 0.1, 0.5),       # CQ
+    (31, 15, 64, 2, 0.05, 0.3),      # 2D CQ
+])
+def test_dense_forcing(pint, mx, my, N, k, kappa, alpha):
+    """pint_set_problem: a non-separable f(t_n, x) with its starting corrections
+    a_n f(0) and b_{l,n} tau^l f^(l)(0); iterates match the oracle (which sees the same data as a
+    separable record with one source per level), read after every m and unread."""
+    prob, f, f0, fd = inputs.random_dense_forcing(mx, my, N, k, kappa, alpha, seed=mx + N)
+    o = wr.wr_naive(prob, 3, dft="fft", wrap="fft")
+    with pint.Plan(prob.mx, prob.my, N, k, kappa, prob.tau, alpha) as p:
+        p.set_problem_dense(prob.v, f, f0, fd if fd.size else None)
+        assert not p.path()["fused"]
+        for m in range(1, 4):
+            p.iterate()
+            assert rel(p.get_solution(), o[m]) < TOL, m
+    with pint.Plan(prob.mx, prob.my, N, k, kappa, prob.tau, alpha) as p:
+        p.set_problem_dense(prob.v, f, f0, fd if fd.size else None)
+        for _ in range(3):
+            p.iterate()
+        assert rel(p.get_solution(), o[3]) < TOL
+
+
+def test_dense_forcing_newton(pint):
+    """Newton-WR with the Example-4 forcing passed densely equals the separable run."""
+    from oracle import nonlinear as nl
+    prob = inputs.example4_allen_cahn(0.75, 2, N=128)
+    f = np.ascontiguousarray((prob.phi[:, 1:].T @ prob.g))
+    f0 = np.ascontiguousarray(prob.phi[:, 0] @ prob.g)
+    res = []
+    for dense in (False, True):
+        with pint.Plan(prob.mx, 1, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha) as p:
+            if dense:
+                p.set_problem_dense(prob.v, f, f0)
+            else:
+                p.set_problem(prob.v, prob.g, prob.phi, prob.dphi)
+            p.set_nonlinearity(1.0)
+            c, u, st = p.newton_solve(3)
+            res.append((c, p.get_solution()))
+    assert res[0][0] == res[1][0]
+    assert rel(res[1][1], res[0][1]) < 1e-12
