@@ -470,3 +470,16 @@ def test_dense_forcing_newton(pint):
             res.append((c, p.get_solution()))
     assert res[0][0] == res[1][0]
     assert rel(res[1][1], res[0][1]) < 1e-12
+
+
+def test_wr_solve_divergence_guard(pint):
+    """S:406 / SURVEY §8(b): the WR iteration diverges when kappa R / (1 - kappa R) > 1 (BDF1
+    contraction factor) — a scalar problem with a tiny T (R ~ 1) and kappa = 0.9 —
+    and pint_wr_solve reports PINT_ERR_DIVERGED after 3 consecutive increases."""
+    prob = inputs.random_complex_problem(1, 1, 64, 1, 0.9, 1.0, R=0, seed=3, T=1e-3)
+    from oracle import theory
+    assert theory.bdf1_closed_form(prob.N, prob.kappa, prob.tau, 8.0) > 1.0     # lambda = 2/h^2, h = 1/2
+    with pint.Plan.from_problem(prob) as p:
+        it, u, st = p.solve(1e-12, 100, raise_on_fail=False)
+        assert st == pint.PINT_ERR_DIVERGED, (it, u, st)
+        assert it < 100
