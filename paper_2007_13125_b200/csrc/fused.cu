@@ -84,7 +84,15 @@ cudaError_t launch_modal(bool store_w, const FusedArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st) {
+cudaError_t launch_finish(const FinishArgs& a0, int mode, cudaStream_t st) {
+  FinishArgs a = a0;
+  if (mode == FIN_PARTIALS && a.nch > 16) {  // many chunks: reduce them first, warp-parallel
+    const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
+    wr_reduce_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.nch = 1;                 // the sums sit in chunk 0; the chunk stride stays a0.nch
+  }
   const long total = a.Qb * a.Lf;
   const long blocks = std::min<long>((total + TPB - 1) / TPB, 148L * 8);
   if (blocks <= 0) return cudaSuccess;

@@ -477,6 +477,7 @@ struct FinishArgs {
   unsigned long long* upd;
   long N, Qb;
   int L, Lf, Lpad, WB, NB, k, nk, nsparse, nch;
+  int pstride;             // chunks per x-mode in the memory layout of P; nch = how many are summed
 };
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
@@ -691,6 +692,26 @@ __global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const Fu
   }
 }
 
+// Chunk reduction for small problems (many frequency-group chunks per x-mode, e.g. 1D): one warp per
+// (q, y), lanes over the chunks; the sum replaces chunk 0 (P[q][0][j][y]), deterministic order.
+__global__ void __launch_bounds__(TPB) wr_reduce_kernel(const FinishArgs a) {
+  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.Qb * (long)a.Lf) return;
+  const long q = gw / a.Lf;
+  const int y = (int)(gw % a.Lf);
+  for (int j = 0; j < a.k; ++j) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = lane; c < a.nch; c += 32) s = cadd(s, a.P[((q * a.pstride + c) * a.k + j) * a.Lf + y]);
+    for (int o = 16; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    __syncwarp();
+    if (lane == 0) const_cast<double2*>(a.P)[((q * a.pstride) * a.k + j) * a.Lf + y] = s;
+  }
+}
+
 __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int mode) {
   double updl = 0.0;
   bool nonfinite = false;
@@ -708,7 +729,7 @@ __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int 
       if (j < k && live) {
         if (mode == FIN_PARTIALS) {
           double2 s = make_double2(0.0, 0.0);
-          for (int c = 0; c < a.nch; ++c) s = cadd(s, a.P[((q * a.nch + c) * k + j) * a.Lf + y]);
+          for (int c = 0; c < a.nch; ++c) s = cadd(s, a.P[((q * a.pstride + c) * k + j) * a.Lf + y]);
           U[j] = cscale(s, __ldg(&a.igs[a.N - k + j]));
           const double2 o = a.wrap_old[wb + j * a.WB];
           const double dd = sqrt(cabs2(csub(U[j], o)));

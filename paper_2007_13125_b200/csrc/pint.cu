@@ -658,7 +658,7 @@ static pint_status finish_pass(pint_plan p, int mode, const double2* wold, doubl
   a.src = p->src; a.coef = p->coef; a.spar = p->srclist; a.nsparse = p->nsparse;
   a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->upd;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
-  a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch;
+  a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.pstride = p->nch;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing && mode == FIN_PARTIALS) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
