@@ -77,15 +77,48 @@ def _c4_narrow(mx: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region: NVML polled every 5 ms from a
+    thread (one sample is also taken on entry and exit, so sub-millisecond regions are covered);
+    nvidia-smi -lms 200 when NVML is unavailable."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,power.draw")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.rows, self.proc, self.nv, self.stop = device, [], None, None, threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        pr = torch.cuda.get_device_properties(self.device)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+
+    def _nvml_sample(self):
+        nv, h = self.nv
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        self.rows.append([str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                          str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), hex(r)]
+                         + ["Active" if r & b else "Not Active" for b in bits]
+                         + [f"{nv.nvmlDeviceGetPowerUsage(h) / 1000.0:.2f}"])
+
+    def _nvml_loop(self):
+        while not self.stop.wait(0.005):
+            self._nvml_sample()
 
     def __enter__(self):
+        try:
+            self.nv = self._nvml_handle()
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:   # noqa: BLE001 - no NVML: fall back to nvidia-smi
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -101,6 +134,10 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nv:
+            self._nvml_sample()
+            self.stop.set()
+            self.t.join(1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -111,13 +148,14 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        pw = [float(r[7]) for r in self.rows if len(r) > 7 and r[7].replace(".", "").isdigit()]
+        rows = list(self.rows)
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        pw = [float(r[7]) for r in rows if len(r) > 7 and r[7].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None,
+                "source": "nvml" if self.nv else "nvidia-smi"}
 
 
 def cpu_baseline(prob_name: str, budget_s: float = 30.0):
@@ -228,7 +266,6 @@ def main():
     for _ in range(args.warmup):
         plan.iterate()
     launches0 = plan.info()["kernel_launches"]
-    plan.set_timing(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -243,9 +280,15 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    launches = plan.info()["kernel_launches"] - launches0
+    # per-kernel durations for the roofline: a second run of the same iterations with CUDA events
+    # around every launch on the plan stream (eager launches: the timed run above replays the fused
+    # iteration as a CUDA graph)
+    plan.set_timing(True)
+    for _ in range(args.steps):
+        plan.iterate()
     tm = plan.get_timing()
     plan.set_timing(False)
-    launches = plan.info()["kernel_launches"] - launches0
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -307,7 +350,17 @@ def main():
     # time is the max over ranks.
     e2e = None
     if not args.no_e2e:
-        vh = np.ascontiguousarray(prob.v)
+        def pinned(a):   # page-locked host copy (the contract's pinned host buffers)
+            t = torch.empty(a.shape, dtype=torch.complex128, pin_memory=True)
+            t.numpy()[...] = a
+            return t.numpy()
+        vh = pinned(prob.v)
+        gh = pinned(np.ascontiguousarray(prob.g)) if prob.R else None
+        if world > 1:
+            qb, qe = plan.partition()
+            out = torch.empty((1, prob.my, qe - qb), dtype=torch.complex128, pin_memory=True).numpy()
+        else:
+            out = torch.empty((1, prob.M), dtype=torch.complex128, pin_memory=True).numpy()
         steps, t_tot, its = args.e2e_steps, 0.0, 0
         out_bytes = 0
         for i in range(steps + 1):
@@ -315,13 +368,11 @@ def main():
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            plan.set_problem(vh, np.ascontiguousarray(prob.g) if prob.R else None,
-                             prob.phi if prob.R else None, prob.dphi if prob.R else None)
+            plan.set_problem(vh, gh, prob.phi if prob.R else None, prob.dphi if prob.R else None)
             it, u, st = plan.solve(prob.tol, 20, raise_on_fail=False)
             if world > 1:
-                out = plan.get_modal_levels(prob.N - 1, 1)
+                plan.get_modal_levels(prob.N - 1, 1, out)
             else:
-                out = np.empty((1, prob.M), np.complex128)
                 plan.get_levels(prob.N - 1, 1, out)
             dt = time.perf_counter() - t0
             if world > 1:
@@ -335,7 +386,7 @@ def main():
         e2e = {"value": total_unknowns * its / t_tot, "unit": UNIT,
                "h2d_bytes_per_step": int(vh.nbytes + (prob.g.nbytes if prob.R else 0)),
                "d2h_bytes_per_step": int(out_bytes + 8 * its // steps),
-               "what": f"set_problem(host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
+               "what": f"set_problem(pinned host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
                        + ("final time level to host" if world == 1 else "each rank's modal slab of the final level to host")
                        + ", per step (max over ranks); unknowns/s per WR iteration"}
 

@@ -60,7 +60,9 @@ struct FusedArgs {
   const double* sig_q;     // modal path: [Qb] h^2 lambda_q
   int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
                            // 8 u-form recurrences on every line
+  int reserved;            // zero: keeps the struct free of padding (the graph replay memcmp's it)
 };
+static_assert(sizeof(FusedArgs) == 168, "FusedArgs must stay padding-free");
 
 // smem row swizzle: lane l of the solve owns rows [lC, lC + C); XOR-ing the low bits with the
 // chunk index keeps its 16-byte accesses bank-conflict free, and consecutive rows (row phases)
@@ -479,6 +481,7 @@ struct FinishArgs {
   int L, Lf, Lpad, WB, NB, k, nk, nsparse, nch;
   int pstride;             // chunks per x-mode in the memory layout of P; nch = how many are summed
 };
+static_assert(sizeof(FinishArgs) == 144, "FinishArgs must stay padding-free");
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
 

@@ -161,6 +161,8 @@ struct pint_plan_s {
   double2* phys = nullptr;   // [2][M] physical staging (v, A v)
   double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
+  unsigned long long* updh = nullptr;   // pinned host copy of upd
+  bool upd_queued = false;              // the D2H copy of upd is already on the stream
   // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
   bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
   bool half = false;          // PINT_FLAG_REAL_DATA: half-spectrum fused iteration
@@ -202,6 +204,13 @@ struct pint_plan_s {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev, sev;
   double t_ms = 0, s_ms = 0;
   int64_t t_n = 0, s_n = 0;
+  // fused iteration replayed as a CUDA graph (memset, fused kernel, [reduce], finish), one per
+  // (wcur, xcur) parity; re-captured whenever the kernel arguments differ from the captured ones
+  bool graphs = true;
+  cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
+  FusedArgs gfa[4];
+  FinishArgs gfin[4];
+  int64_t glaunch = 0;        // kernels per graph replay
 };
 
 
@@ -285,6 +294,8 @@ static void free_plan(pint_plan p) {
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   for (auto& e : p->tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : p->sev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (cudaGraphExec_t g : p->gexec) if (g) cudaGraphExecDestroy(g);
+  if (p->updh) cudaFreeHost(p->updh);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -368,6 +379,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(ce)); }
     p->own_stream = true;
   }
+  // graph replay of the fused iteration (PINT_NO_GRAPH=1: eager launches; the legacy stream cannot capture)
+  p->graphs = getenv("PINT_NO_GRAPH") == nullptr && p->stream != cudaStreamLegacy;
 
   const size_t arr = (size_t)p->ntiles * TILE;
   pint_status st;
@@ -397,6 +410,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = dalloc(p, &p->sig_p, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->sig_q, p->Qb)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->upd, 1)) != PINT_OK) return bail(st);
+  ce = cudaHostAlloc((void**)&p->updh, sizeof(unsigned long long), cudaHostAllocDefault);
+  if (ce != cudaSuccess) { p->updh = nullptr; return bail(fail(PINT_ERR_ALLOC, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce))); }
   if ((st = dalloc(p, &p->phys, 2 * (size_t)M)) != PINT_OK) return bail(st);
   if (dim == 2 && (st = dalloc(p, &p->twE, NE)) != PINT_OK) return bail(st);
   // fused heat iteration: v2 = two warps per line (64 lanes x Cf rows), v1 = one warp (32 x Cf);
@@ -652,13 +667,18 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
 
 // window of U (mode: FIN_PARTIALS from the fused partial sums, FIN_FROM_WRAP / FIN_FROM_V /
 // FIN_ZERO at bootstrap) -> wrap_new, update monitor, and X for the next iteration
-static pint_status finish_pass(pint_plan p, int mode, const double2* wold, double2* wnew, double2* X) {
+static FinishArgs finargs(pint_plan p, const double2* wold, double2* wnew, double2* X) {
   FinishArgs a{};
   a.P = p->Pp; a.wrap_old = wold; a.wrap_new = wnew; a.X = X;
   a.src = p->src; a.coef = p->coef; a.spar = p->srclist; a.nsparse = p->nsparse;
   a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->upd;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.pstride = p->nch;
+  return a;
+}
+
+static pint_status finish_pass(pint_plan p, int mode, const double2* wold, double2* wnew, double2* X) {
+  const FinishArgs a = finargs(p, wold, wnew, X);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing && mode == FIN_PARTIALS) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
@@ -981,11 +1001,49 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // ------------------------------------------------------------------------------------------
 // iteration
 // ------------------------------------------------------------------------------------------
+// one fused iteration: update monitor reset, Steps 1-3 (fused kernel), window / X / monitor (finish)
+static pint_status fused_step(pint_plan p) {
+  CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+  TRY(fused_pass(p, p->X[p->xcur], false));                                       // Steps 1-3
+  TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
+  CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
+  return PINT_OK;
+}
+
+// Replay fused_step as a CUDA graph: one host launch per iteration instead of three (small
+// problems are launch-bound).  The graph for parity key is (re)captured when the arguments the
+// kernels would get now differ from the captured ones (set_problem may move sources, nk, ...).
+static pint_status fused_step_graph(pint_plan p) {
+  const int key = p->wcur * 2 + p->xcur;
+  const FusedArgs fa = fargs(p, p->X[p->xcur]);
+  const FinishArgs fin = finargs(p, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]);
+  if (!p->gexec[key] || memcmp(&fa, &p->gfa[key], sizeof fa) != 0 || memcmp(&fin, &p->gfin[key], sizeof fin) != 0) {
+    if (p->gexec[key]) { CUDA_TRY(cudaGraphExecDestroy(p->gexec[key])); p->gexec[key] = nullptr; }
+    const int64_t l0 = p->launches;
+    CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeRelaxed));
+    const pint_status st = fused_step(p);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(p->stream, &g);
+    if (st != PINT_OK) { if (g) cudaGraphDestroy(g); return st; }
+    CUDA_TRY(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&p->gexec[key], g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(ei);
+    p->glaunch = p->launches - l0;
+    p->launches = l0;
+    p->gfa[key] = fa;
+    p->gfin[key] = fin;
+  }
+  CUDA_TRY(cudaGraphLaunch(p->gexec[key], p->stream));
+  p->launches += p->glaunch;
+  return PINT_OK;
+}
+
 static pint_status iterate_async(pint_plan p) {
   if (p->fused) {
-    CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
-    TRY(fused_pass(p, p->X[p->xcur], false));                                     // Steps 1-3
-    TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
+    if (p->graphs && !p->timing) TRY(fused_step_graph(p));   // per-kernel timing needs eager launches
+    else TRY(fused_step(p));
+    p->upd_queued = true;
     p->wcur ^= 1;
     p->xcur ^= 1;
     p->stateA = 0;   // A no longer holds U_m
@@ -1017,11 +1075,11 @@ static pint_status iterate_async(pint_plan p) {
 }
 
 static pint_status read_update(pint_plan p, double* out) {
-  unsigned long long bits = 0;
-  CUDA_TRY(cudaMemcpyAsync(&bits, p->upd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+  if (!p->upd_queued) CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
+  p->upd_queued = false;
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   double u;
-  std::memcpy(&u, &bits, sizeof(u));
+  std::memcpy(&u, p->updh, sizeof(u));
   if (p->nranks > 1) {
     if (p->allreduce(&u, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
   }

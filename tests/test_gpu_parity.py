@@ -483,3 +483,43 @@ def test_wr_solve_divergence_guard(pint):
         it, u, st = p.solve(1e-12, 100, raise_on_fail=False)
         assert st == pint.PINT_ERR_DIVERGED, (it, u, st)
         assert it < 100
+
+
+@pytest.mark.parametrize("mx,my,N,k", [(63, 1, 64, 2), (63, 30, 256, 3), (1023, 1, 1024, 4)])
+def test_graph_replay_matches_eager(pint, monkeypatch, mx, my, N, k):
+    """The fused iteration replayed as a CUDA graph (default) gives bit-identical iterates and
+    update norms to eager launches (PINT_NO_GRAPH=1), also across pint_set_problem calls that
+    change the kernel arguments (a forcing with a different nk forces a re-capture) and across
+    timing-mode (eager) iterations in between; the reported launch counts agree."""
+    prob1 = inputs.random_complex_problem(mx, my, N, k, 0.05, 1.0, R=1, seed=mx + k)
+    prob2 = inputs.random_complex_problem(mx, my, N, k, 0.02, 1.0, R=1, seed=mx + k + 1)
+    phi = prob2.phi.copy()
+    phi[:, 6:] = 0.0                         # forcing on the first 5 levels: nk = 5
+    prob2 = prob2.with_(phi=phi)
+    monkeypatch.setenv("PINT_NO_GRAPH", "1")
+    eager = pint.Plan.from_problem(prob1)
+    monkeypatch.delenv("PINT_NO_GRAPH")
+    graph = pint.Plan.from_problem(prob1)
+    try:
+        for p in (eager, graph):
+            assert p.path()["fused"]
+        l0 = [p.info()["kernel_launches"] for p in (eager, graph)]
+        for it in range(4):
+            if it == 2:
+                graph.set_timing(True)
+            ue, ug = eager.iterate(), graph.iterate()
+            graph.set_timing(False)
+            assert ue == ug, (it, ue, ug)
+        assert [p.info()["kernel_launches"] - l for p, l in zip((eager, graph), l0)] == [8, 8]
+        assert np.array_equal(eager.get_solution(), graph.get_solution())
+        for p in (eager, graph):
+            p.set_problem(prob2.v, np.ascontiguousarray(prob2.g), prob2.phi, prob2.dphi)
+            assert p.path()["nk"] == 5
+        ups = [(eager.iterate(), graph.iterate()) for _ in range(3)]
+        assert all(a == b for a, b in ups), ups
+        sol = graph.get_solution()
+        assert np.array_equal(eager.get_solution(), sol)
+        assert rel(sol, wr.wr_naive(prob2, 3, dft="fft")[3]) <= TOL
+    finally:
+        eager.close()
+        graph.close()
