@@ -9,9 +9,22 @@ size_t fused_smem_bytes(int lanes, int C, int k, bool tm) {
          (lanes == 64 ? 8 * 4 * sizeof(double2) : 0);
 }
 
+using FusedKern = void (*)(const FusedArgs);
+
+// hot instantiation: real-data variant and the compile-time nk bound (one warp per line only)
+template <int C, int LANES, bool HALF>
+static FusedKern fused_pick(int nk) {
+  if constexpr (LANES == 32) {
+    if (nk <= 4) return wr_fused_kernel<C, LANES, false, true, HALF, 4>;
+    if (nk <= 6) return wr_fused_kernel<C, LANES, false, true, HALF, 6>;
+  }
+  return wr_fused_kernel<C, LANES, false, true, HALF, 8>;
+}
+
 template <int C, int LANES, bool SW, bool TM>
 static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
-  auto kern = (TM && !SW && a.half) ? wr_fused_kernel<C, LANES, SW, TM, TM && !SW> : wr_fused_kernel<C, LANES, SW, TM>;
+  FusedKern kern = wr_fused_kernel<C, LANES, SW, TM>;
+  if constexpr (TM && !SW) kern = a.half ? fused_pick<C, LANES, true>(a.nk) : fused_pick<C, LANES, false>(a.nk);
   const size_t smem = fused_smem_bytes(LANES, C, a.k, TM && !SW) + (a.xs ? (size_t)a.nk * LANES * C * sizeof(double2) : 0);
   // set on every launch: the occupancy query at plan creation (fused_occ) also sets this attribute
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

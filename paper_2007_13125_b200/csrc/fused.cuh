@@ -35,7 +35,8 @@ struct LineConst {
   double2 rrh;      // r^{CS}
   double2 uc[8];    // u-forms of a^{C 2^i}
   double2 ap[5];    // a^{2^i} (value form), i < 5: per-lane powers of the boundary fix-up
-  double la, thr;   // log|a|;  log(1e-18 |1 - a^{2L+2}|)
+  double tl;        // log(1e-18 |1 - a^{2L+2}|) / log|a|: |a^e / (1 - a^{2L+2})| > 1e-18 iff e < tl
+  double pad0;
 };                  // 320 bytes
 constexpr int LC_CHUNKS = 20;   // 16-byte cp.async chunks per LineConst
 static_assert(sizeof(LineConst) == 16 * LC_CHUNKS, "LineConst is staged in 16-byte chunks");
@@ -183,8 +184,12 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
       st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
       d[s2 * CS + r] = st[s2];
     }
-  if (nv < C) {                                             // the lane holding row L-1: the backward
-#pragma unroll                                              // sweep starts from zero at row L
+  // the lane holding row L-1: the backward sweep starts from zero at row L.  L = LF - 1 (the
+  // 2^n - 1 grids) has one pad row: a warp-uniform branch avoids C predicated selects per lane.
+  if (L >= LANES * C - 1) {
+    if (nv < C) d[C - 1] = make_double2(0.0, 0.0);
+  } else if (nv < C) {
+#pragma unroll
     for (int r = 0; r < C; ++r)
       if (r >= nv) d[r] = make_double2(0.0, 0.0);
   }
@@ -240,14 +245,14 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     w0.y = __shfl_sync(0xffffffffu, d[0].y, 0);
   }
   const double2 K = cmul(w0, lc.ru2L);
-  // rows y < rP carry a P term K a^{y+2} above the 1e-18 threshold: (y + 2) la > thr.  When they are
+  // rows y < rP carry a P term K a^{y+2} above the 1e-18 threshold: y + 2 < tl.  When they are
   // few (rP <= 256: the large-shift lines) the warp fixes them up after the store, one row per lane,
   // instead of every lane running the C-row correction loop for lane 0's sake.
-  const double rPd = lc.thr / lc.la - 2.0;                                 // la < 0, thr < 0
+  const double rPd = lc.tl - 2.0;
   const bool fastP = !STORE_W && !PAIR && rPd <= 256.0;
   if (nv > 0) {
-    const double la = lc.la, thr = lc.thr;
-    if (!fastP && (y0 + 2) * la > thr) {                                   // |a^{y+2}| is largest at y0
+    const double tl = lc.tl;
+    if (!fastP && y0 + 2 < tl) {                                           // |a^{y+2}| is largest at y0
       double2 ul = uprod(lc.u, lc.u);                                      // a^2
 #pragma unroll
       for (int i = 0; i < (PAIR ? 6 : 5); ++i)
@@ -262,7 +267,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 #pragma unroll
         for (int s2 = 0; s2 < NS; ++s2) { d[s2 * CS + r] = csub(d[s2 * CS + r], KP[s2]); KP[s2] = cmul(KP[s2], a1); }
     }
-    if ((2.0 * L + 2 - (y0 + nv - 1)) * la > thr) {                        // |a^{2L+2-y}| largest at the chunk end
+    if (2.0 * L + 2 - (y0 + nv - 1) < tl) {                                // |a^{2L+2-y}| largest at the chunk end
       const int m = (2 * L + 2) / C - gl;                                  // 2L+2-y0 = e + C m, e = (2L+2) mod C
       double2 uq = lc.uE;
 #pragma unroll
@@ -356,7 +361,7 @@ __device__ __forceinline__ double2 wcontrib(double2 Y, double2 w, int half, doub
 // Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
 // next synthesis and the group's twiddles are issued first (one memory round trip), then each row
 // reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
-template <int C, int LANES, bool WINDOW, bool TM = false, bool HALF = false>
+template <int C, int LANES, bool WINDOW, bool TM = false, bool HALF = false, int NKC = 8>
 __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, double2* acc, const double2* Xq,
                                            long q, int i, bool next, uint32_t tacc = 0) {
   constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
@@ -371,7 +376,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int j = t - 8 + k;                                                               // level n = N - 8 + t
-      double2 w = (j >= 0) ? __ldg(&a.tw[((N - 8 + t) * i) & (N - 1)]) : make_double2(0.0, 0.0);
+      double2 w = (t >= 8 - NKC && j >= 0) ? __ldg(&a.tw[((N - 8 + t) * i) & (N - 1)]) : make_double2(0.0, 0.0);
       w.y = -w.y;                                                                            // e^{+2 pi i n i/N}
       tww[t] = w;
     }
@@ -391,7 +396,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
         dft8<+1>(x);                                     // Y_r = sum_s e^{+2 pi i rs/8} W_{i + (N/8) s}
 #pragma unroll
         for (int r = 2; r < 8; ++r)
-          if (r - 8 + k >= 0)
+          if (r >= 8 - NKC && r - 8 + k >= 0)
             tw_put(w[rr], r - 2, HALF ? cadd(tw_get(w[rr], r - 2), wcontrib(x[r], tww[r], 1, hw))
                                         : cfma(x[r], tww[r], tw_get(w[rr], r - 2)));
         tmem_st24(tacc + 24 * rr, w[rr]);
@@ -408,7 +413,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int j = r - 8 + k;
-          if (j >= 0)
+          if (r >= 8 - NKC && j >= 0)
             acc[j * LF + y] = HALF ? cadd(acc[j * LF + y], wcontrib(x[r], tww[r], 1, hw))
                                      : cfma(x[r], tww[r], acc[j * LF + y]);
         }
@@ -423,18 +428,18 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
       const int y = threadIdx.x + T * rr;
 #pragma unroll
       for (int t = 0; t < 8; ++t)
-        xv[rr][t] = (t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
+        xv[rr][t] = (t < NKC && t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
     }
     double2 tws[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) tws[t] = (t > 0 && t < nk) ? __ldg(&a.tw[t * i1]) : make_double2(1.0, 0.0);   // w_N^{t (i+1)}
+    for (int t = 0; t < 8; ++t) tws[t] = (t > 0 && t < NKC && t < nk) ? __ldg(&a.tw[t * i1]) : make_double2(1.0, 0.0);   // w_N^{t (i+1)}
 #pragma unroll
     for (int rr = 0; rr < RPT; ++rr) {
       const int y = threadIdx.x + T * rr;
       if (LF < T && y >= LF) break;
       double2* z = xv[rr];
 #pragma unroll
-      for (int t = 1; t < 8; ++t) z[t] = cmul(z[t], tws[t]);                     // X_t w_N^{t (i+1)}
+      for (int t = 1; t < NKC; ++t) z[t] = cmul(z[t], tws[t]);                   // X_t w_N^{t (i+1)}
       dft8<-1>(z);                                       // H_{i+1 + (N/8) s} = sum_t (.) e^{-2 pi i ts/8}
       for (int dd = 0; dd < a.ndense; ++dd) {
         const double2 g = y < a.L ? __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * a.Qb + q) * a.Lpad + y])
@@ -494,7 +499,9 @@ template <int C, int LANES> struct FTmem {
 
 // TM: window partial sums in tensor memory (default) instead of shared memory.
 // HALF: real-data half spectrum (PINT_FLAG_REAL_DATA; instantiated with TM only).
-template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false>
+// NKC: compile-time bound on nk (and k): X_t = 0 for t >= NKC and window slots r < 8 - NKC are
+// unused, so the synthesis twiddles and the DFT8 butterflies on those zeros/outputs are pruned.
+template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false, int NKC = 8>
 __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const FusedArgs a) {
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
   if (!STORE_W && !TMA)
     for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
       for (int j = 0; j < a.k; ++j) acc[j * LF + y] = make_double2(0.0, 0.0);
-  fused_rows<C, LANES, false>(a, Hs, acc, Xq, q, g0 - 1, true);   // synthesise group g0
+  fused_rows<C, LANES, false, false, false, NKC>(a, Hs, acc, Xq, q, g0 - 1, true);   // synthesise group g0
   cp_async_wait0();
   __syncthreads();
 #ifdef PINT_FUSED_PROF
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     PINT_TS(t2);
     const bool next = i + 1 < g1;
     if (next) fused_stage_lc(a, slc, q, i + 1);
-    fused_rows<C, LANES, !STORE_W, TMA, HALF>(a, Hs, acc, Xq, q, i, next, tacc);
+    fused_rows<C, LANES, !STORE_W, TMA, HALF, NKC>(a, Hs, acc, Xq, q, i, next, tacc);
     if constexpr (TMA) tmem_wait_st();
     cp_async_wait0();
     PINT_TS(t3);
@@ -796,8 +803,10 @@ __global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const dou
     c.uE = upow(c.u, (2L * L + 2) % C);
     c.ap[0] = one_minus(c.u);
     for (int i = 1; i < 5; ++i) c.ap[i] = cmul(c.ap[i - 1], c.ap[i - 1]);
-    c.la = 0.5 * log(cabs2(one_minus(c.u)));
-    c.thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));
+    const double la = 0.5 * log(cabs2(one_minus(c.u)));                // log|a| < 0
+    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));      // log(1e-18 |1 - a^{2L+2}|)
+    c.tl = la < 0.0 ? thr / la : INFINITY;
+    c.pad0 = 0.0;
     lc[e] = c;
   }
 }
