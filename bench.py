@@ -281,13 +281,14 @@ def main():
         dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = plan.info()["kernel_launches"] - launches0
-    # per-kernel durations for the roofline: a second run of the same iterations with CUDA events
-    # around every launch on the plan stream (eager launches: the timed run above replays the fused
-    # iteration as a CUDA graph)
+    # per-kernel durations for the roofline: the same K iterations again with CUDA events around
+    # every kernel on the plan stream (event nodes inside the replayed graph; kept out of the timed
+    # region above, where they would cost small problems several microseconds per iteration)
     plan.set_timing(True)
-    for _ in range(args.steps):
-        plan.iterate()
-    tm = plan.get_timing()
+    with ClockSampler(local) as clk_k:
+        for _ in range(args.steps):
+            plan.iterate()
+        tm = plan.get_timing()
     plan.set_timing(False)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -329,7 +330,8 @@ def main():
                     "peak_source": f"derived: 2 x {FP64_FMA_PER_CLK_SM} FP64 FMA/clk/SM x SMs x {smx:.0f} MHz (DESIGN.md §5)",
                     "algorithmic_flops_per_unknown": fl, "algorithmic_flops_per_launch": flops_launch,
                     "passes": {"fused_ms": s_avg, "finish_ms": t_avg, "chunks_per_xmode": path["chunks"],
-                               "fused_share_of_step": s_avg / ms_step}}
+                               "fused_share_of_step": s_avg / ms_step,
+                               "timing_pass_clocks": clk_k.summary()}}
     else:
         bytes_launch = BYTES_PER_UNKNOWN_PASS * local_unknowns
         dom = ("tpass", t_avg) if t_avg >= s_avg else ("spass", s_avg)
@@ -343,7 +345,8 @@ def main():
                                "tpass_GBs": bytes_launch / (t_avg / 1e3) / 1e9,
                                "spass_GBs": bytes_launch / (s_avg / 1e3) / 1e9,
                                "iteration_GBs": 2 * bytes_launch / (ms_step / 1e3) / 1e9,
-                               "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm}}
+                               "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm,
+                               "timing_pass_clocks": clk_k.summary()}}
 
     # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host.
     # N > 1: every rank reads its own x-mode slab of the final level (pint_get_modal_levels); the

@@ -19,9 +19,9 @@ static long persistent_grid(const void* kern, int smem) {
   return (long)nsm * (per > 0 ? per : 1);
 }
 
-template <int MI, int MO, bool CQ>
+template <int MI, int MO, bool CQ, bool FD = false>
 static cudaError_t go(const TPassArgs& a, long ntiles, cudaStream_t st) {
-  auto kern = tpass_kernel<PINT_N, MI, MO, CQ>;
+  auto kern = tpass_kernel<PINT_N, MI, MO, CQ, FD>;
   const int smem = phys_size(TILE) * (int)sizeof(double2);
   // persistent grid: SMs x resident CTAs per SM (thread-safe one-time init; one device per process)
   static const long resident = persistent_grid((const void*)kern, smem);
@@ -56,8 +56,20 @@ cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntil
 #endif
 }
 
+// dense right-hand side (a.fdense: pint_set_problem with the streaming path, Newton inner solves)
+template <bool CQ>
+static cudaError_t go_fd(int mi, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  switch (mi) {
+    case IN_FREQ: return go<IN_FREQ, OUT_H, CQ, true>(a, ntiles, st);
+    case IN_TIME_V: return go<IN_TIME_V, OUT_H, CQ, true>(a, ntiles, st);
+    case IN_TIME_ZERO: return go<IN_TIME_ZERO, OUT_H, CQ, true>(a, ntiles, st);
+    default: return go<IN_TIME_BUF, OUT_H, CQ, true>(a, ntiles, st);
+  }
+}
+
 cudaError_t PINT_CAT(launch_tpass_, PINT_N)(int mi, int mo, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st) {
   if (mo == OUT_U) return go<IN_FREQ, OUT_U, false>(a, ntiles, st);
+  if (a.fdense) return cq ? go_fd<true>(mi, a, ntiles, st) : go_fd<false>(mi, a, ntiles, st);
   if (!cq) {
     switch (mi) {
       case IN_FREQ: return go<IN_FREQ, OUT_H, false>(a, ntiles, st);

@@ -207,9 +207,13 @@ struct pint_plan_s {
   // fused iteration replayed as a CUDA graph (memset, fused kernel, [reduce], finish), one per
   // (wcur, xcur) parity; re-captured whenever the kernel arguments differ from the captured ones
   bool graphs = true;
-  cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
-  FusedArgs gfa[4];
-  FinishArgs gfin[4];
+  // slots 4..7: the same with CUDA-event nodes around the fused and finish kernels (timing mode)
+  cudaGraphExec_t gexec[8] = {};
+  FusedArgs gfa[8];
+  FinishArgs gfin[8];
+  cudaEvent_t gev[8][4] = {};
+  cudaEvent_t* cap_ev = nullptr;   // during a timing capture: the slot's events
+  int gpending = -1;          // slot whose event nodes ran last and are not yet accumulated
   int64_t glaunch = 0;        // kernels per graph replay
 };
 
@@ -295,6 +299,7 @@ static void free_plan(pint_plan p) {
   for (auto& e : p->tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : p->sev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (cudaGraphExec_t g : p->gexec) if (g) cudaGraphExecDestroy(g);
+  for (auto& ev : p->gev) for (cudaEvent_t e : ev) if (e) cudaEventDestroy(e);
   if (p->updh) cudaFreeHost(p->updh);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -654,14 +659,20 @@ static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
     a.gpc = (int)(p->N / 8);
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (p->timing && !store_w) {
+  if (p->cap_ev && !store_w) {                 // graph capture: the slot's own event nodes
+    e0 = p->cap_ev[0]; e1 = p->cap_ev[1];
+    CUDA_TRY(cudaEventRecordWithFlags(e0, p->stream, cudaEventRecordExternal));
+  } else if (p->timing && !store_w) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
   if (p->modal) CUDA_TRY(launch_modal(store_w, a, p->stream));
   else CUDA_TRY(launch_fused(p->flanes, p->Cf, store_w, p->ftm, a, p->stream));
   ++p->launches;
-  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->sev.push_back({e0, e1}); }
+  if (e0) {
+    CUDA_TRY(cudaEventRecordWithFlags(e1, p->stream, p->cap_ev ? cudaEventRecordExternal : cudaEventRecordDefault));
+    if (!p->cap_ev) p->sev.push_back({e0, e1});
+  }
   return PINT_OK;
 }
 
@@ -680,13 +691,19 @@ static FinishArgs finargs(pint_plan p, const double2* wold, double2* wnew, doubl
 static pint_status finish_pass(pint_plan p, int mode, const double2* wold, double2* wnew, double2* X) {
   const FinishArgs a = finargs(p, wold, wnew, X);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (p->timing && mode == FIN_PARTIALS) {
+  if (p->cap_ev && mode == FIN_PARTIALS) {
+    e0 = p->cap_ev[2]; e1 = p->cap_ev[3];
+    CUDA_TRY(cudaEventRecordWithFlags(e0, p->stream, cudaEventRecordExternal));
+  } else if (p->timing && mode == FIN_PARTIALS) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
   CUDA_TRY(launch_finish(a, mode, p->stream));
   ++p->launches;
-  if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->tev.push_back({e0, e1}); }
+  if (e0) {
+    CUDA_TRY(cudaEventRecordWithFlags(e1, p->stream, p->cap_ev ? cudaEventRecordExternal : cudaEventRecordDefault));
+    if (!p->cap_ev) p->tev.push_back({e0, e1});
+  }
   return PINT_OK;
 }
 
@@ -1014,14 +1031,18 @@ static pint_status fused_step(pint_plan p) {
 // problems are launch-bound).  The graph for parity key is (re)captured when the arguments the
 // kernels would get now differ from the captured ones (set_problem may move sources, nk, ...).
 static pint_status fused_step_graph(pint_plan p) {
-  const int key = p->wcur * 2 + p->xcur;
+  const int key = p->wcur * 2 + p->xcur + (p->timing ? 4 : 0);
   const FusedArgs fa = fargs(p, p->X[p->xcur]);
   const FinishArgs fin = finargs(p, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]);
   if (!p->gexec[key] || memcmp(&fa, &p->gfa[key], sizeof fa) != 0 || memcmp(&fin, &p->gfin[key], sizeof fin) != 0) {
     if (p->gexec[key]) { CUDA_TRY(cudaGraphExecDestroy(p->gexec[key])); p->gexec[key] = nullptr; }
     const int64_t l0 = p->launches;
+    if (p->timing && !p->gev[key][0])
+      for (cudaEvent_t& e : p->gev[key]) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeRelaxed));
+    p->cap_ev = p->timing ? p->gev[key] : nullptr;
     const pint_status st = fused_step(p);
+    p->cap_ev = nullptr;
     cudaGraph_t g = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(p->stream, &g);
     if (st != PINT_OK) { if (g) cudaGraphDestroy(g); return st; }
@@ -1036,12 +1057,27 @@ static pint_status fused_step_graph(pint_plan p) {
   }
   CUDA_TRY(cudaGraphLaunch(p->gexec[key], p->stream));
   p->launches += p->glaunch;
+  if (p->timing) p->gpending = key;
+  return PINT_OK;
+}
+
+// timing mode with graph replay: add the last replay's fused / finish durations (the event nodes
+// are re-recorded by every replay, so they are read after each iteration's synchronisation)
+static pint_status graph_timing_collect(pint_plan p) {
+  if (p->gpending < 0) return PINT_OK;
+  cudaEvent_t* e = p->gev[p->gpending];
+  p->gpending = -1;
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e[0], e[1]));
+  p->s_ms += ms; ++p->s_n;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e[2], e[3]));
+  p->t_ms += ms; ++p->t_n;
   return PINT_OK;
 }
 
 static pint_status iterate_async(pint_plan p) {
   if (p->fused) {
-    if (p->graphs && !p->timing) TRY(fused_step_graph(p));   // per-kernel timing needs eager launches
+    if (p->graphs) TRY(fused_step_graph(p));
     else TRY(fused_step(p));
     p->upd_queued = true;
     p->wcur ^= 1;
@@ -1078,6 +1114,7 @@ static pint_status read_update(pint_plan p, double* out) {
   if (!p->upd_queued) CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
   p->upd_queued = false;
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  TRY(graph_timing_collect(p));
   double u;
   std::memcpy(&u, p->updh, sizeof(u));
   if (p->nranks > 1) {
@@ -1443,6 +1480,7 @@ extern "C" pint_status pint_set_timing(pint_plan p, int32_t enable) {
   for (auto& e : p->sev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   p->tev.clear(); p->sev.clear();
   p->t_ms = p->s_ms = 0; p->t_n = p->s_n = 0;
+  p->gpending = -1;
   p->timing = enable != 0;
   return PINT_OK;
 }
@@ -1451,6 +1489,7 @@ extern "C" pint_status pint_get_timing(pint_plan p, double* tpass_ms, double* sp
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   CUDA_TRY(cudaSetDevice(p->device));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  TRY(graph_timing_collect(p));
   for (auto& e : p->tev) {
     float ms = 0; CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
     p->t_ms += ms; ++p->t_n; cudaEventDestroy(e.first); cudaEventDestroy(e.second);

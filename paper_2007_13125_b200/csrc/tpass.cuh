@@ -102,16 +102,19 @@ __device__ __forceinline__ void block_max_atomic(double x, unsigned long long* d
 
 // F_static(n, c) = sum_s coef[s][n] * src[s][tile][c]; zero for n >= nmax.
 // srcp = src + tile*WB + c, sstride = ntiles*WB (one spatial vector per source).
+// FD: a.fdense is set (a template switch: the runtime test and the element index cost the CQ T-pass
+// 15 % through register pressure, 8.3 -> 9.5 ms on C5)
+template <bool FD>
 __device__ __forceinline__ double2 static_rhs(const TPassArgs& a, const double2* srcp, long sstride, int N, int n,
                                               long e) {
   double2 f = make_double2(0.0, 0.0);
   if (n >= a.nmax) return f;
   for (int s = 0; s < a.S; ++s) f = cfmar(ldt(&srcp[s * sstride]), ldt(&a.coef[(long)s * N + n]), f);
-  if (a.fdense) f = cadd(f, ldt(&a.fdense[e]));
+  if constexpr (FD) f = cadd(f, ldt(&a.fdense[e]));
   return f;
 }
 
-template <int N, int MODE_IN, int MODE_OUT, bool CQ>
+template <int N, int MODE_IN, int MODE_OUT, bool CQ, bool FD = false>
 __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpass_kernel(const TPassArgs a, long ntiles) {
   using TM = TimeMap<N>;
   using FM = FreqMap<N>;
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
         // F_static is zero for n >= nmax; with nmax <= PL only s == 0 slots can be nonzero
         const bool live = (s == 0) || dense || (TM::PL < 8);
         double2 F = make_double2(0.0, 0.0);
-        if (live) F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
+        if (live) F = static_rhs<FD>(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
         if ((s == 0 || TM::PL < 8) && n < k) {
           // (kappa/tau) sum_{j=n+1}^{k} omega_j U_m^{N+n-j} (0-based levels), window index k+n-j
           for (int jw = n + 1; jw <= k; ++jw) F = cfmar(sW[(k + n - jw) * WB + c], __ldg(&a.wk[jw]), F);
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
         const int n = TM::n(j, s, tid), c = TM::c(j, tid);
-        const double2 F = static_rhs(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
+        const double2 F = static_rhs<FD>(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
         const int r = j * TM::RL + s;
         v[r] = cfmar(F, ldt(&a.gsfq[n]), cmul(v[r], ldt(&a.thm[n])));
       }

@@ -506,8 +506,12 @@ def test_graph_replay_matches_eager(pint, monkeypatch, mx, my, N, k):
         l0 = [p.info()["kernel_launches"] for p in (eager, graph)]
         for it in range(4):
             if it == 2:
-                graph.set_timing(True)
+                graph.set_timing(True)   # event nodes inside the replayed graph
             ue, ug = eager.iterate(), graph.iterate()
+            if it == 2:
+                tm = graph.get_timing()
+                assert tm["spass_launches"] == 1 and tm["tpass_launches"] == 1, tm
+                assert tm["spass_ms"] > 0.0 and tm["tpass_ms"] > 0.0, tm
             graph.set_timing(False)
             assert ue == ug, (it, ue, ug)
         assert [p.info()["kernel_launches"] - l for p, l in zip((eager, graph), l0)] == [8, 8]
