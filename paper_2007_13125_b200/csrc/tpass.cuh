@@ -28,6 +28,9 @@ namespace pint {
 #ifndef PINT_TPASS_MINB
 #define PINT_TPASS_MINB 2
 #endif
+#ifndef CQ_SV
+#define CQ_SV 2   // CQ T-pass: sources whose column values stay in registers for the whole tile
+#endif
 
 enum { IN_FREQ = 0, IN_TIME_V = 1, IN_TIME_ZERO = 2, IN_TIME_BUF = 3 };
 enum { OUT_H = 0, OUT_U = 1 };
@@ -80,6 +83,26 @@ __device__ __forceinline__ double ldt(const double* p) {
   double r;
   asm volatile("ld.global.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
+}
+
+// L2 eviction-priority policies (createpolicy) for loads/stores with an explicit cache hint
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* ptr, unsigned long long pol) {
+  double2 r;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_hint(double2* ptr, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
 
 __device__ __forceinline__ void prefetch_l2_t(const void* p, unsigned bytes) {
@@ -144,8 +167,15 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
 
   // ---------------- input ----------------
   if constexpr (MODE_IN == IN_FREQ) {
+    if constexpr (CQ && MODE_OUT == OUT_H) {
+      // W is re-read for the D W term at the end of the tile: keep it in L2 until then
+      const unsigned long long keep = l2_evict_last();
 #pragma unroll
-    for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
+      for (int t = 0; t < 16; ++t) v[t] = ld_hint(&a.in[base + FM::e(t, tid)], keep);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
+    }
     run_passes<N, +1, false>(v, sm, tw, tid);        // u = V W  (unnormalised inverse DFT)
   } else {
     // time-domain input U (registers in TimeMap)
@@ -243,13 +273,27 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = cmul(v[t], ldt(&a.dpr[FM::p(t, tid)]));
     run_passes<N, +1, false>(v, sm, tw, tid);
-    // X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s
+    // X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s.  A thread's column is the same for
+    // every element (TPB % WB == 0): the first CQ_SV source values are loaded once per tile.
+    static_assert(TPB % WB == 0, "fixed column per thread");
+    const int cc = tid % WB;
+    double2 sv[CQ_SV];
+#pragma unroll
+    for (int q = 0; q < CQ_SV; ++q) sv[q] = q < a.S ? ldt(&a.src[(long)q * ntiles * WB + tile * WB + cc]) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int j = 0; j < TM::NJ; ++j)
 #pragma unroll
       for (int s = 0; s < TM::RL; ++s) {
-        const int n = TM::n(j, s, tid), c = TM::c(j, tid);
-        const double2 F = static_rhs<FD>(a, a.src + tile * WB + c, ntiles * WB, N, n, base + TM::e(j, s, tid));
+        const int n = TM::n(j, s, tid);
+        double2 F = make_double2(0.0, 0.0);
+        if (n < a.nmax) {
+#pragma unroll
+          for (int q = 0; q < CQ_SV; ++q)
+            if (q < a.S) F = cfmar(sv[q], ldt(&a.coef[(long)q * N + n]), F);
+          for (int q = CQ_SV; q < a.S; ++q)
+            F = cfmar(ldt(&a.src[(long)q * ntiles * WB + tile * WB + cc]), ldt(&a.coef[(long)q * N + n]), F);
+          if constexpr (FD) F = cadd(F, ldt(&a.fdense[base + TM::e(j, s, tid)]));
+        }
         const int r = j * TM::RL + s;
         v[r] = cfmar(F, ldt(&a.gsfq[n]), cmul(v[r], ldt(&a.thm[n])));
       }
@@ -258,13 +302,21 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
 #pragma unroll
       for (int t = 0; t < 16; ++t) v[t] = cadd(v[t], dw[t]);
     } else {
+      const unsigned long long last = l2_evict_first();   // W's last use
 #pragma unroll
-      for (int t = 0; t < 16; ++t) v[t] = cfma(a.in[base + FM::e(t, tid)], ldt(&a.dh[FM::p(t, tid)]), v[t]);
+      for (int t = 0; t < 16; ++t) v[t] = cfma(ld_hint(&a.in[base + FM::e(t, tid)], last), ldt(&a.dh[FM::p(t, tid)]), v[t]);
     }
   }
 
+  if constexpr (CQ) {
+    // H is next read by the S-pass after the whole T-pass: do not let it displace the W tiles
+    const unsigned long long stream = l2_evict_first();
 #pragma unroll
-  for (int t = 0; t < 16; ++t) a.out[base + FM::e(t, tid)] = v[t];
+    for (int t = 0; t < 16; ++t) st_hint(&a.out[base + FM::e(t, tid)], v[t], stream);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) a.out[base + FM::e(t, tid)] = v[t];
+  }
   __syncthreads();   // smem reused by the next tile
   }  // tile loop
 
