@@ -22,7 +22,7 @@ def fbar(prob) -> np.ndarray:
     (PAPER.md:281-288 eqn:BDF; the same f̄ for CQ-BDFk, PAPER.md:974-982 eqn:BDF-frac).
     Corrections vanish for n >= k."""
     N, M, k, tau = prob.N, prob.M, prob.k, prob.tau
-    Av = spatial.apply_A(prob.v, prob.mx, prob.my)
+    Av = spatial.apply_A(prob.v, prob.mx, prob.my, getattr(prob, "space", "fd"))
     f0 = forcing_at(prob, 0)
     out = np.zeros((N, M), np.complex128)
     for n in range(1, N + 1):

@@ -11,12 +11,13 @@ from . import bdf, problem, spatial
 
 
 def _solver(prob, shift: complex, method: str):
+    space = getattr(prob, "space", "fd")
     if method == "dst":
-        return lambda b: spatial.solve_shifted_dst(np.array([shift]), b[None, :], prob.mx, prob.my)[0]
+        return lambda b: spatial.solve_shifted_dst(np.array([shift]), b[None, :], prob.mx, prob.my, space)[0]
     if method == "banded":
         if prob.my != 1:
             raise ValueError("banded LU is 1D only")
-        return lambda b: spatial.solve_shifted_banded(shift, b[None, :], prob.mx)[0]
+        return lambda b: spatial.solve_shifted_banded(shift, b[None, :], prob.mx, space)[0]
     if method == "lu":
         lu = spatial.ShiftedLU(shift, prob.mx, prob.my)
         return lu.solve

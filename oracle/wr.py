@@ -83,7 +83,7 @@ class Operator:
     def solve(self, shifts: np.ndarray, H: np.ndarray) -> np.ndarray:
         if self.diag is not None:
             return H / (shifts[:, None] + self.diag[None, :])
-        return spatial.solve_shifted_dst(shifts, H, self.prob.mx, self.prob.my)
+        return spatial.solve_shifted_dst(shifts, H, self.prob.mx, self.prob.my, getattr(self.prob, "space", "fd"))
 
 
 def initial_guess(prob) -> np.ndarray:

@@ -41,6 +41,8 @@ class Problem:
     dphi: np.ndarray   # float64 [R][max(k-2,0)]
     u0: str = "v"      # WR initial guess: "v" or "zero" (tables)
     tol: float = 1e-12
+    space: str = "fd"  # "fd": 3/5-point stencil (BASELINE); "fem": 1D P1 Galerkin,
+                       # v and g_r are then nodal coefficient vectors
 
     @property
     def dim(self) -> int:
@@ -176,6 +178,12 @@ def example1_fd(k: int, M: int = 999, N: int = 100, kappa: float = 0.5) -> Probl
     g = np.cos(x).astype(np.complex128)[None, :]
     dphi = np.ones((1, max(k - 2, 0)))
     return Problem(f"E1_k{k}", M, 1, T, N, k, kappa, 1.0, v, g, phi, dphi, u0="zero")
+
+
+def example1_fem(k: int, M: int = 999, N: int = 100, kappa: float = 0.5) -> Problem:
+    """The paper's Example 1 in its own discretisation (P1 FEM):
+    v_h and f~ = the nodal interpolants of chi_(0,1/2) and e^t cos x (READING R-FEMdata), U_0 = 0."""
+    return example1_fd(k, M, N, kappa).with_(name=f"E1fem_k{k}", space="fem")
 
 
 def example2_fd(k: int, M: int = 999, N: int = 100, kappa: float = 0.1,

@@ -3,6 +3,7 @@ import os
 
 import numpy as np
 import pytest
+import scipy.linalg
 
 from oracle import bdf, dense, modal, sequential, spatial, theory, wr
 from paper_2007_13125_b200 import inputs
@@ -215,3 +216,79 @@ def test_modal_equals_grid():
     md = modal.modal_wr(p, basis, C, Gc, 3)
     for m in range(4):
         assert rel(basis.to_grid(md[m]), grid[m]) < 1e-12
+
+
+# --- P1 FEM operator -----------------------------
+
+@pytest.mark.parametrize("m", [7, 31])
+def test_fem_eigenpairs(m):
+    """fem_eigenvalues (K_j / M_j closed form) against LAPACK's generalised symmetric eigensolver
+    for K x = lambda M x; the sine vectors are the eigenvectors."""
+    K, Mm = (x.toarray() for x in spatial.fem_matrices(m))
+    ref = scipy.linalg.eigh(K, Mm, eigvals_only=True)
+    lam = spatial.fem_eigenvalues(m)
+    assert np.allclose(np.sort(lam), ref, rtol=1e-12, atol=0)
+    S = spatial.dst1_matrix(m)
+    assert np.allclose(K @ S, (Mm @ S) * lam[None, :], rtol=0, atol=1e-9 * lam.max())
+    # A = M^{-1} K applied by the oracle equals the dense product
+    u = np.random.default_rng(1).standard_normal(m) + 0j
+    assert np.allclose(spatial.apply_A(u, m, 1, "fem"), np.linalg.solve(Mm, K @ u), rtol=1e-12, atol=1e-9)
+
+
+def test_fem_banded_vs_dst():
+    m, rng = 63, np.random.default_rng(2)
+    shifts = np.array([3.0 + 40j, 1e-3 - 2e-3j, 250.0])
+    b = rng.standard_normal((3, m)) + 1j * rng.standard_normal((3, m))
+    x_dst = spatial.solve_shifted_dst(shifts, b, m, 1, "fem")
+    x_lu = np.stack([spatial.solve_shifted_banded(s, b[i:i + 1], m, "fem")[0] for i, s in enumerate(shifts)])
+    assert np.abs(x_dst - x_lu).max() <= 1e-10 * np.abs(x_lu).max()
+    K, Mm = (x.toarray() for x in spatial.fem_matrices(m))
+    for i, s in enumerate(shifts):   # the defining equation (s M + K) x = M b
+        r = (s * Mm + K) @ x_dst[i] - Mm @ b[i]
+        assert np.abs(r).max() <= 1e-9 * np.abs(Mm @ b[i]).max()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_fem_observed_order(k):
+    """Nodal sin(pi x) is an exact eigenvector of A = M^{-1} K, so the semi-discrete solution is
+    e^{-lambda_1 t} sin(pi x_i) with the FEM eigenvalue: BDFk converges to it at order k.  The FD
+    eigenvalue differs by O(h^2) and would stall the error at ~1e-3 (checked)."""
+    M = 15
+    x = inputs.grid1d(M)
+    lam_fem, lam_fd = spatial.fem_eigenvalues(M)[0], spatial.fd_eigenvalues(M)[0]
+    errs = []
+    for N in (40, 80):
+        p = inputs.example1_fem(k, M=M, N=N).with_(T=1.0, u0="v", v=np.sin(np.pi * x).astype(complex),
+                                                    g=np.zeros((0, M), complex), phi=np.zeros((0, N + 1)),
+                                                    dphi=np.zeros((0, max(k - 2, 0))))
+        U = sequential.sequential(p)[-1]
+        errs.append(np.abs(U - np.exp(-lam_fem) * np.sin(np.pi * x)).max())
+        if N == 80 and k >= 3:   # (k <= 2: the time error itself is as large as the O(h^2) gap)
+            assert np.abs(U - np.exp(-lam_fd) * np.sin(np.pi * x)).max() > 10 * errs[-1]
+    rate = np.log2(errs[0] / errs[1])
+    assert abs(rate - k) < 0.3, (k, rate, errs)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_fem_fixed_point_and_dense(alpha):
+    """The WR iteration with the FEM operator converges to sequential FEM stepping (banded LU), and
+    one iteration equals the dense all-at-once kappa-periodic solve with A = M^{-1} K."""
+    p = inputs.random_complex_problem(15, 1, 16, 2, 0.05, alpha, R=1, seed=4).with_(space="fem")
+    Us = sequential.sequential(p)
+    U = wr.wr_naive(p, 12)[-1]
+    assert np.linalg.norm(U - Us) <= 1e-11 * np.linalg.norm(Us)
+    U0 = wr.initial_guess(p)
+    assert rel(wr.wr_naive(p, 1, U0=U0)[1], dense.dense_iteration(p, U0)) < 1e-12
+
+
+@pytest.mark.parametrize("k", range(1, 7))
+def test_table2_example1_fem(k):
+    """PAPER.md:1414-1436 in the paper's own discretisation (P1 FEM, FE mass norm): e_m^N for
+    m = 0..3 within one unit in the third digit (as the FD analog)."""
+    g = _golden("table2_example1.txt")
+    p = inputs.example1_fem(k)
+    Us = sequential.sequential(p)
+    _, Mm = spatial.fem_matrices(p.mx)
+    e = [float(np.sqrt(np.real(np.vdot(U[-1] - Us[-1], Mm @ (U[-1] - Us[-1]))))) for U in wr.wr_naive(p, 3)]
+    for m in range(4):
+        assert abs(e[m] - g[m][k - 1]) <= 0.011 * g[m][k - 1] + 1e-13, (k, m, e[m], g[m][k - 1])
