@@ -56,7 +56,14 @@ typedef enum {
   PINT_ERR_UNSUPPORTED = 8     /* valid but not implemented on this path (message says what) */
 } pint_status;
 
-enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2 };
+/* PINT_OP_FEM1D_DIRICHLET: the paper's own discretisation of Examples 1-2 (PAPER.md:1374-1375,
+ * SURVEY §8(f) item 4): piecewise-linear Galerkin on the uniform mesh of (0,1), h = 1/(mx+1),
+ * stiffness K = (1/h) tridiag(-1,2,-1), mass M = (h/6) tridiag(1,4,1); the plan solves
+ * U' + A U = f~ with A = M^{-1} K (v, g_r, U: nodal coefficient vectors; f~ the projected or
+ * interpolated forcing).  my must be 1.  It runs on the fully modal path (the DST diagonalises
+ * both K and M: lambda_j = K_j / M_j), so it needs alpha = 1 and 2(mx+1) a power of two
+ * (UNSUPPORTED otherwise); PINT_FLAG_MODAL is implied. */
+enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2, PINT_OP_FEM1D_DIRICHLET = 3 };
 enum { PINT_HOST = 0, PINT_DEVICE = 1 };
 enum {
   PINT_FLAG_U0_ZERO = 1,       /* WR initial guess U_0 = 0 instead of U_0^n = v */
@@ -70,15 +77,16 @@ enum {
   PINT_FLAG_REAL_DATA = 16,    /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
                                   and only the frequencies p <= N/2 are solved (SURVEY §8(f) item
                                   2b); pint_set_problem_separable returns ARG for complex data */
-  PINT_FLAG_MODAL = 32         /* 2D heat: fully modal variant — the DST is
-                                  applied along y as well (hoisted), every (x-mode, y-mode) is a
-                                  scalar problem and the shifted solves are divisions; needs
-                                  2(my+1) a power of two (UNSUPPORTED otherwise), excludes
-                                  PINT_FLAG_STREAM / PINT_FLAG_DST_PER_ITER (ARG) */
+  PINT_FLAG_MODAL = 32         /* heat: fully modal variant — the DST is
+                                  applied along the line axis as well (2D: y; 1D: x; hoisted), every
+                                  mode is a scalar problem and the shifted solves are divisions;
+                                  needs 2(L+1) a power of two, L = my (2D) or mx (1D)
+                                  (UNSUPPORTED otherwise), excludes PINT_FLAG_STREAM /
+                                  PINT_FLAG_DST_PER_ITER (ARG) */
 };
 
 typedef struct {
-  int32_t kind;                /* PINT_OP_FD1D_DIRICHLET or PINT_OP_FD2D_DIRICHLET */
+  int32_t kind;                /* PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET or PINT_OP_FEM1D_DIRICHLET */
   int64_t mx, my;              /* grid points per axis (1D: my = 1); M = mx*my */
 } pint_operator;
 

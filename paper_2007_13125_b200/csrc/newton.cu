@@ -37,4 +37,9 @@ cudaError_t launch_imag_max(const double2* A, long count, unsigned long long* up
   return cudaGetLastError();
 }
 
+cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st) {
+  mode_scale_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, in, mu, s, L);
+  return cudaGetLastError();
+}
+
 }  // namespace pint

@@ -141,6 +141,13 @@ __global__ void imag_max_kernel(const double2* A, long count, unsigned long long
   if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
 }
 
+// out[j] = in[j] mu[j] s: an operator diagonal in the DST modes applied to a modal vector
+// (P1-FEM: A v = M^{-1} K v with mu_j = h^2 K_j / M_j, s = 1/h^2)
+__global__ void mode_scale_kernel(double2* out, const double2* in, const double* mu, double s, int L) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < L; j += gridDim.x * blockDim.x)
+    out[j] = cscale(in[j], mu[j] * s);
+}
+
 #endif  // PINT_DEFINE_NEWTON_KERNELS
 
 }  // namespace pint

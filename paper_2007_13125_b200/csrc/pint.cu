@@ -167,6 +167,7 @@ struct pint_plan_s {
   bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
   bool half = false;          // PINT_FLAG_REAL_DATA: half-spectrum fused iteration
   bool modal = false;         // PINT_FLAG_MODAL: DST along y too, one warp per (q, j) mode
+  bool fem = false;           // PINT_OP_FEM1D_DIRICHLET (modal, mu_j = h^2 K_j / M_j)
   int NEy = 0;
   double2* twEy = nullptr;    // [NEy] DST-y twiddles
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
@@ -320,29 +321,33 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (N < k + 1) return fail(PINT_ERR_ARG, "N must be >= k+1 (DESIGN.md reading R-Nk)");
   const double alpha = opt ? opt->alpha : 1.0;
   if (!(alpha > 0.0 && alpha <= 1.0)) return fail(PINT_ERR_ARG, "alpha must be in (0,1]");
-  if (op->kind != PINT_OP_FD1D_DIRICHLET && op->kind != PINT_OP_FD2D_DIRICHLET)
-    return fail(PINT_ERR_ARG, "op->kind must be PINT_OP_FD1D_DIRICHLET or PINT_OP_FD2D_DIRICHLET");
+  if (op->kind != PINT_OP_FD1D_DIRICHLET && op->kind != PINT_OP_FD2D_DIRICHLET && op->kind != PINT_OP_FEM1D_DIRICHLET)
+    return fail(PINT_ERR_ARG, "op->kind must be PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET or PINT_OP_FEM1D_DIRICHLET");
   if (op->mx < 1 || op->my < 1) return fail(PINT_ERR_ARG, "op->mx, op->my must be >= 1");
-  if (op->kind == PINT_OP_FD1D_DIRICHLET && op->my != 1) return fail(PINT_ERR_ARG, "1D operator needs my == 1");
+  const bool fem = op->kind == PINT_OP_FEM1D_DIRICHLET;
+  if ((op->kind == PINT_OP_FD1D_DIRICHLET || fem) && op->my != 1) return fail(PINT_ERR_ARG, "1D operator needs my == 1");
   if (op->mx * op->my != M) return fail(PINT_ERR_ARG, "M must equal mx*my");
   const int rank = opt ? opt->rank : 0, nranks = opt ? opt->nranks : 1;
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PINT_ERR_ARG, "need 0 <= rank < nranks");
-  if (nranks > 1 && op->kind == PINT_OP_FD1D_DIRICHLET)
+  if (nranks > 1 && op->kind != PINT_OP_FD2D_DIRICHLET)
     return fail(PINT_ERR_ARG, "1D operators do not shard (replicas only): nranks must be 1");
   if (nranks > op->mx) return fail(PINT_ERR_ARG, "nranks must be <= mx");
   if (opt && (opt->flags & PINT_FLAG_DST_PER_ITER) && (op->kind != PINT_OP_FD2D_DIRICHLET || nranks != 1))
     return fail(PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator on one rank");
-  if (opt && (opt->flags & PINT_FLAG_MODAL)) {
-    if (op->kind != PINT_OP_FD2D_DIRICHLET || (opt->alpha != 1.0))
-      return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL needs a 2D heat problem (alpha = 1)");
-    if (opt->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER))
+  const int32_t flags = (opt ? opt->flags : 0) | (fem ? PINT_FLAG_MODAL : 0);   // P1-FEM runs modal
+  if (fem && (opt ? opt->alpha : 1.0) != 1.0)
+    return fail(PINT_ERR_UNSUPPORTED, "PINT_OP_FEM1D_DIRICHLET runs on the fully modal heat path (alpha = 1)");
+  if (flags & PINT_FLAG_MODAL) {
+    const int64_t Lm = op->kind == PINT_OP_FD2D_DIRICHLET ? op->my : op->mx;
+    if ((opt ? opt->alpha : 1.0) != 1.0) return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL needs a heat problem (alpha = 1)");
+    if (flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER))
       return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL excludes PINT_FLAG_STREAM and PINT_FLAG_DST_PER_ITER");
-    if (!is_pow2(2 * (op->my + 1)) || 2 * (op->my + 1) < 16 || 2 * (op->my + 1) > 4096)
-      return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_MODAL needs 2(my+1) a power of two in [16, 4096]");
+    if (!is_pow2(2 * (Lm + 1)) || 2 * (Lm + 1) < 16 || 2 * (Lm + 1) > 4096)
+      return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_MODAL needs 2(L+1) a power of two in [16, 4096] (L = my in 2D, mx in 1D)");
   }
   if (nranks > 1 && !(opt && opt->allreduce_max)) return fail(PINT_ERR_ARG, "nranks > 1 needs allreduce_max");
   if (!is_pow2(N) || N < 16 || N > 4096) return fail(PINT_ERR_UNSUPPORTED, "N must be a power of two in [16, 4096]");
-  const int dim = op->kind == PINT_OP_FD1D_DIRICHLET ? 1 : 2;
+  const int dim = op->kind == PINT_OP_FD2D_DIRICHLET ? 2 : 1;
   const int64_t L = dim == 1 ? op->mx : op->my;
   if (L > 1024) return fail(PINT_ERR_UNSUPPORTED, "line length (1D: mx, 2D: my) must be <= 1024");
   int NE = 0;
@@ -353,7 +358,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
 
   pint_plan p = new pint_plan_s();
   p->M = M; p->N = N; p->mx = op->mx; p->my = op->my; p->k = k; p->dim = dim;
-  p->flags = opt ? opt->flags : 0; p->rank = rank; p->nranks = nranks;
+  p->flags = flags; p->rank = rank; p->nranks = nranks; p->fem = fem;
   p->kappa = kappa; p->tau = tau; p->alpha = alpha;
   p->allreduce = opt ? opt->allreduce_max : nullptr; p->actx = opt ? opt->allreduce_ctx : nullptr;
   p->L = L; p->h = 1.0 / (double)(L + 1); p->NE = NE;
@@ -439,7 +444,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   p->modal = (p->flags & PINT_FLAG_MODAL) != 0;
   if (p->modal) {
     p->Lf = (int)(p->NB * p->WB);    // X / partials indexed by the y-mode j < my
-    p->NEy = (int)(2 * (op->my + 1));
+    p->NEy = (int)(2 * (L + 1));
   }
   if (p->fused_ok && p->modal) {
     p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
@@ -449,7 +454,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       if ((st = dalloc(p, &p->X[i], (size_t)p->Qb * 8 * p->Lf)) != PINT_OK) return bail(st);
     if ((st = dalloc(p, &p->Pp, (size_t)p->Qb * k * p->Lf)) != PINT_OK) return bail(st);
     if ((st = dalloc(p, &p->twEy, p->NEy)) != PINT_OK) return bail(st);
-    if ((st = dalloc(p, &p->mu, (size_t)op->my)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->mu, (size_t)L)) != PINT_OK) return bail(st);
     for (int i = 0; i < 2; ++i) {
       ce = cudaMemsetAsync(p->X[i], 0, (size_t)p->Qb * 8 * p->Lf * sizeof(double2), p->stream);
       if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
@@ -558,10 +563,12 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       twEy[m] = make_double2((double)cosl(ang), (double)-sinl(ang));
     }
     if ((st = h2d(p, p->twEy, twEy)) != PINT_OK) return bail(st);
-    std::vector<double> mu(p->my);
-    for (int64_t jj = 0; jj < p->my; ++jj) {
-      const ld sn = sinl((ld)(jj + 1) * PI_L / (2.0L * (ld)(p->my + 1)));
-      mu[jj] = (double)(4.0L * sn * sn);
+    // h^2 lambda_j of the line operator: FD 4 s^2 (tridiag(-1,2,-1)); P1 FEM K_j / M_j =
+    // 4 s^2 / (1 - (2/3) s^2), s = sin(j pi h / 2) (stiffness and mass share the sine modes)
+    std::vector<double> mu(L);
+    for (int64_t jj = 0; jj < L; ++jj) {
+      const ld sn = sinl((ld)(jj + 1) * PI_L / (2.0L * (ld)(L + 1)));
+      mu[jj] = (double)(fem ? 4.0L * sn * sn / (1.0L - 2.0L * sn * sn / 3.0L) : 4.0L * sn * sn);
     }
     if ((st = h2d(p, p->mu, mu)) != PINT_OK) return bail(st);
   }
@@ -720,9 +727,9 @@ static DstArgs dargs(pint_plan p) {
 static pint_status dst_y(pint_plan p, const double2* in, double2* out, long levels, long nq) {
   DstArgs a{};
   a.in = in; a.out = out; a.rows = nq * levels;
-  a.mx = (int)p->my; a.my = 1; a.WB = p->WB; a.NB = p->NB; a.N = levels; a.n0 = 0;
+  a.mx = (int)p->L; a.my = 1; a.WB = p->WB; a.NB = p->NB; a.N = levels; a.n0 = 0;
   a.q0 = 0; a.Qb = nq; a.M = p->M;
-  a.scale = (double)sqrtl(2.0L / (ld)(p->my + 1));
+  a.scale = (double)sqrtl(2.0L / (ld)(p->L + 1));
   a.tw = p->twEy;
   CUDA_TRY(launch_dst(p->NEy, a, DST_TILE_Y, p->stream));
   ++p->launches;
@@ -823,6 +830,10 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     TRY(to_source(p, p->phys, 2 + r));
   }
   if (p->modal && p->fused_ok) TRY(dst_y(p, p->src, p->src, 1, (long)S * p->Qb));   // sources -> (q, j) modes
+  if (p->fem) {   // A v = M^{-1} K v is diagonal in the modes: (A v)_j = (mu_j / h^2) v_j (source 1 <- source 0)
+    CUDA_TRY(launch_mode_scale(p->src + (size_t)p->ntiles * p->WB, p->src, p->mu, 1.0 / (p->h * p->h), (int)p->L, p->stream));
+    ++p->launches;
+  }
   if (chk_real) {
     double im = 0.0;
     unsigned long long bits = 0;
@@ -1178,8 +1189,8 @@ extern "C" pint_status pint_set_nonlinearity(pint_plan p, int32_t kind, double e
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (kind != PINT_NL_ALLEN_CAHN) return fail(PINT_ERR_ARG, "kind must be PINT_NL_ALLEN_CAHN");
   if (!(eps > 0.0) || !std::isfinite(eps)) return fail(PINT_ERR_ARG, "eps must be > 0");
-  if (p->dim != 1 || p->nranks != 1)
-    return fail(PINT_ERR_UNSUPPORTED, "the Newton-WR extension is 1D on one rank (g'(Ubar(x)) breaks the DST)");
+  if (p->dim != 1 || p->nranks != 1 || p->fem)
+    return fail(PINT_ERR_UNSUPPORTED, "the Newton-WR extension is 1D FD on one rank (g'(Ubar(x)) breaks the DST)");
   CUDA_TRY(cudaSetDevice(p->device));
   p->nl_eps = eps;
   p->fused_ok = false;

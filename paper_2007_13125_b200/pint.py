@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PINT_LIB", os.path.join(HERE, "libpint.so"))
 
 PINT_OK, PINT_ERR_ARG, PINT_ERR_ALLOC, PINT_ERR_CUDA, PINT_ERR_COMM, PINT_ERR_STATE, \
     PINT_ERR_NOT_CONVERGED, PINT_ERR_DIVERGED, PINT_ERR_UNSUPPORTED = range(9)
-PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET = 1, 2
+PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET, PINT_OP_FEM1D_DIRICHLET = 1, 2, 3
 PINT_HOST, PINT_DEVICE = 0, 1
 PINT_FLAG_U0_ZERO = 1
 PINT_FLAG_FULL_FFT = 2
@@ -144,11 +144,13 @@ class Plan:
                  device: int = 0, stream: int | None = None, u0_zero: bool = False,
                  rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False,
                  stream_path: bool = False, dst_per_iter: bool = False, real_data: bool = False,
-                 modal: bool = False):
+                 modal: bool = False, fem: bool = False):
+        """fem=True: 1D P1 finite elements (PINT_OP_FEM1D_DIRICHLET; nodal coefficient vectors)."""
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
         self.M = self.mx * self.my
-        op = pint_operator(PINT_OP_FD1D_DIRICHLET if my == 1 else PINT_OP_FD2D_DIRICHLET, mx, my)
+        kind = PINT_OP_FEM1D_DIRICHLET if fem else (PINT_OP_FD1D_DIRICHLET if my == 1 else PINT_OP_FD2D_DIRICHLET)
+        op = pint_operator(kind, mx, my)
         self._cb = ALLREDUCE_FN(0)
         if allreduce_max is not None:
             def _cb(p, ctx):
@@ -193,6 +195,7 @@ class Plan:
 
     @classmethod
     def from_problem(cls, prob, device_arrays: bool = False, **kw) -> "Plan":
+        kw.setdefault("fem", getattr(prob, "space", "fd") == "fem")
         p = cls(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha,
                 u0_zero=(prob.u0 == "zero"), **kw)
         v, g = prob.v, (prob.g if prob.R else None)

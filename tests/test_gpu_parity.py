@@ -527,3 +527,43 @@ def test_graph_replay_matches_eager(pint, monkeypatch, mx, my, N, k):
     finally:
         eager.close()
         graph.close()
+
+
+FEM_CASES = [
+    ("fem_63_bdf2", lambda: inputs.random_complex_problem(63, 1, 64, 2, 0.1, 1.0, R=2, seed=12).with_(space="fem"), 4),
+    ("fem_1023_bdf4", lambda: inputs.random_complex_problem(1023, 1, 1024, 4, 0.01, 1.0, R=1, seed=11).with_(space="fem"), 3),
+    ("fem_example1_bdf3", lambda: inputs.example1_fem(3, M=1023, N=128), 3),
+    ("fd_modal_1d_bdf6", lambda: inputs.random_complex_problem(255, 1, 256, 6, 0.05, 1.0, R=1, seed=13), 3),
+]
+
+
+@pytest.mark.parametrize("name,make,iters", FEM_CASES, ids=[c[0] for c in FEM_CASES])
+def test_fem_and_modal_1d(pint, name, make, iters):
+    """1D on the fully modal path: P1 FEM (PINT_OP_FEM1D_DIRICHLET) and the FD
+    operator with PINT_FLAG_MODAL, against the oracle (FEM: A = M^{-1} K), every iterate; then
+    wr_solve converges to the oracle's sequential stepping in the same discretisation."""
+    prob = make()
+    o = wr.wr_naive(prob, iters, dft="fft")
+    kw = {} if prob.space == "fem" else {"modal": True}
+    errs = []
+    with pint.Plan.from_problem(prob, **kw) as p:
+        assert p.path()["fused"]
+        for m in range(1, iters + 1):
+            p.iterate()
+            errs.append(rel(p.get_solution(), o[m]))
+        it, u, st = p.solve(1e-12, 40)
+        seq_err = rel(p.get_solution(), sequential.sequential(prob))
+    print(name, errs, it, seq_err)
+    assert max(errs) <= TOL, errs
+    assert st == 0 and seq_err <= 1e-9, (st, seq_err)
+
+
+def test_fem_rejects_unsupported(pint):
+    prob = inputs.random_complex_problem(63, 1, 64, 2, 0.1, 0.5, R=0, seed=1).with_(space="fem")
+    with pytest.raises(pint.PintError) as e:
+        pint.Plan.from_problem(prob)
+    assert e.value.status == pint.PINT_ERR_UNSUPPORTED
+    prob = inputs.random_complex_problem(62, 1, 64, 2, 0.1, 1.0, R=0, seed=1).with_(space="fem")   # 2(mx+1) = 126
+    with pytest.raises(pint.PintError) as e:
+        pint.Plan.from_problem(prob)
+    assert e.value.status == pint.PINT_ERR_UNSUPPORTED
