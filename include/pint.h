@@ -61,8 +61,9 @@ typedef enum {
  * stiffness K = (1/h) tridiag(-1,2,-1), mass M = (h/6) tridiag(1,4,1); the plan solves
  * U' + A U = f~ with A = M^{-1} K (v, g_r, U: nodal coefficient vectors; f~ the projected or
  * interpolated forcing).  my must be 1.  It runs on the fully modal path (the DST diagonalises
- * both K and M: lambda_j = K_j / M_j), so it needs alpha = 1 and 2(mx+1) a power of two
- * (UNSUPPORTED otherwise); PINT_FLAG_MODAL is implied. */
+ * both K and M: lambda_j = K_j / M_j; heat: fused modal kernel, CQ: streaming path with the
+ * shifted solves as divisions), so it needs 2(mx+1) a power of two (UNSUPPORTED otherwise);
+ * PINT_FLAG_MODAL is implied. */
 enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2, PINT_OP_FEM1D_DIRICHLET = 3 };
 enum { PINT_HOST = 0, PINT_DEVICE = 1 };
 enum {
@@ -77,11 +78,12 @@ enum {
   PINT_FLAG_REAL_DATA = 16,    /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
                                   and only the frequencies p <= N/2 are solved (SURVEY §8(f) item
                                   2b); pint_set_problem_separable returns ARG for complex data */
-  PINT_FLAG_MODAL = 32         /* heat: fully modal variant — the DST is
-                                  applied along the line axis as well (2D: y; 1D: x; hoisted), every
-                                  mode is a scalar problem and the shifted solves are divisions;
-                                  needs 2(L+1) a power of two, L = my (2D) or mx (1D)
-                                  (UNSUPPORTED otherwise), excludes PINT_FLAG_STREAM /
+  PINT_FLAG_MODAL = 32         /* fully modal variant — the DST is applied
+                                  along the line axis as well (2D: y; 1D: x; hoisted), every mode is
+                                  a scalar problem and the shifted solves are divisions (heat: the
+                                  fused modal kernel; CQ or PINT_FLAG_STREAM: the streaming path with
+                                  an elementwise division pass); needs 2(L+1) a power of two, L = my
+                                  (2D) or mx (1D) (UNSUPPORTED otherwise); excludes
                                   PINT_FLAG_DST_PER_ITER (ARG) */
 };
 

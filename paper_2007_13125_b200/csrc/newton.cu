@@ -37,6 +37,14 @@ cudaError_t launch_imag_max(const double2* A, long count, unsigned long long* up
   return cudaGetLastError();
 }
 
+cudaError_t launch_modal_div(const SPassArgs& a, const double* mu, long Qb, cudaStream_t st) {
+  const long total = Qb * a.NB * a.N * a.WB;
+  const long blocks = std::min<long>((total + 255) / 256, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  modal_div_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, mu, total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st) {
   mode_scale_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, in, mu, s, L);
   return cudaGetLastError();

@@ -141,6 +141,26 @@ __global__ void imag_max_kernel(const double2* A, long count, unsigned long long
   if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
 }
 
+// Streaming modal path (PINT_FLAG_MODAL with CQ or PINT_FLAG_STREAM): with the DST applied along
+// the line axis too, Step 2 of Algorithm 1/2 is W_{p,q,j} = H_{p,q,j} / (sigma_p + sigma_q + mu_j)
+// (h^2-scaled shift + eigenvalues; the shift is never added to a rounded 2: exact in the shift).
+// Tile layout [q][jb][N][WB], j = jb WB + w; pad modes j >= L stay zero.  32 B per unknown.
+__global__ void modal_div_kernel(const SPassArgs a, const double* mu, long total) {
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int w = (int)(e % a.WB);
+    const long r = e / a.WB;
+    const long n = r % a.N, r2 = r / a.N;
+    const long jb = r2 % a.NB, q = r2 / a.NB;
+    const int j = (int)(jb * a.WB + w);
+    double2 x = make_double2(0.0, 0.0);
+    if (j < a.L) {
+      const double2 sp = __ldg(&a.sig_p[n]);
+      x = cdiv(__ldg(&a.in[e]), make_double2(sp.x + __ldg(&a.sig_q[q]) + __ldg(&mu[j]), sp.y));
+    }
+    a.out[e] = x;
+  }
+}
+
 // out[j] = in[j] mu[j] s: an operator diagonal in the DST modes applied to a modal vector
 // (P1-FEM: A v = M^{-1} K v with mu_j = h^2 K_j / M_j, s = 1/h^2)
 __global__ void mode_scale_kernel(double2* out, const double2* in, const double* mu, double s, int L) {

@@ -335,13 +335,9 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (opt && (opt->flags & PINT_FLAG_DST_PER_ITER) && (op->kind != PINT_OP_FD2D_DIRICHLET || nranks != 1))
     return fail(PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator on one rank");
   const int32_t flags = (opt ? opt->flags : 0) | (fem ? PINT_FLAG_MODAL : 0);   // P1-FEM runs modal
-  if (fem && (opt ? opt->alpha : 1.0) != 1.0)
-    return fail(PINT_ERR_UNSUPPORTED, "PINT_OP_FEM1D_DIRICHLET runs on the fully modal heat path (alpha = 1)");
   if (flags & PINT_FLAG_MODAL) {
     const int64_t Lm = op->kind == PINT_OP_FD2D_DIRICHLET ? op->my : op->mx;
-    if ((opt ? opt->alpha : 1.0) != 1.0) return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL needs a heat problem (alpha = 1)");
-    if (flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER))
-      return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL excludes PINT_FLAG_STREAM and PINT_FLAG_DST_PER_ITER");
+    if (flags & PINT_FLAG_DST_PER_ITER) return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL excludes PINT_FLAG_DST_PER_ITER");
     if (!is_pow2(2 * (Lm + 1)) || 2 * (Lm + 1) < 16 || 2 * (Lm + 1) > 4096)
       return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_MODAL needs 2(L+1) a power of two in [16, 4096] (L = my in 2D, mx in 1D)");
   }
@@ -446,6 +442,10 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     p->Lf = (int)(p->NB * p->WB);    // X / partials indexed by the y-mode j < my
     p->NEy = (int)(2 * (L + 1));
   }
+  if (p->modal) {   // DST along the line axis (fused modal kernel, or division pass of the streaming path)
+    if ((st = dalloc(p, &p->twEy, p->NEy)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->mu, (size_t)L)) != PINT_OK) return bail(st);
+  }
   if (p->fused_ok && p->modal) {
     p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
     p->nch = 1;
@@ -453,8 +453,6 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     for (int i = 0; i < 2; ++i)
       if ((st = dalloc(p, &p->X[i], (size_t)p->Qb * 8 * p->Lf)) != PINT_OK) return bail(st);
     if ((st = dalloc(p, &p->Pp, (size_t)p->Qb * k * p->Lf)) != PINT_OK) return bail(st);
-    if ((st = dalloc(p, &p->twEy, p->NEy)) != PINT_OK) return bail(st);
-    if ((st = dalloc(p, &p->mu, (size_t)L)) != PINT_OK) return bail(st);
     for (int i = 0; i < 2; ++i) {
       ce = cudaMemsetAsync(p->X[i], 0, (size_t)p->Qb * 8 * p->Lf * sizeof(double2), p->stream);
       if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(ce)); }
@@ -556,7 +554,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     }
     if ((st = h2d(p, p->twE, twE)) != PINT_OK) return bail(st);
   }
-  if (p->modal && p->fused_ok) {
+  if (p->modal) {
     std::vector<double2> twEy(p->NEy);
     for (int m = 0; m < p->NEy; ++m) {
       const ld ang = 2.0L * PI_L * (ld)m / (ld)p->NEy;
@@ -622,6 +620,17 @@ static pint_status spass(pint_plan p, const double2* in, double2* out) {
   SPassArgs a{};
   a.in = in; a.out = out; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
   a.N = p->N; a.NB = p->NB; a.WB = p->WB; a.L = (int)p->L;
+  if (p->modal) {   // streaming modal path: Step 2 is W = H / (sigma_p + sigma_q + mu_j), elementwise
+    cudaEvent_t m0 = nullptr, m1 = nullptr;
+    if (p->timing) {
+      CUDA_TRY(cudaEventCreate(&m0)); CUDA_TRY(cudaEventCreate(&m1));
+      CUDA_TRY(cudaEventRecord(m0, p->stream));
+    }
+    CUDA_TRY(launch_modal_div(a, p->mu, p->Qb, p->stream));
+    ++p->launches;
+    if (m0) { CUDA_TRY(cudaEventRecord(m1, p->stream)); p->sev.push_back({m0, m1}); }
+    return PINT_OK;
+  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->timing) {
     CUDA_TRY(cudaEventCreate(&e0)); CUDA_TRY(cudaEventCreate(&e1));
@@ -829,7 +838,7 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     if (chk_real) CUDA_TRY(launch_imag_max(p->phys, M, p->upd, p->stream));
     TRY(to_source(p, p->phys, 2 + r));
   }
-  if (p->modal && p->fused_ok) TRY(dst_y(p, p->src, p->src, 1, (long)S * p->Qb));   // sources -> (q, j) modes
+  if (p->modal) TRY(dst_y(p, p->src, p->src, 1, (long)S * p->Qb));   // sources -> (q, j) modes
   if (p->fem) {   // A v = M^{-1} K v is diagonal in the modes: (A v)_j = (mu_j / h^2) v_j (source 1 <- source 0)
     CUDA_TRY(launch_mode_scale(p->src + (size_t)p->ntiles * p->WB, p->src, p->mu, 1.0 / (p->h * p->h), (int)p->L, p->stream));
     ++p->launches;
@@ -1011,7 +1020,7 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
   }
   ++p->launches;
   // H_1 and the wrap state of U_0 from the time-domain array
-  if (p->fused && p->modal) {   // fully modal: the window lives in (q, j) space
+  if (p->modal) {   // fully modal: the iteration lives in (q, j) space
     TRY(dst_y(p, p->A, p->B, p->N, p->Qb));
     TRY(tpass(p, IN_TIME_BUF, OUT_H, p->B, p->A, nullptr, p->wrap[p->wcur], false));
   } else {
@@ -1098,6 +1107,7 @@ static pint_status iterate_async(pint_plan p) {
     return PINT_OK;
   }
   if (p->stateA == 1) {   // A holds U_m (after get_levels): re-derive H_{m+1}
+    if (p->modal) TRY(dst_y(p, p->A, p->A, p->N, p->Qb));   // physical (q, y) -> (q, j) modes
     TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
     p->stateA = 0;
   }
@@ -1329,6 +1339,7 @@ static pint_status materialize(pint_plan p) {
   if (p->fused) TRY(fused_pass(p, p->X[1 - p->xcur], true));
   // U_m = Gamma^{-1} V W_m (Step 3) from B into A (time domain)
   TRY(tpass(p, IN_FREQ, OUT_U, p->B, p->A, nullptr, nullptr, false));
+  if (p->modal) TRY(dst_y(p, p->A, p->A, p->N, p->Qb));   // streaming modal: (q, j) -> (q, y), B keeps W_m
   p->stateA = 1;
   return PINT_OK;
 }
@@ -1355,14 +1366,14 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
     if (!p->wstage) TRY(dalloc(p, &p->wstage, (size_t)p->k * p->M));
     double2* wdst = mem == PINT_DEVICE ? (double2*)U : p->wstage;
     const double2* wsrc = p->wrap[p->wcur];
-    if (p->fused && p->modal) {   // window levels are (q, j)-modal: DST-y back first
+    if (p->modal) {   // window levels are (q, j)-modal: DST-y back first
       if (!p->wtmp) TRY(dalloc(p, &p->wtmp, (size_t)p->ntiles * p->k * p->WB));
       TRY(dst_y(p, p->wrap[p->wcur], p->wtmp, p->k, p->Qb));
       wsrc = p->wtmp;
     }
     if (p->dim == 1) {
       RemapArgs r{};
-      r.in = p->wrap[p->wcur]; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
+      r.in = wsrc; r.out = wdst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
       r.N = p->k; r.n0 = n_begin - (p->N - p->k); r.M = p->M; r.Qb = 1;
       CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
     } else if (p->dst_iter) {

@@ -534,6 +534,10 @@ FEM_CASES = [
     ("fem_1023_bdf4", lambda: inputs.random_complex_problem(1023, 1, 1024, 4, 0.01, 1.0, R=1, seed=11).with_(space="fem"), 3),
     ("fem_example1_bdf3", lambda: inputs.example1_fem(3, M=1023, N=128), 3),
     ("fd_modal_1d_bdf6", lambda: inputs.random_complex_problem(255, 1, 256, 6, 0.05, 1.0, R=1, seed=13), 3),
+    # CQ (streaming path, Step 2 as an elementwise division in the modes)
+    ("fem_cq_a05_bdf2", lambda: inputs.random_complex_problem(127, 1, 128, 2, 0.05, 0.5, R=1, seed=14).with_(space="fem"), 3),
+    ("fem_example2_cq", lambda: inputs.example2_fd(2, M=255, N=256).with_(space="fem"), 3),
+    ("fd_modal_2d_cq", lambda: inputs.random_complex_problem(31, 63, 64, 3, 0.05, 0.3, R=2, seed=15), 3),
 ]
 
 
@@ -546,10 +550,13 @@ def test_fem_and_modal_1d(pint, name, make, iters):
     o = wr.wr_naive(prob, iters, dft="fft")
     kw = {} if prob.space == "fem" else {"modal": True}
     errs = []
+    N, k = prob.N, prob.k
     with pint.Plan.from_problem(prob, **kw) as p:
-        assert p.path()["fused"]
+        assert p.path()["fused"] is (prob.alpha == 1.0)
         for m in range(1, iters + 1):
             p.iterate()
+            win = p.get_levels(N - k, k)          # window levels before materialisation
+            errs.append(float(np.linalg.norm(win - o[m][N - k:]) / np.linalg.norm(o[m])))
             errs.append(rel(p.get_solution(), o[m]))
         it, u, st = p.solve(1e-12, 40)
         seq_err = rel(p.get_solution(), sequential.sequential(prob))
@@ -559,10 +566,6 @@ def test_fem_and_modal_1d(pint, name, make, iters):
 
 
 def test_fem_rejects_unsupported(pint):
-    prob = inputs.random_complex_problem(63, 1, 64, 2, 0.1, 0.5, R=0, seed=1).with_(space="fem")
-    with pytest.raises(pint.PintError) as e:
-        pint.Plan.from_problem(prob)
-    assert e.value.status == pint.PINT_ERR_UNSUPPORTED
     prob = inputs.random_complex_problem(62, 1, 64, 2, 0.1, 1.0, R=0, seed=1).with_(space="fem")   # 2(mx+1) = 126
     with pytest.raises(pint.PintError) as e:
         pint.Plan.from_problem(prob)
