@@ -32,6 +32,21 @@ cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStre
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_tpass_cq_split(int N, int half, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  switch (N) {
+    case 16: return launch_tpass_cq_split_16(half, a, ntiles, st);
+    case 32: return launch_tpass_cq_split_32(half, a, ntiles, st);
+    case 64: return launch_tpass_cq_split_64(half, a, ntiles, st);
+    case 128: return launch_tpass_cq_split_128(half, a, ntiles, st);
+    case 256: return launch_tpass_cq_split_256(half, a, ntiles, st);
+    case 512: return launch_tpass_cq_split_512(half, a, ntiles, st);
+    case 1024: return launch_tpass_cq_split_1024(half, a, ntiles, st);
+    case 2048: return launch_tpass_cq_split_2048(half, a, ntiles, st);
+    case 4096: return launch_tpass_cq_split_4096(half, a, ntiles, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st) {
   switch (NE) {
     case 16: return launch_dst_16(a, mode, st);

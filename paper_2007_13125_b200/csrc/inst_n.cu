@@ -47,6 +47,22 @@ static cudaError_t go_pruned(const TPassArgs& a, long ntiles, cudaStream_t st) {
 }
 #endif
 
+template <bool B>
+static cudaError_t go_cq_split(const TPassArgs& a, long ntiles, cudaStream_t st) {
+  auto kern = B ? tpass_cq_b_kernel<PINT_N> : tpass_cq_a_kernel<PINT_N>;
+  const int smem = phys_size(TILE) * (int)sizeof(double2);
+  static const long resident = persistent_grid((const void*)kern, smem);
+  if (resident <= 0) return cudaErrorInvalidValue;
+  if (ntiles <= 0) return cudaSuccess;
+  const long grid = ntiles < resident ? ntiles : resident;
+  kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
+  return cudaGetLastError();
+}
+
+cudaError_t PINT_CAT(launch_tpass_cq_split_, PINT_N)(int half, const TPassArgs& a, long ntiles, cudaStream_t st) {
+  return half ? go_cq_split<true>(a, ntiles, st) : go_cq_split<false>(a, ntiles, st);
+}
+
 cudaError_t PINT_CAT(launch_tpass_pruned_, PINT_N)(const TPassArgs& a, long ntiles, cudaStream_t st) {
 #if PINT_N >= 256
   return a.ndense > 0 ? go_pruned<true>(a, ntiles, st) : go_pruned<false>(a, ntiles, st);

@@ -16,6 +16,8 @@ cudaError_t launch_tpass(int N, int mode_in, int mode_out, bool cq, const TPassA
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st);
 // pruned heat T-pass (FREQ -> H), N in {512, 1024, 2048, 4096}
 cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st);
+// CQ FREQ -> H as two kernels (half 0: W -> Z, half 1: Z, W -> H; tpass.cuh)
+cudaError_t launch_tpass_cq_split(int N, int half, const TPassArgs& a, long ntiles, cudaStream_t st);
 // layout remaps and the FD stencil (dispatch.cu)
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);
@@ -50,7 +52,8 @@ cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double*
   cudaError_t launch_tpass_##NN(int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, \
                                 cudaStream_t st);                                                  \
   cudaError_t launch_dst_##NN(const DstArgs& a, int mode, cudaStream_t st);                    \
-  cudaError_t launch_tpass_pruned_##NN(const TPassArgs& a, long ntiles, cudaStream_t st);
+  cudaError_t launch_tpass_pruned_##NN(const TPassArgs& a, long ntiles, cudaStream_t st);        \
+  cudaError_t launch_tpass_cq_split_##NN(int half, const TPassArgs& a, long ntiles, cudaStream_t st);
 PINT_DECLARE_N(16)
 PINT_DECLARE_N(32)
 PINT_DECLARE_N(64)

@@ -153,6 +153,7 @@ struct pint_plan_s {
   int nsparse = 0, ndense = 0;
   int* srclist = nullptr;     // [S]: sparse sources, then dense sources
   double2* chat = nullptr;    // [S][N] DFTs of dense coefficient sequences
+  double2* cqhat = nullptr;   // [S][N] CQ split T-pass: DFTs of Gamma h^2/N c_s(n) for every source
   double2 *tw = nullptr, *twE = nullptr;
   double *gsf = nullptr, *igs = nullptr, *gsN = nullptr, *wk = nullptr;
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
@@ -251,6 +252,27 @@ static pint_status h2d(pint_plan p, T* dst, const std::vector<T>& v) {
 }
 
 static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
+
+// in-place radix-2 DFT in long double (host plan tables): x_p <- sum_n x_n e^{sign 2 pi i n p / N}
+static void fft_ld(std::vector<cld>& x, int sign) {
+  const size_t N = x.size();
+  for (size_t i = 1, j = 0; i < N; ++i) {   // bit reversal
+    size_t bit = N >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(x[i], x[j]);
+  }
+  for (size_t len = 2; len <= N; len <<= 1) {
+    for (size_t i = 0; i < N; i += len)
+      for (size_t m = 0; m < len / 2; ++m) {
+        const long double ang = (long double)sign * 2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)len;
+        const cld w(cosl(ang), sinl(ang));
+        const cld u = x[i + m], v = x[i + m + len / 2] * w;
+        x[i + m] = u + v;
+        x[i + m + len / 2] = u - v;
+      }
+  }
+}
 
 static pint_status valloc(pint_plan p, double2** ptr, size_t count, int comp) {
   VmmApi& v = vmm();
@@ -609,8 +631,18 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
   }
   const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 256 &&
                       p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT) && !p->has_fd;
+  // CQ iteration: two kernels of two transforms each (tpass.cuh "CQ T-pass split"); PINT_CQ_MONO=1
+  // keeps the single four-transform kernel (A/B)
+  static const bool mono = getenv("PINT_CQ_MONO") != nullptr;
+  const bool split = !mono && p->alpha != 1.0 && mode_in == IN_FREQ && mode_out == OUT_H && !a.fdense && in != out;
   if (pruned) CUDA_TRY(launch_tpass_pruned((int)p->N, a, p->ntiles, p->stream));
-  else CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
+  else if (split) {
+    CUDA_TRY(launch_tpass_cq_split((int)p->N, 0, a, p->ntiles, p->stream));      // W -> Z (into out)
+    TPassArgs b = a;
+    b.in = out; b.vsrc = in; b.chat = p->cqhat;                                   // Z, W -> H
+    CUDA_TRY(launch_tpass_cq_split((int)p->N, 1, b, p->ntiles, p->stream));
+    ++p->launches;
+  } else CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
   ++p->launches;
   if (e0) { CUDA_TRY(cudaEventRecord(e1, p->stream)); p->tev.push_back({e0, e1}); }
   return PINT_OK;
@@ -820,6 +852,7 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     TRY(dalloc(p, &p->nhi, S));
     TRY(dalloc(p, &p->srclist, S));
     TRY(dalloc(p, &p->chat, (size_t)S * N));
+    if (p->alpha != 1.0) TRY(dalloc(p, &p->cqhat, (size_t)S * N));
     p->S = S;
   }
   CUDA_TRY(cudaMemsetAsync(p->src, 0, (size_t)S * p->ntiles * p->WB * sizeof(double2), p->stream));
@@ -915,6 +948,20 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     p->fused = p->fused_ok && nk <= 8;
     TRY(h2d(p, p->srclist, lst));
     if (!ch.empty()) TRY(h2d(p, p->chat, ch));
+  }
+  if (p->cqhat) {
+    // CQ split T-pass: H_static = V^{-1} Gamma F_static h^2/N is iteration-invariant and separable,
+    // H_static[p] = sum_s chat_s[p] src_s with chat_s the DFT of kappa^{n/N} h^2/N c_s(n): long
+    // double, radix-2 FFT (N a power of two), once per problem
+    const ld hl = 1.0L / (ld)(p->L + 1), Nl = (ld)N;
+    std::vector<double2> ch((size_t)S * N);
+    std::vector<cld> x(N);
+    for (int s = 0; s < S; ++s) {
+      for (int64_t n = 0; n < N; ++n) x[n] = (ld)coef[(size_t)s * N + n] * powl((ld)p->kappa, (ld)n / Nl) * hl * hl / Nl;
+      fft_ld(x, -1);
+      for (int64_t pp = 0; pp < N; ++pp) ch[(size_t)s * N + pp] = d2(x[pp]);
+    }
+    TRY(h2d(p, p->cqhat, ch));
   }
   TRY(h2d(p, p->coef, coef));
   TRY(h2d(p, p->nhi, nhi));

@@ -327,6 +327,113 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CQ T-pass split in two kernels of two transforms each (mode FREQ -> H, no dense RHS).  The
+// monolithic kernel above holds a tile through four transforms and the table applications and
+// spills at the 128-register bound; each half below has the register shape of the heat T-pass.
+// The product Z = D' V^{-1} Theta V W (frequency domain) goes through the H buffer:
+//   A: W --V--> u --(window, monitor)--> Theta u --V^{-1}--> D' z = Z            (out = H buffer)
+//   B: Z --V--> s; X = Gamma F_static h^2/N - (h^2/(2 N tau^a)) Theta^{-1} s --V^{-1}--> + D W = H
+// HBM: A reads W, writes Z; B reads Z and W, writes H: 80 B/unknown instead of 32.
+// ---------------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_cq_a_kernel(const TPassArgs a, long ntiles) {
+  using TM = TimeMap<N>;
+  using FM = FreqMap<N>;
+  constexpr int WB = TILE / N;
+  extern __shared__ double2 sm[];
+  const int k = a.k;
+  double upd = 0.0;
+  bool nonfinite = false;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    const long base = tile * (long)TILE;
+    if (a.prefetch) {
+      const long nt = tile + gridDim.x;
+      if (tid < 4 && nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
+    }
+    double2 v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
+    run_passes<N, +1, false>(v, sm, a.tw, tid);          // u = V W
+    // window levels of U_m = Gamma^{-1} u: monitor and new wrap state
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s2 = 0; s2 < TM::RL; ++s2) {
+        const int n = TM::n(j, s2, tid);
+        if ((s2 == TM::RL - 1 || TM::PL < 8) && n >= N - k) {
+          const double2 U = cscale(v[j * TM::RL + s2], __ldg(&a.igs[n]));
+          const long wi = (tile * k + (n - (N - k))) * WB + TM::c(j, tid);
+          const double d = sqrt(cabs2(csub(U, a.wrap_old[wi])));
+          if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+          upd = fmax(upd, d);
+          a.wrap_new[wi] = U;
+        }
+      }
+    // Z = D' V^{-1} Theta u
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s2 = 0; s2 < TM::RL; ++s2) v[j * TM::RL + s2] = cmul(v[j * TM::RL + s2], __ldg(&a.thp[TM::n(j, s2, tid)]));
+    run_passes<N, -1, true>(v, sm, a.tw, tid);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) a.out[base + FM::e(t, tid)] = cmul(v[t], __ldg(&a.dpr[FM::p(t, tid)]));
+    __syncthreads();   // smem reused by the next tile
+  }
+  if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
+  block_max_atomic(upd, a.upd);
+}
+
+// a.in = Z (may alias a.out), a.vsrc = W, a.chat = [S][N] spectra of the static sources:
+// H = V^{-1}(-(h^2/(2 N tau^a)) Theta^{-1} V Z) + sum_s chat_s[p] src_s + D W
+template <int N>
+__global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_cq_b_kernel(const TPassArgs a, long ntiles) {
+  using TM = TimeMap<N>;
+  using FM = FreqMap<N>;
+  constexpr int WB = TILE / N;
+  static_assert(TPB % WB == 0, "fixed column per thread");
+  extern __shared__ double2 sm[];
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    const long base = tile * (long)TILE;
+    // L2 bulk prefetch: the next tile's Z, and this tile's W (read only after both transforms)
+    if (tid < 4) {
+      const long nt = tile + gridDim.x;
+      if (nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
+    } else if (tid < 8) {
+      prefetch_l2_t(a.vsrc + base + (tid - 4) * (TILE / 4), TILE / 4 * 16);
+    }
+    double2 v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
+    run_passes<N, +1, false>(v, sm, a.tw, tid);          // s = V Z
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s2 = 0; s2 < TM::RL; ++s2) v[j * TM::RL + s2] = cmul(v[j * TM::RL + s2], __ldg(&a.thm[TM::n(j, s2, tid)]));
+    run_passes<N, -1, true>(v, sm, a.tw, tid);
+    const int cc = tid % WB;
+    double2 sv[CQ_SV];
+#pragma unroll
+    for (int q = 0; q < CQ_SV; ++q) sv[q] = q < a.S ? __ldg(&a.src[(long)q * ntiles * WB + tile * WB + cc]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int p = FM::p(t, tid);
+      double2 h = cfma(a.vsrc[base + FM::e(t, tid)], __ldg(&a.dh[p]), v[t]);
+#pragma unroll
+      for (int q = 0; q < CQ_SV; ++q)
+        if (q < a.S) h = cfma(__ldg(&a.chat[(long)q * N + p]), sv[q], h);
+      for (int q = CQ_SV; q < a.S; ++q)
+        h = cfma(__ldg(&a.chat[(long)q * N + p]), __ldg(&a.src[(long)q * ntiles * WB + tile * WB + cc]), h);
+      a.out[base + FM::e(t, tid)] = h;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace pint
 
 namespace pint {
