@@ -109,6 +109,9 @@ constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 #ifndef PINT_FUSED_NS
 #define PINT_FUSED_NS 4
 #endif
+#ifndef PINT_TM_BATCH
+#define PINT_TM_BATCH 4   // rows per TMEM load batch in the window phase
+#endif
 template <int LANES> struct FCfg {
   static constexpr int THREADS = FG * LANES;
   static constexpr int NSMAX = LANES == 32 ? PINT_FUSED_NS : 2;
@@ -381,13 +384,17 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
       tww[t] = w;
     }
     if constexpr (TM) {
-      uint32_t w[RPT][24];                               // slots r = 2..7 of each row: one TMEM round trip
-#pragma unroll
-      for (int rr = 0; rr < RPT; ++rr)
-        if (!(LF < T && threadIdx.x + T * rr >= LF)) tmem_ld24_async(tacc + 24 * rr, w[rr]);
-      tmem_wait_ld();
+      // slots r = 2..7 of each row; TMEM loads in batches of TMB rows (one round trip per batch)
+      constexpr int TMB = PINT_TM_BATCH < RPT ? PINT_TM_BATCH : RPT;
+      uint32_t w[RPT][24];
 #pragma unroll
       for (int rr = 0; rr < RPT; ++rr) {
+        if (rr % TMB == 0) {
+#pragma unroll
+          for (int b = rr; b < rr + TMB && b < RPT; ++b)
+            if (!(LF < T && threadIdx.x + T * b >= LF)) tmem_ld24_async(tacc + 24 * b, w[b]);
+          tmem_wait_ld();
+        }
         const int y = threadIdx.x + T * rr;
         if (LF < T && y >= LF) break;                    // warp-uniform (LF % 32 == 0)
         double2 x[8];

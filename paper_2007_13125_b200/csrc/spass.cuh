@@ -379,8 +379,11 @@ __global__ void __launch_bounds__(128, 3) spass_direct_kernel(const SPassArgs a)
 // per-thread registers (more resident warps) relative to one warp per line.
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
+#ifndef PINT_PAIR_MINB
+#define PINT_PAIR_MINB 4
+#endif
 template <int C>
-__global__ void __launch_bounds__(128, 4) spass_pair_kernel(const SPassArgs a) {
+__global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const SPassArgs a) {
   __shared__ double2 xch[2][4];                      // per pair: fwd total, bwd total, w0, spare
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const int pair = warp >> 1, half = warp & 1;
