@@ -47,16 +47,22 @@ def test_status_strings_and_kappa_rule():
     (dict(mx=100, my=10), P.PINT_ERR_UNSUPPORTED, "2(mx+1)"),
     (dict(nranks=2, rank=0), P.PINT_ERR_ARG, "1D operators do not shard"),
     (dict(dst_per_iter=True), P.PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator"),
+    (dict(fem=True, mx=63, my=3), P.PINT_ERR_ARG, "1D operator needs my == 1"),
+    (dict(fem=True, mx=62), P.PINT_ERR_UNSUPPORTED, "2(L+1) a power of two"),
+    (dict(modal=True, mx=62), P.PINT_ERR_UNSUPPORTED, "2(L+1) a power of two"),
+    (dict(modal=True, mx=63, my=63, dst_per_iter=True), P.PINT_ERR_ARG, "PINT_FLAG_MODAL excludes"),
+    (dict(fem=True, nranks=2, rank=1), P.PINT_ERR_ARG, "1D operators do not shard"),
 ])
 def test_create_rejects(kw, status, needle):
     a = dict(mx=63, my=1, N=64, k=2, kappa=0.1, tau=1 / 64, alpha=1.0)
     nr = kw.pop("nranks", 1)
     rk = kw.pop("rank", 0)
     dpi = kw.pop("dst_per_iter", False)
+    modal, fem = kw.pop("modal", False), kw.pop("fem", False)
     a.update(kw)
     with pytest.raises(P.PintError) as e:
         P.Plan(a["mx"], a["my"], a["N"], a["k"], a["kappa"], a["tau"], a["alpha"], rank=rk, nranks=nr,
-               dst_per_iter=dpi)
+               dst_per_iter=dpi, modal=modal, fem=fem)
     assert e.value.status == status
     assert needle in str(e.value)
 
