@@ -382,32 +382,12 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 #ifndef PINT_PAIR_MINB
 #define PINT_PAIR_MINB 4
 #endif
-template <int C>
-__global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const SPassArgs a) {
-  __shared__ double2 xch[2][4];                      // per pair: fwd total, bwd total, w0, spare
-  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  const int pair = warp >> 1, half = warp & 1;
-  const long line = (long)blockIdx.x * 2 + pair;
-  const long N = a.N, NB = a.NB;
-  const bool live = line < a.nwork;
-  const long q = live ? line / N : 0, p = live ? line - q * N : 0;
-  const int WB = a.WB, lwb = a.lwb, L = a.L;
-  const int Lpad = (int)NB * WB;
-  const int gl = half * 32 + lane;
-  const double2* in = a.in + (q * NB * N + p) * WB;
-  double2 d[C];
-#pragma unroll
-  for (int r = 0; r < C; r += 2) {
-    const int y = gl * C + r;
-    if (live && y < Lpad) ld256(in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
-    else { d[r] = make_double2(0.0, 0.0); d[r + 1] = d[r]; }
-  }
-  const double2 sp = live ? __ldg(&a.sig_p[p]) : make_double2(1.0, 0.0);
-  const double2 sig = make_double2(sp.x + (live ? __ldg(&a.sig_q[q]) : 0.0), sp.y);
-  const int nv = min(max(L - gl * C, 0), C);
-#pragma unroll
-  for (int r = 0; r < C; ++r) if (r >= nv) d[r] = make_double2(0.0, 0.0);
 
+// The pair solve: lane gl = 32 half + lane of the pair owns rows [gl C, gl C + C) in d (rows >= L
+// zero on entry); on exit d holds the solution rows (zero beyond L).  xch: the pair's exchange slots.
+template <int C>
+__device__ __forceinline__ void pair_solve(double2 (&d)[C], double2 sig, int L, int lane, int half, int gl, int nv,
+                                           double2* xch, int pair) {
   // ---- line setup (as in solve_line_regs) ----
   const double2 s2 = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
   const double2 t1 = cscale(cadd(sig, s2), 0.5), t2 = cscale(csub(sig, s2), 0.5);
@@ -443,13 +423,13 @@ __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const S
     x.y = __shfl_up_sync(0xffffffffu, f.y, o);
     if (lane >= o) f = cadd(f, amul(uc[i], x));
   }
-  if (half == 0 && lane == 31) xch[pair][0] = f;     // warp-0 total (inclusive at its last row)
+  if (half == 0 && lane == 31) xch[0] = f;     // warp-0 total (inclusive at its last row)
   pair_bar(1 + pair);
-  if (half == 1) f = cadd(f, amul(ufw, xch[pair][0]));
+  if (half == 1) f = cadd(f, amul(ufw, xch[0]));
   double2 carry;
   carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
   carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
-  if (lane == 0) carry = half ? xch[pair][0] : make_double2(0.0, 0.0);
+  if (lane == 0) carry = half ? xch[0] : make_double2(0.0, 0.0);
   f = carry;
 #pragma unroll
   for (int r = 0; r < C; ++r) {
@@ -468,12 +448,12 @@ __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const S
     x.y = __shfl_down_sync(0xffffffffu, w.y, o);
     if (lane + o < 32) w = cadd(w, amul(uc[i], x));
   }
-  if (half == 1 && lane == 0) xch[pair][1] = w;      // warp-1 total (suffix from its first row)
+  if (half == 1 && lane == 0) xch[1] = w;      // warp-1 total (suffix from its first row)
   pair_bar(1 + pair);
-  if (half == 0) w = cadd(w, amul(ubw, xch[pair][1]));
+  if (half == 0) w = cadd(w, amul(ubw, xch[1]));
   carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
   carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
-  if (lane == 31) carry = half ? make_double2(0.0, 0.0) : xch[pair][1];
+  if (lane == 31) carry = half ? make_double2(0.0, 0.0) : xch[1];
   w = carry;
 #pragma unroll
   for (int r = C - 1; r >= 0; --r) {
@@ -481,9 +461,9 @@ __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const S
     d[r] = w;
   }
   // ---- rank-1 Dirichlet correction ----
-  if (half == 0 && lane == 0) xch[pair][2] = d[0];
+  if (half == 0 && lane == 0) xch[2] = d[0];
   pair_bar(1 + pair);
-  const double2 w0 = xch[pair][2];
+  const double2 w0 = xch[2];
   const double2 u2L = upow(u, 2L * L + 2);
   const double2 K = cdiv(w0, u2L);
   const int y0 = gl * C;
@@ -506,13 +486,41 @@ __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const S
       for (int r = 0; r < C; ++r) { d[r] = cadd(d[r], KQ); KQ = cmul(KQ, rr); }
     }
   }
+#pragma unroll
+  for (int r = 0; r < C; ++r) d[r] = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+}
+
+template <int C>
+__global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const SPassArgs a) {
+  __shared__ double2 xch[2][4];                      // per pair: fwd total, bwd total, w0, spare
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int pair = warp >> 1, half = warp & 1;
+  const long line = (long)blockIdx.x * 2 + pair;
+  const long N = a.N, NB = a.NB;
+  const bool live = line < a.nwork;
+  const long q = live ? line / N : 0, p = live ? line - q * N : 0;
+  const int WB = a.WB, lwb = a.lwb, L = a.L;
+  const int Lpad = (int)NB * WB;
+  const int gl = half * 32 + lane;
+  const double2* in = a.in + (q * NB * N + p) * WB;
+  double2 d[C];
+#pragma unroll
+  for (int r = 0; r < C; r += 2) {
+    const int y = gl * C + r;
+    if (live && y < Lpad) ld256(in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
+    else { d[r] = make_double2(0.0, 0.0); d[r + 1] = d[r]; }
+  }
+  const double2 sp = live ? __ldg(&a.sig_p[p]) : make_double2(1.0, 0.0);
+  const double2 sig = make_double2(sp.x + (live ? __ldg(&a.sig_q[q]) : 0.0), sp.y);
+  const int nv = min(max(L - gl * C, 0), C);
+#pragma unroll
+  for (int r = 0; r < C; ++r) if (r >= nv) d[r] = make_double2(0.0, 0.0);
+  pair_solve<C>(d, sig, L, lane, half, gl, nv, xch[pair], pair);
   double2* out = a.out + (q * NB * N + p) * WB;
 #pragma unroll
   for (int r = 0; r < C; r += 2) {
     const int y = gl * C + r;
-    const double2 x0 = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
-    const double2 x1 = (r + 1 < nv) ? amul(u, d[r + 1]) : make_double2(0.0, 0.0);
-    if (live && y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), x0, x1);
+    if (live && y < Lpad) st256(out + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
   }
 }
 
