@@ -25,7 +25,8 @@ template <int C, int LANES, bool SW, bool TM>
 static cudaError_t fused_go(const FusedArgs& a, long grid, cudaStream_t st) {
   FusedKern kern = wr_fused_kernel<C, LANES, SW, TM>;
   if constexpr (TM && !SW) kern = a.half ? fused_pick<C, LANES, true>(a.nk) : fused_pick<C, LANES, false>(a.nk);
-  const size_t smem = fused_smem_bytes(LANES, C, a.k, TM && !SW) + (a.xs ? (size_t)a.nk * LANES * C * sizeof(double2) : 0);
+  // X staged in shared memory only by the shared-memory-window variant (the TMEM kernels keep X in TMEM)
+  const size_t smem = fused_smem_bytes(LANES, C, a.k, TM && !SW) + ((a.xs && !(TM && !SW)) ? (size_t)a.nk * LANES * C * sizeof(double2) : 0);
   // set on every launch: the occupancy query at plan creation (fused_occ) also sets this attribute
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

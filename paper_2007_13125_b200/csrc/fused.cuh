@@ -345,6 +345,51 @@ __device__ __forceinline__ void tmem_st24(uint32_t addr, const uint32_t (&w)[24]
                   "r"(w[23]) : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// NW (16, 24 or 32) columns of this thread's TMEM lane, in chunks of 16 and 8 (X levels, 4 per level)
+template <int O, int NW> __device__ __forceinline__ void tmem_ld16_at(uint32_t addr, uint32_t (&w)[NW]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+               : "=r"(w[O + 0]), "=r"(w[O + 1]), "=r"(w[O + 2]), "=r"(w[O + 3]), "=r"(w[O + 4]), "=r"(w[O + 5]),
+                 "=r"(w[O + 6]), "=r"(w[O + 7]), "=r"(w[O + 8]), "=r"(w[O + 9]), "=r"(w[O + 10]), "=r"(w[O + 11]),
+                 "=r"(w[O + 12]), "=r"(w[O + 13]), "=r"(w[O + 14]), "=r"(w[O + 15])
+               : "r"(addr + O));
+}
+template <int O, int NW> __device__ __forceinline__ void tmem_ld8_at(uint32_t addr, uint32_t (&w)[NW]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(w[O + 0]), "=r"(w[O + 1]), "=r"(w[O + 2]), "=r"(w[O + 3]), "=r"(w[O + 4]), "=r"(w[O + 5]),
+                 "=r"(w[O + 6]), "=r"(w[O + 7])
+               : "r"(addr + O));
+}
+template <int O, int NW> __device__ __forceinline__ void tmem_st16_at(uint32_t addr, const uint32_t (&w)[NW]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+               :: "r"(addr + O), "r"(w[O + 0]), "r"(w[O + 1]), "r"(w[O + 2]), "r"(w[O + 3]), "r"(w[O + 4]),
+                  "r"(w[O + 5]), "r"(w[O + 6]), "r"(w[O + 7]), "r"(w[O + 8]), "r"(w[O + 9]), "r"(w[O + 10]),
+                  "r"(w[O + 11]), "r"(w[O + 12]), "r"(w[O + 13]), "r"(w[O + 14]), "r"(w[O + 15]) : "memory");
+}
+template <int O, int NW> __device__ __forceinline__ void tmem_st8_at(uint32_t addr, const uint32_t (&w)[NW]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+               :: "r"(addr + O), "r"(w[O + 0]), "r"(w[O + 1]), "r"(w[O + 2]), "r"(w[O + 3]), "r"(w[O + 4]),
+                  "r"(w[O + 5]), "r"(w[O + 6]), "r"(w[O + 7]) : "memory");
+}
+template <int NW> __device__ __forceinline__ void tmem_ldn_async(uint32_t addr, uint32_t (&w)[NW]) {
+  static_assert(NW == 16 || NW == 24 || NW == 32, "16, 24 or 32 columns");
+  tmem_ld16_at<0>(addr, w);
+  if constexpr (NW == 24) tmem_ld8_at<16>(addr, w);
+  if constexpr (NW == 32) tmem_ld16_at<16>(addr, w);
+}
+template <int NW> __device__ __forceinline__ void tmem_stn(uint32_t addr, const uint32_t (&w)[NW]) {
+  static_assert(NW == 16 || NW == 24 || NW == 32, "16, 24 or 32 columns");
+  tmem_st16_at<0>(addr, w);
+  if constexpr (NW == 24) tmem_st8_at<16>(addr, w);
+  if constexpr (NW == 32) tmem_st16_at<16>(addr, w);
+}
+template <int NW> __device__ __forceinline__ double2 tw_getn(const uint32_t (&w)[NW], int s) {
+  return make_double2(__hiloint2double((int)w[4 * s + 1], (int)w[4 * s]), __hiloint2double((int)w[4 * s + 3], (int)w[4 * s + 2]));
+}
+template <int NW> __device__ __forceinline__ void tw_putn(uint32_t (&w)[NW], int s, double2 v) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(v.x), b = (unsigned long long)__double_as_longlong(v.y);
+  w[4 * s] = (uint32_t)a; w[4 * s + 1] = (uint32_t)(a >> 32); w[4 * s + 2] = (uint32_t)b; w[4 * s + 3] = (uint32_t)(b >> 32);
+}
 __device__ __forceinline__ double2 tw_get(const uint32_t (&w)[24], int s) {
   return make_double2(__hiloint2double((int)w[4 * s + 1], (int)w[4 * s]), __hiloint2double((int)w[4 * s + 3], (int)w[4 * s + 2]));
 }
@@ -364,9 +409,10 @@ __device__ __forceinline__ double2 wcontrib(double2 Y, double2 w, int half, doub
 // Row phase between two solves, thread per row (rows y = tid + THREADS r): all X loads of the
 // next synthesis and the group's twiddles are issued first (one memory round trip), then each row
 // reduces group i into the window (Step 3) and synthesises group i + 1 in place (Step 1).
-template <int C, int LANES, bool WINDOW, bool TM = false, bool HALF = false, int NKC = 8>
+// XT: X of this x-mode read from tensor memory (txs: this thread's X columns, 4 NKC per row)
+template <int C, int LANES, bool WINDOW, bool TM = false, bool HALF = false, int NKC = 8, bool XT = false>
 __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, double2* acc, const double2* Xq,
-                                           long q, int i, bool next, uint32_t tacc = 0) {
+                                           long q, int i, bool next, uint32_t tacc = 0, uint32_t txs = 0) {
   constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
   constexpr int RPT = LF >= T ? LF / T : 1;
   const int N = (int)a.N, k = a.k, nk = a.nk;
@@ -430,12 +476,25 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
   // ---- Step 1 (synthesis of group i + 1) in place ----
   if (next && !(a.dbg & 4)) {
     double2 xv[RPT][8];
+    if constexpr (XT) {
+      constexpr int XC = 4 * NKC;
+      uint32_t xw[RPT][XC];
 #pragma unroll
-    for (int rr = 0; rr < RPT; ++rr) {
-      const int y = threadIdx.x + T * rr;
+      for (int rr = 0; rr < RPT; ++rr)
+        if (!(LF < T && threadIdx.x + T * rr >= LF)) tmem_ldn_async<XC>(txs + XC * rr, xw[rr]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        xv[rr][t] = (t < NKC && t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
+      for (int rr = 0; rr < RPT; ++rr)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) xv[rr][t] = t < NKC ? tw_getn<XC>(xw[rr], t) : make_double2(0.0, 0.0);
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int y = threadIdx.x + T * rr;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          xv[rr][t] = (t < NKC && t < nk && y < LF) ? Xq[t * LF + y] : make_double2(0.0, 0.0);
+      }
     }
     double2 tws[8];
 #pragma unroll
@@ -497,10 +556,13 @@ static_assert(sizeof(FinishArgs) == 144, "FinishArgs must stay padding-free");
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
 
-template <int C, int LANES> struct FTmem {
+// TMEM columns per lane quadrant: the window sums (24 per row) and X (4 NKC per row) of the
+// (T / 128) threads sharing the quadrant
+template <int C, int LANES, int NKC = 8> struct FTmem {
   static constexpr int LF = LANES * C, T = FCfg<LANES>::THREADS;
   static constexpr int RPT = LF >= T ? LF / T : 1;
-  static constexpr int NEED = (T / 128) * RPT * 24;          // columns
+  static constexpr int WCOLS = (T / 128) * RPT * 24;
+  static constexpr int NEED = WCOLS + (T / 128) * RPT * 4 * NKC;   // columns
   static constexpr int COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
 };
 
@@ -528,29 +590,41 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
   const int line = LANES == 64 ? warp >> 1 : warp, half = LANES == 64 ? warp & 1 : 0;
   const double2* Xg = a.X + q * 8 * LF;
   const double2* Xq = Xg;
-  if (a.xs) {   // X is the same for every frequency group of this x-mode: stage it once
+  if (!TMA && a.xs) {   // X is the same for every frequency group of this x-mode: stage it once
     for (int e = threadIdx.x; e < a.nk * LF; e += FCfg<LANES>::THREADS) cp_async16(&Xs[e], &Xg[e]);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     cp_async_wait0();
     __syncthreads();
     Xq = Xs;
   }
-  uint32_t tacc = 0;
+  uint32_t tacc = 0, txs = 0;
   if constexpr (TMA) {
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
-                   :: "r"((uint32_t)__cvta_generic_to_shared(&tbase)), "n"(FTmem<C, LANES>::COLS) : "memory");
+                   :: "r"((uint32_t)__cvta_generic_to_shared(&tbase)), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * FTmem<C, LANES>::RPT * 24);
+    tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * FTmem<C, LANES, NKC>::RPT * 24);
     uint32_t z[24];
 #pragma unroll
     for (int j = 0; j < 24; ++j) z[j] = 0u;
 #pragma unroll
-    for (int rr = 0; rr < FTmem<C, LANES>::RPT; ++rr) tmem_st24(tacc + 24 * rr, z);
+    for (int rr = 0; rr < FTmem<C, LANES, NKC>::RPT; ++rr) tmem_st24(tacc + 24 * rr, z);
+    // X of this x-mode (the same for every frequency group) into this thread's TMEM columns
+    constexpr int XC = 4 * NKC, RPTX = FTmem<C, LANES, NKC>::RPT;
+    txs = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)FTmem<C, LANES, NKC>::WCOLS + (uint32_t)((warp >> 2) * RPTX * XC);
+#pragma unroll
+    for (int rr = 0; rr < RPTX; ++rr) {
+      const int y = threadIdx.x + FCfg<LANES>::THREADS * rr;
+      if (LF < FCfg<LANES>::THREADS && y >= LF) break;          // warp-uniform
+      uint32_t xw[XC];
+#pragma unroll
+      for (int t = 0; t < NKC; ++t) tw_putn<XC>(xw, t, Xg[t * LF + y]);
+      tmem_stn<XC>(txs + XC * rr, xw);
+    }
     tmem_wait_st();
   }
   fused_stage_lc(a, slc, q, g0);
@@ -580,7 +654,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     PINT_TS(t2);
     const bool next = i + 1 < g1;
     if (next) fused_stage_lc(a, slc, q, i + 1);
-    fused_rows<C, LANES, !STORE_W, TMA, HALF, NKC>(a, Hs, acc, Xq, q, i, next, tacc);
+    fused_rows<C, LANES, !STORE_W, TMA, HALF, NKC, TMA>(a, Hs, acc, Xq, q, i, next, tacc, txs);
     if constexpr (TMA) tmem_wait_st();
     cp_async_wait0();
     PINT_TS(t3);
@@ -603,7 +677,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
     double2* P = a.P + ((q * a.nch + ch) * a.k) * LF;
     if constexpr (TMA) {
 #pragma unroll
-      for (int rr = 0; rr < FTmem<C, LANES>::RPT; ++rr) {
+      for (int rr = 0; rr < FTmem<C, LANES, NKC>::RPT; ++rr) {
         const int y = threadIdx.x + FCfg<LANES>::THREADS * rr;
         if (LF < FCfg<LANES>::THREADS && y >= LF) break;          // warp-uniform (LF % 32 == 0)
         uint32_t w[24];
@@ -618,7 +692,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const
       __syncthreads();
       if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n"
-                     :: "r"(tbase), "n"(FTmem<C, LANES>::COLS) : "memory");
+                     :: "r"(tbase), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
     } else {
       for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
         for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
