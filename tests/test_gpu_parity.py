@@ -123,6 +123,34 @@ def test_c4_modal_sampled(pint):
             assert worst < TOL, (m, worst)
 
 
+def test_c5_full_size_modal_sampled(pint):
+    """C5 at full size (511^2 x 1024, CQ-BDF2, alpha = 0.5, the bench configuration): the GPU
+    iterate projected on a sample of 7 x 7 sine modes (exact DST projections; the FD sine modes are
+    exact eigenvectors, so each mode coefficient follows the scalar WR of the per-mode oracle O4)
+    at sampled levels, m = 1..3.  Metric: relative L2 over the sampled (mode, level) set."""
+    prob = inputs.config_c5()
+    m = prob.mx
+    modes = np.array([1, 2, 3, 7, 50, 255, 511])
+    basis = modal.ModalBasis(m, m, modes, modes)
+    Sx, Sy = basis.synth_x(), basis.synth_y()
+    sc = (2.0 / (m + 1)) ** 2
+
+    def project(u):                      # [M] grid -> [q][p] coefficients, layout of the basis
+        return (sc * (Sy.T @ u.reshape(m, m) @ Sx)).reshape(-1)
+
+    iters = 3
+    md = modal.modal_wr(prob, basis, project(prob.v), np.zeros((0, modes.size ** 2)), iters)
+    levels = [0, 1, 2, 100, 511, 1022, 1023]
+    with pint.Plan.from_problem(prob) as p:
+        for it in range(1, iters + 1):
+            p.iterate()
+            g = np.stack([project(p.get_levels(n, 1)[0]) for n in levels])
+            o = md[it][levels]
+            err = float(np.linalg.norm(g - o) / np.linalg.norm(o))
+            print(f"C5 full size m={it}: sampled modal relative L2 = {err:.3e}")
+            assert err < TOL, (it, err)
+
+
 def test_u0_zero_and_initial_guess(pint):
     prob = inputs.example1_fd(3, M=99, N=64)            # U_0 = 0 (table setting)
     check(pint, prob, 3)
