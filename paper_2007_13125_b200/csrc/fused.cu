@@ -78,10 +78,13 @@ static int fused_occ_c(int C, int k, bool tm) {
   return 0;
 }
 
-// one CTA per SM at most when the window sums live in TMEM (each CTA allocates its columns)
+// resident CTAs per SM; with the window sums (and X) in TMEM each CTA allocates its columns, so at
+// most 512 / columns of them (C <= 16: 256 columns, two CTAs)
 int fused_ctas_per_sm(int lanes, int C, int k, bool tm) {
   const int per = lanes == 64 ? fused_occ_c<64>(C, k, tm) : fused_occ_c<32>(C, k, tm);
-  return tm ? (per > 1 ? 1 : per) : per;
+  if (!tm) return per;
+  const int cols = lanes == 32 && C <= 16 ? 256 : 512;
+  return std::min(per, 512 / cols);
 }
 
 int fused_rows_per_subchain(int lanes, int C) {

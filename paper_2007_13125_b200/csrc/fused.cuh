@@ -112,9 +112,15 @@ constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 #ifndef PINT_TM_BATCH
 #define PINT_TM_BATCH 4   // rows per TMEM load batch in the window phase
 #endif
+#ifndef PINT_FUSED_MINB16
+#define PINT_FUSED_MINB16 2   // resident CTAs per SM for lines of <= 512 rows (C <= 16)
+#endif
 template <int LANES> struct FCfg {
   static constexpr int THREADS = FG * LANES;
   static constexpr int NSMAX = LANES == 32 ? PINT_FUSED_NS : 2;
+  // C <= 16 (L <= 512): half the line registers, 64 KB of lines, <= 256 TMEM columns: two CTAs
+  // per SM interleave their solve and row phases
+  static constexpr int minb(int C) { return (LANES == 32 && C <= 16) ? PINT_FUSED_MINB16 : 1; }
 };
 template <int C, int LANES> constexpr int fused_ns() { return C < FCfg<LANES>::NSMAX ? C : FCfg<LANES>::NSMAX; }
 
@@ -571,7 +577,7 @@ template <int C, int LANES, int NKC = 8> struct FTmem {
 // NKC: compile-time bound on nk (and k): X_t = 0 for t >= NKC and window slots r < 8 - NKC are
 // unused, so the synthesis twiddles and the DFT8 butterflies on those zeros/outputs are pruned.
 template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false, int NKC = 8>
-__global__ void __launch_bounds__(FCfg<LANES>::THREADS, 1) wr_fused_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr_fused_kernel(const FusedArgs a) {
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
   constexpr bool TMA = TM && !STORE_W;                  // TMEM accumulators in use
