@@ -230,6 +230,7 @@ def main():
     ap.add_argument("--dst-per-iter", action="store_true",
                     help="ablation (SURVEY §8(a) A6): DST-x around every S-pass instead of hoisted (streaming)")
     args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)   # timing rule: at least 3 untimed warm-up steps (reported as run)
     if args.impl == "reference":
         return run_reference(args)
 
