@@ -103,6 +103,12 @@ cudaError_t launch_modal(bool store_w, const FusedArgs& a, cudaStream_t st) {
 
 cudaError_t launch_finish(const FinishArgs& a0, int mode, cudaStream_t st) {
   FinishArgs a = a0;
+  static const bool two = getenv("PINT_FINISH_TWO_KERNELS") != nullptr;   // A/B: reduce, then finish
+  if (mode == FIN_PARTIALS && a.nch > 16 && !two) {   // many chunks: warp per row, reduce + finish
+    const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
+    wr_reduce_finish_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   if (mode == FIN_PARTIALS && a.nch > 16) {  // many chunks: reduce them first, warp-parallel
     const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
     wr_reduce_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);

@@ -791,6 +791,71 @@ __global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const Fu
 
 // Chunk reduction for small problems (many frequency-group chunks per x-mode, e.g. 1D): one warp per
 // (q, y), lanes over the chunks; the sum replaces chunk 0 (P[q][0][j][y]), deterministic order.
+// The finish step for one row (q, y) from its window sums S_j = sum_p e^{2 pi i n_j p/N} W_p
+// (all chunks summed): U_m window, monitor, new wrap state and X for the next iteration
+// (wr_finish_kernel, mode FIN_PARTIALS)
+__device__ __forceinline__ void finish_row(const FinishArgs& a, long q, int y, const double2 (&S)[8], double& updl,
+                                           bool& nonfinite) {
+  const int k = a.k;
+  const bool live = y < a.L;
+  const long wb = (q * a.NB + y / a.WB) * k * a.WB + (y % a.WB);
+  double2 U[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    U[j] = make_double2(0.0, 0.0);
+    if (j < k && live) {
+      U[j] = cscale(S[j], __ldg(&a.igs[a.N - k + j]));
+      const double dd = sqrt(cabs2(csub(U[j], a.wrap_old[wb + j * a.WB])));
+      if (!(dd <= 1.7976931348623157e308)) nonfinite = true;
+      updl = fmax(updl, dd);
+      a.wrap_new[wb + j * a.WB] = U[j];
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    double2 F = make_double2(0.0, 0.0);
+    if (t < a.nk && live) {
+      for (int i = 0; i < a.nsparse; ++i) {
+        const int s = __ldg(&a.spar[i]);
+        F = cfmar(__ldg(&a.src[((long)s * a.Qb + q) * a.Lpad + y]), __ldg(&a.coef[(long)s * a.N + t]), F);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j >= t && j < k) F = cfmar(U[j], __ldg(&a.wk[k + t - j]), F);
+      F = cscale(F, __ldg(&a.gsf[t]));
+    }
+    a.X[(q * 8 + t) * a.Lf + y] = F;
+  }
+}
+
+// many chunks (nch > 16, 1D problems): one warp per row sums the chunks' window sums (lanes over
+// chunks, shuffle tree), then lane 0 runs the finish step — one kernel instead of reduce + finish
+__global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs a) {
+  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double updl = 0.0;
+  bool nonfinite = false;
+  if (gw < a.Qb * (long)a.Lf) {
+    const long q = gw / a.Lf;
+    const int y = (int)(gw % a.Lf);
+    double2 S[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double2 s = make_double2(0.0, 0.0);
+      if (j < a.k)
+        for (int c = lane; c < a.nch; c += 32) s = cadd(s, a.P[((q * a.pstride + c) * a.k + j) * a.Lf + y]);
+      for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      S[j] = s;
+    }
+    if (lane == 0) finish_row(a, q, y, S, updl, nonfinite);
+  }
+  if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
+  block_max_atomic(updl, a.upd);
+}
+
 __global__ void __launch_bounds__(TPB) wr_reduce_kernel(const FinishArgs a) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
