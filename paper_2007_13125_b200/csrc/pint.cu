@@ -1068,8 +1068,10 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
   ++p->launches;
   // H_1 and the wrap state of U_0 from the time-domain array
   if (p->modal) {   // fully modal: the iteration lives in (q, j) space
-    TRY(dst_y(p, p->A, p->B, p->N, p->Qb));
-    TRY(tpass(p, IN_TIME_BUF, OUT_H, p->B, p->A, nullptr, p->wrap[p->wcur], false));
+    // in place: A's pad rows (y >= L) are zero, while B still holds the user's array in the
+    // physical layout, whose values would sit in the pad slots the DST does not write
+    TRY(dst_y(p, p->A, p->A, p->N, p->Qb));
+    TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
   } else {
     TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
   }

@@ -598,3 +598,29 @@ def test_fem_rejects_unsupported(pint):
     with pytest.raises(pint.PintError) as e:
         pint.Plan.from_problem(prob)
     assert e.value.status == pint.PINT_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("make", [
+    lambda: inputs.random_complex_problem(63, 1, 128, 3, 0.05, 1.0, R=1, seed=21),
+    lambda: inputs.random_complex_problem(31, 15, 64, 2, 0.1, 0.6, R=1, seed=22),
+    lambda: inputs.random_complex_problem(63, 1, 64, 2, 0.1, 1.0, R=1, seed=23).with_(space="fem"),
+], ids=["heat1d_stream", "cq2d", "fem_heat_stream"])
+def test_streaming_modal_and_initial_guess(pint, make):
+    """The streaming modal path (PINT_FLAG_MODAL with PINT_FLAG_STREAM or CQ): iterates vs the
+    oracle, and a user initial guess (the sequential solution, DST'd into the modes at
+    pint_set_initial_guess) is a fixed point."""
+    prob = make()
+    o = wr.wr_naive(prob, 2, dft="fft")
+    kw = {"modal": True, "stream_path": True} if prob.space == "fd" else {"stream_path": True}
+    with pint.Plan.from_problem(prob, **kw) as p:
+        assert not p.path()["fused"]
+        errs = []
+        for m in (1, 2):
+            p.iterate()
+            errs.append(rel(p.get_solution(), o[m]))
+        assert max(errs) <= TOL, errs
+        Us = sequential.sequential(prob)
+        p.set_initial_guess(np.ascontiguousarray(Us))
+        u = p.iterate()
+        assert u < 1e-10 * np.abs(Us).max(), u
+        assert rel(p.get_solution(), Us) < 1e-10
