@@ -209,21 +209,24 @@ def test_state_errors_and_timing(pint):
         assert st == P.PINT_ERR_NOT_CONVERGED and it == 2
 
 
+@pytest.mark.parametrize("variant", ["fused", "modal", "cq_stream", "cq_modal"])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_xmode_slabs_reproduce_single_plan(pint, nranks):
+def test_xmode_slabs_reproduce_single_plan(pint, nranks, variant):
     """The multi-GPU partition on one GPU: each x-mode slab plan iterates independently (the WR
     iteration has no inter-slab exchange), the gathered modal slabs map back to the single-plan
     physical solution (bitwise up to the DST ordering: checked to 1e-14)."""
     from paper_2007_13125_b200 import dist as pdist
-    prob = inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=12)
-    with pint.Plan.from_problem(prob) as p:
+    alpha = 0.5 if variant.startswith("cq") else 1.0
+    kw = {"modal": True} if variant.endswith("modal") else {}
+    prob = inputs.random_complex_problem(63, 31, 128, 4, 0.05, alpha, R=1, seed=12)
+    with pint.Plan.from_problem(prob, **kw) as p:
         for _ in range(3):
             p.iterate()
         ref = p.get_solution()
     slabs, bounds, plans = [], [], []
     for r in range(nranks):
         pl = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha,
-                       rank=r, nranks=nranks, allreduce_max=lambda x: x)
+                       rank=r, nranks=nranks, allreduce_max=lambda x: x, **kw)
         pl.set_problem(prob.v, prob.g, prob.phi, prob.dphi)
         for _ in range(3):
             pl.iterate()
@@ -392,6 +395,7 @@ REAL_CASES = [
     ("C3", lambda: inputs.config_c3()),
     ("2D-real", lambda: inputs.random_complex_problem(63, 40, 256, 4, 0.05, 1.0, R=1, seed=5).real_part()),
     ("1D-N16", lambda: inputs.random_complex_problem(37, 1, 16, 1, 0.3, 1.0, R=2, seed=8).real_part()),
+    ("FEM-1D", lambda: inputs.random_complex_problem(127, 1, 256, 3, 0.05, 1.0, R=1, seed=9).real_part().with_(space="fem")),
 ]
 
 
