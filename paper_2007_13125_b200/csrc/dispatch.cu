@@ -112,11 +112,20 @@ static cudaError_t spass_pair_go(const SPassArgs& a, long Qb, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_spass_const(SPassConst* out, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int L,
+                               cudaStream_t st) {
+  const long total = N * Qb;
+  const long blocks = std::min<long>((total + 127) / 128, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  spass_const_kernel<<<(unsigned)blocks, 128, 0, st>>>(out, sig_p, sig_q, N, Qb, C, L);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
   static const bool staged = getenv("PINT_SPASS_STAGED") != nullptr;   // A/B switches for profiling
   static const bool direct = getenv("PINT_SPASS_DIRECT") != nullptr;
   // two warps per line (C/2 rows per lane) when the line needs C >= 4 rows per lane
-  if (!staged && !direct && a.WB >= 2 && C >= 4) {
+  if (!staged && !direct && a.WB >= 2 && C >= 4 && a.lc) {
     switch (C) {
       case 4: return spass_pair_go<2>(a, Qb, st);
       case 8: return spass_pair_go<4>(a, Qb, st);

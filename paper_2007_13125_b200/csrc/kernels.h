@@ -14,6 +14,9 @@ namespace pint {
 cudaError_t launch_tpass(int N, int mode_in, int mode_out, bool cq, const TPassArgs& a, long ntiles, cudaStream_t st);
 // S-pass: chunk C = ceil(L/32) rounded up to a power of two (1..32), G lines per CTA.
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st);
+// plan time: pair S-pass line constants for C rows per lane (spass.cuh)
+cudaError_t launch_spass_const(SPassConst* out, const double2* sig_p, const double* sig_q, long N, long Qb, int C, int L,
+                               cudaStream_t st);
 // pruned heat T-pass (FREQ -> H), N in {512, 1024, 2048, 4096}
 cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st);
 // CQ FREQ -> H as two kernels (half 0: W -> Z, half 1: Z, W -> H; tpass.cuh)

@@ -183,6 +183,7 @@ struct pint_plan_s {
   double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
   int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
   LineConst* lc = nullptr;    // [Qb][N]
+  SPassConst* slc = nullptr;  // [Qb][N] line constants of the pair S-pass (streaming path)
   double2* Pp = nullptr;      // [Qb][nch][k][Lf]
   int64_t dev_bytes = 0;
   unsigned long long* prof = nullptr;   // -DPINT_FUSED_PROF builds: phase cycle counters (not owned)
@@ -562,6 +563,11 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->thm, thm)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
+  if (p->C >= 4 && p->WB >= 2) {   // the pair S-pass (C/2 rows per lane) reads its line constants
+    if ((st = dalloc(p, &p->slc, (size_t)p->Qb * N)) != PINT_OK) return bail(st);
+    ce = launch_spass_const(p->slc, p->sig_p, p->sig_q, N, p->Qb, p->C / 2, (int)L, p->stream);
+    if (ce != cudaSuccess) { free_plan(p); return fail(PINT_ERR_CUDA, std::string("spass_const: ") + cudaGetErrorString(ce)); }
+  }
   if (p->fused_ok && !p->modal) {
     ce = launch_line_const(p->lc, p->sig_p, p->sig_q, N, p->Qb, p->Cf, fused_rows_per_subchain(p->flanes, p->Cf), (int)L,
                            p->stream);
@@ -651,7 +657,7 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
 static pint_status spass(pint_plan p, const double2* in, double2* out) {
   SPassArgs a{};
   a.in = in; a.out = out; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
-  a.N = p->N; a.NB = p->NB; a.WB = p->WB; a.L = (int)p->L;
+  a.N = p->N; a.NB = p->NB; a.WB = p->WB; a.L = (int)p->L; a.lc = p->slc;
   if (p->modal) {   // streaming modal path: Step 2 is W = H / (sigma_p + sigma_q + mu_j), elementwise
     cudaEvent_t m0 = nullptr, m1 = nullptr;
     if (p->timing) {

@@ -16,6 +16,15 @@
 
 namespace pint {
 
+// Per-line constants of the pair S-pass (plan time, spass_const_kernel): the factorisation
+// a = 1 - u of tridiag(-1, 2 + sigma, -1), the u-form of a^C (C rows per lane), 1/(1 - a^{2L+2}),
+// r = 1/a, and tl = log(1e-18 |1 - a^{2L+2}|) / log|a| (a^e / (1 - a^{2L+2}) matters iff e < tl)
+struct SPassConst {
+  double2 u, uc0, ru2L, rr;
+  double tl, pad;
+};
+static_assert(sizeof(SPassConst) == 80, "SPassConst layout");
+
 struct SPassArgs {
   const double2* in;      // H, tile-blocked layout [q][yb][N][WB]
   double2* out;           // W (may not alias in)
@@ -25,6 +34,7 @@ struct SPassArgs {
   int WB, L;
   int lwb, lgw;           // log2(WB), log2(G*WB)
   long nwork;             // Qb * (N / G) strips
+  const SPassConst* lc;   // [Qb][N] pair-kernel line constants (C/2 rows per lane)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -386,21 +396,23 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 // The pair solve: lane gl = 32 half + lane of the pair owns rows [gl C, gl C + C) in d (rows >= L
 // zero on entry); on exit d holds the solution rows (zero beyond L).  xch: the pair's exchange slots.
 template <int C>
-__device__ __forceinline__ void pair_solve(double2 (&d)[C], double2 sig, int L, int lane, int half, int gl, int nv,
-                                           double2* xch, int pair) {
-  // ---- line setup (as in solve_line_regs) ----
-  const double2 s2 = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
-  const double2 t1 = cscale(cadd(sig, s2), 0.5), t2 = cscale(csub(sig, s2), 0.5);
-  const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
-  const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);
-  const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
-  const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
-  const double2 rr = make_double2(1.0 + tt.x, tt.y);
-  const double2 u = cdiv(tt, rr);
-  double2 uc[6];                                     // u-forms of a^{C 2^j}, j = 0..5
-  uc[0] = u;
+__device__ __forceinline__ void pair_solve(double2 (&d)[C], const SPassConst& lc, int L, int lane, int half, int gl,
+                                           int nv, double2* xch, int pair) {
+  // ---- line constants (plan-time table) ----
+  const double2 u = lc.u, rr = lc.rr;
+  // the lane holding row L-1 zeroes its rows >= L (2^n - 1 lines: one pad row, a single register)
+  const bool pad1 = L >= 64 * C - 1;
+  auto zero_tail = [&](double2 (&v)[C]) {
+    if (pad1) {
+      if (nv < C) v[C - 1] = make_double2(0.0, 0.0);
+    } else if (nv < C) {
 #pragma unroll
-  for (int c = 1; c < C; c <<= 1) uc[0] = uprod(uc[0], uc[0]);
+      for (int r = 0; r < C; ++r)
+        if (r >= nv) v[r] = make_double2(0.0, 0.0);
+    }
+  };
+  double2 uc[6];                                     // u-forms of a^{C 2^j}, j = 0..5
+  uc[0] = lc.uc0;
 #pragma unroll
   for (int i = 1; i < 6; ++i) uc[i] = uprod(uc[i - 1], uc[i - 1]);
   // per-lane u-form of a^{C (lane+1)} and a^{C (32-lane)} (for the cross-warp carries)
@@ -434,8 +446,9 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], double2 sig, int L, 
 #pragma unroll
   for (int r = 0; r < C; ++r) {
     f = cadd(d[r], amul(u, f));
-    d[r] = (r < nv) ? f : make_double2(0.0, 0.0);
+    d[r] = f;
   }
+  zero_tail(d);
   // ---- backward recurrence ----
   double2 w = make_double2(0.0, 0.0);
 #pragma unroll
@@ -464,15 +477,12 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], double2 sig, int L, 
   if (half == 0 && lane == 0) xch[2] = d[0];
   pair_bar(1 + pair);
   const double2 w0 = xch[2];
-  const double2 u2L = upow(u, 2L * L + 2);
-  const double2 K = cdiv(w0, u2L);
+  const double2 K = cmul(w0, lc.ru2L);
   const int y0 = gl * C;
   if (nv > 0) {
     const double2 a1 = make_double2(1.0 - u.x, -u.y);
-    const double la = 0.5 * log(cabs2(a1));
-    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));
-    const bool needP = (y0 + 2) * la > thr;
-    const bool needQ = (2.0 * L + 2 - (y0 + nv - 1)) * la > thr;
+    const bool needP = y0 + 2 < lc.tl;
+    const bool needQ = 2.0 * L + 2 - (y0 + nv - 1) < lc.tl;
     if (needP) {
       const double2 uP = upow(u, y0 + 2);
       double2 KP = cmul(K, make_double2(1.0 - uP.x, -uP.y));
@@ -487,8 +497,38 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], double2 sig, int L, 
     }
   }
 #pragma unroll
-  for (int r = 0; r < C; ++r) d[r] = (r < nv) ? amul(u, d[r]) : make_double2(0.0, 0.0);
+  for (int r = 0; r < C; ++r) d[r] = amul(u, d[r]);
+  zero_tail(d);
 }
+
+// plan time: per-line constants of the pair S-pass (C = rows per lane of the pair kernel)
+static __global__ void spass_const_kernel(SPassConst* out, const double2* sig_p, const double* sig_q, long N, long Qb, int C,
+                                   int L) {
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < N * Qb; e += (long)gridDim.x * blockDim.x) {
+    const long q = e / N, p = e % N;
+    const double2 sp = sig_p[p];
+    const double2 sig = make_double2(sp.x + sig_q[q], sp.y);
+    const double2 s2 = csqrt_(cmul(sig, make_double2(4.0 + sig.x, sig.y)));
+    const double2 t1 = cscale(cadd(sig, s2), 0.5), t2 = cscale(csub(sig, s2), 0.5);
+    const double2 tb = cabs2(t1) >= cabs2(t2) ? t1 : t2;
+    const double2 ts = cdiv(make_double2(-sig.x, -sig.y), tb);          // tb * ts = -sigma
+    const double2 rb = make_double2(1.0 + tb.x, tb.y), rs = make_double2(1.0 + ts.x, ts.y);
+    const double2 tt = cabs2(rb) > cabs2(rs) ? tb : ts;
+    SPassConst c;
+    c.rr = make_double2(1.0 + tt.x, tt.y);                              // r = 1/a, |r| > 1
+    c.u = cdiv(tt, c.rr);                                               // u = 1 - a
+    c.uc0 = upow(c.u, C);
+    const double2 u2L = upow(c.u, 2L * L + 2);                          // 1 - a^{2L+2}
+    c.ru2L = cdiv(make_double2(1.0, 0.0), u2L);
+    const double la = 0.5 * log(cabs2(make_double2(1.0 - c.u.x, -c.u.y)));   // log|a| < 0
+    const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));
+    c.tl = la < 0.0 ? thr / la : INFINITY;
+    c.pad = 0.0;
+    out[e] = c;
+  }
+}
+
+
 
 template <int C>
 __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const SPassArgs a) {
@@ -510,12 +550,10 @@ __global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const S
     if (live && y < Lpad) ld256(in + ((long)(y >> lwb) * N) * WB + (y & (WB - 1)), d[r], d[r + 1]);
     else { d[r] = make_double2(0.0, 0.0); d[r + 1] = d[r]; }
   }
-  const double2 sp = live ? __ldg(&a.sig_p[p]) : make_double2(1.0, 0.0);
-  const double2 sig = make_double2(sp.x + (live ? __ldg(&a.sig_q[q]) : 0.0), sp.y);
   const int nv = min(max(L - gl * C, 0), C);
-#pragma unroll
-  for (int r = 0; r < C; ++r) if (r >= nv) d[r] = make_double2(0.0, 0.0);
-  pair_solve<C>(d, sig, L, lane, half, gl, nv, xch[pair], pair);
+  // input rows y >= L are exact zeros (pad rows of H), so no masking after the loads
+  SPassConst lc = live ? a.lc[q * N + p] : a.lc[0];
+  pair_solve<C>(d, lc, L, lane, half, gl, nv, xch[pair], pair);
   double2* out = a.out + (q * NB * N + p) * WB;
 #pragma unroll
   for (int r = 0; r < C; r += 2) {
