@@ -495,6 +495,10 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       if (eff > beff + 1e-9) { beff = eff; best = c; }
       if (eff >= 0.9) { best = c; break; }
     }
+    if (const char* ov = getenv("PINT_FUSED_NCH")) {   // A/B override (power of two <= NG)
+      const long v = atol(ov);
+      if (v >= 1 && v <= NG && (v & (v - 1)) == 0) best = v;
+    }
     p->nch = (int)best;
     p->gpc = (int)((NG + best - 1) / best);
     for (int i = 0; i < 2; ++i)
