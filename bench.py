@@ -224,7 +224,8 @@ def main():
     ap.add_argument("--path", default="fused", choices=["fused", "stream"],
                     help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
     ap.add_argument("--modal", action="store_true",
-                    help="fully modal variant (SURVEY §8(f) 2a; 2D heat): DST along y too, divisions instead of line solves")
+                    help="fully modal variant (SURVEY §8(f) 2a): DST along the line axis too, divisions instead of "
+                         "line solves (heat: fused modal kernel; CQ: streaming path with a division pass)")
     ap.add_argument("--real", action="store_true",
                     help="real-data half spectrum (SURVEY §8(f) 2b; fused path): solves p <= N/2 only")
     ap.add_argument("--dst-per-iter", action="store_true",
