@@ -44,6 +44,8 @@ cudaError_t launch_nl_update(double2* U, const double2* W, long N, int L, int WB
 cudaError_t launch_imag_max(const double2* A, long count, unsigned long long* upd, cudaStream_t st);
 // streaming modal path: W = H / (sig_p + sig_q + mu_j) over the tile layout (Step 2 as a division)
 cudaError_t launch_modal_div(const SPassArgs& a, const double* mu, long Qb, cudaStream_t st);
+// fixed-point residual of the heat scheme for the materialised iterate (newton.cuh)
+cudaError_t launch_resid(const ResidArgs& a, cudaStream_t st);
 // out[j] = in[j] mu[j] s, j < L (modal-basis operator application: P1-FEM A v)
 cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st);
 cudaError_t launch_nl_diffmax(const double2* A, const double2* B, long count, unsigned long long* upd,

@@ -45,6 +45,14 @@ cudaError_t launch_modal_div(const SPassArgs& a, const double* mu, long Qb, cuda
   return cudaGetLastError();
 }
 
+cudaError_t launch_resid(const ResidArgs& a, cudaStream_t st) {
+  const long total = a.Qb * a.NB * a.N * a.WB;
+  const long blocks = std::min<long>((total + 255) / 256, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  resid_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st) {
   mode_scale_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, in, mu, s, L);
   return cudaGetLastError();

@@ -37,6 +37,18 @@ struct VcArgs {
   int L, Lpad, WB;
 };
 
+struct ResidArgs {
+  const double2* U;          // [q][yb][N][WB]
+  const double2* src;        // [S][Qb * NB][WB]; source 0 is v
+  const double* coef;        // [S][N]
+  const double* wk;          // [k+1] (kappa/tau) omega_j
+  const double* sig_q;       // [Qb] h^2 lambda_q
+  unsigned long long* out;   // [2]
+  long N, NB, Qb;
+  int WB, L, S, k;
+  double ikappa, ih2;
+};
+
 #ifdef PINT_DEFINE_NEWTON_KERNELS
 
 __device__ __forceinline__ double2 nl_g(double2 u, double ieps2) {        // (u^3 - u) / eps^2
@@ -158,6 +170,50 @@ __global__ void modal_div_kernel(const SPassArgs a, const double* mu, long total
       x = cdiv(__ldg(&a.in[e]), make_double2(sp.x + __ldg(&a.sig_q[q]) + __ldg(&mu[j]), sp.y));
     }
     a.out[e] = x;
+  }
+}
+
+// Fixed-point residual of the heat scheme (SURVEY §8(c) "the GPU also self-checks"): for the
+// materialised iterate U (tile layout, x in DST modes q, y physical), level n (0-based, = t_{n+1}):
+//   r = (1/tau) sum_{j=0}^{min(k,n)} omega_j U^{n-j} + (lambda_q + A_y) U^n - F_static_n
+// (the all-at-once form: the history U^{<=0} = v sits in F_static),
+// A_y = (2 U_y - U_{y-1} - U_{y+1}) / h^2, lambda_q = sig_q / h^2, F_static_n = sum_s c_s(n) src_s
+// (eqn:BDF).  max|r| -> out[0], max|F_static| -> out[1] (ordered bits).
+
+__global__ void resid_kernel(const ResidArgs a, long total) {
+  double rm = 0.0, fm = 0.0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int w = (int)(e % a.WB);
+    const long r1 = e / a.WB;
+    const long n = r1 % a.N, r2 = r1 / a.N;
+    const long yb = r2 % a.NB, q = r2 / a.NB;
+    const int y = (int)(yb * a.WB + w);
+    if (y >= a.L) continue;
+    auto at = [&](long nn, int yy) -> double2 {       // U^{nn} at row yy (zero outside the line)
+      if (yy < 0 || yy >= a.L) return make_double2(0.0, 0.0);
+      const long ti = q * a.NB + yy / a.WB;
+      if (nn < 0) return a.src[ti * a.WB + yy % a.WB];  // history U^{<=0} = v
+      return a.U[(ti * a.N + nn) * a.WB + yy % a.WB];
+    };
+    const double2 u = a.U[e];
+    double2 r = cscale(csub(cscale(u, 2.0), cadd(at(n, y - 1), at(n, y + 1))), a.ih2);
+    r = cfmar(u, a.sig_q[q] * a.ih2, r);
+    // levels >= 1 only: the history U^{<=0} = v is part of F_static (tau^-1 sum_{j<n} omega_j v)
+    for (int j = 0; j <= a.k && j <= n; ++j) r = cfmar(at(n - j, y), a.wk[j] * a.ikappa, r);
+    double2 F = make_double2(0.0, 0.0);
+    const long ti = q * a.NB + yb;
+    for (int s = 0; s < a.S; ++s) F = cfmar(a.src[((long)s * a.Qb * a.NB + ti) * a.WB + w], a.coef[(long)s * a.N + n], F);
+    r = csub(r, F);
+    rm = fmax(rm, sqrt(cabs2(r)));
+    fm = fmax(fm, sqrt(cabs2(F)));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+    fm = fmax(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&a.out[0], (unsigned long long)__double_as_longlong(rm));
+    atomicMax(&a.out[1], (unsigned long long)__double_as_longlong(fm));
   }
 }
 

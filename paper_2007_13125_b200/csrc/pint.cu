@@ -1587,6 +1587,37 @@ extern "C" pint_status pint_get_timing(pint_plan p, double* tpass_ms, double* sp
   return PINT_OK;
 }
 
+extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* rhs_inf) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
+  if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
+  if (p->alpha != 1.0 || p->fem || p->modal || p->nl || p->dst_iter || p->has_fd)
+    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: heat (alpha = 1), FD operator, line-solve paths, separable data");
+  CUDA_TRY(cudaSetDevice(p->device));
+  TRY(materialize(p));                     // A: U_m, x in DST modes, y physical (tile layout)
+  if (!p->wstage) TRY(dalloc(p, &p->wstage, (size_t)p->k * p->M));
+  unsigned long long* acc = (unsigned long long*)p->wstage;   // 2 words of scratch
+  CUDA_TRY(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), p->stream));
+  ResidArgs a{};
+  a.U = p->A; a.src = p->src; a.coef = p->coef; a.wk = p->wk; a.sig_q = p->sig_q; a.out = acc;
+  a.N = p->N; a.NB = p->NB; a.Qb = p->Qb; a.WB = p->WB; a.L = (int)p->L; a.S = p->S; a.k = p->k;
+  a.ikappa = 1.0 / p->kappa; a.ih2 = 1.0 / (p->h * p->h);
+  CUDA_TRY(launch_resid(a, p->stream));
+  ++p->launches;
+  unsigned long long bits[2];
+  CUDA_TRY(cudaMemcpyAsync(bits, acc, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  double r, f;
+  std::memcpy(&r, &bits[0], sizeof(r));
+  std::memcpy(&f, &bits[1], sizeof(f));
+  if (p->nranks > 1) {
+    if (p->allreduce(&r, p->actx) != 0 || p->allreduce(&f, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
+  }
+  if (residual_inf) *residual_inf = r;
+  if (rhs_inf) *rhs_inf = f;
+  return PINT_OK;
+}
+
 extern "C" pint_status pint_get_info(pint_plan p, int64_t* m, int64_t* launches, int64_t* dev_bytes) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (m) *m = p->m;

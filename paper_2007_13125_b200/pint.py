@@ -32,6 +32,7 @@ EXPORTED = [
     "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
     "pint_kappa_log_rule", "pint_get_path", "pint_set_nonlinearity", "pint_newton_solve", "pint_set_problem",
+    "pint_residual",
 ]
 
 
@@ -84,6 +85,7 @@ def lib(path: str = LIB_PATH):
         "pint_set_nonlinearity": [P, I32, D],
         "pint_set_problem": [P, VP, VP, VP, VP, I32],
         "pint_newton_solve": [P, I32, D, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(I32)],
+        "pint_residual": [P, ctypes.POINTER(D), ctypes.POINTER(D)],
     }
     for name, args in sig.items():
         if not hasattr(L, name) and "PINT_LIB" in os.environ:
@@ -268,6 +270,12 @@ class Plan:
         t, s, tn, sn = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().pint_get_timing(self._h, ctypes.byref(t), ctypes.byref(s), ctypes.byref(tn), ctypes.byref(sn)))
         return {"tpass_ms": t.value, "spass_ms": s.value, "tpass_launches": tn.value, "spass_launches": sn.value}
+
+    def residual(self) -> tuple[float, float]:
+        """(max |residual of the BDF-k scheme at U_m|, max |F_static|) — pint_residual (heat, FD)."""
+        r, f = ctypes.c_double(), ctypes.c_double()
+        _check(lib().pint_residual(self._h, ctypes.byref(r), ctypes.byref(f)))
+        return r.value, f.value
 
     def info(self):
         m, l, b = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

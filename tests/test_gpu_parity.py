@@ -628,3 +628,42 @@ def test_streaming_modal_and_initial_guess(pint, make):
         u = p.iterate()
         assert u < 1e-10 * np.abs(Us).max(), u
         assert rel(p.get_solution(), Us) < 1e-10
+
+
+@pytest.mark.parametrize("make,kw", [
+    (lambda: inputs.config_c1(), {}),
+    (lambda: inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=31), {}),
+    (lambda: inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=31), {"stream_path": True}),
+    (lambda: inputs.random_complex_problem(100, 1, 256, 6, 0.01, 1.0, R=2, seed=33), {}),
+], ids=["C1", "2d_fused", "2d_stream", "1d_bdf6"])
+def test_gpu_residual_self_check(pint, make, kw):
+    """pint_residual: the GPU's own fixed-point residual of the BDF-k scheme equals
+    the oracle residual of the same iterate at m = 1 (far from convergence) and drops to round-off
+    at the WR fixed point."""
+    from oracle import bdf, problem, spatial
+    prob = make()
+    with pint.Plan.from_problem(prob, **kw) as p:
+        p.iterate()
+        r1, f1 = p.residual()
+        U = p.get_solution()
+        # oracle residual of the same iterate in the scheme's own form, eqn:BDF (P:281-288): history
+        # U^{<=0} = v on the left and f̄_n on the right (the GPU uses the all-at-once form with the
+        # history moved into F_static, so the two agree only if both are right)
+        w = [float(x) for x in bdf.bdf_weights(prob.k)]
+        fb = problem.fbar(prob)
+        R = np.stack([sum((w[j] / prob.tau) * (U[n - j] if n - j >= 0 else prob.v) for j in range(prob.k + 1))
+                      + spatial.apply_A(U[n], prob.mx, prob.my) - fb[n] for n in range(prob.N)])
+        if prob.my > 1:                                          # the plan works in the DST-x basis
+            R = spatial.dst1(R.reshape(prob.N, prob.my, prob.mx), axis=-1)
+        ro = float(np.abs(R).max())
+        assert r1 > 1e-8 * f1                                      # not converged after one iteration
+        assert abs(r1 - ro) <= 1e-9 * ro, (r1, ro)
+        it, u, st = p.solve(1e-13, 60, raise_on_fail=False)
+        r, f = p.residual()
+        assert r <= 1e-9 * f, (r, f, it, u)
+    with pint.Plan.from_problem(prob, modal=True) if prob.my > 1 and (prob.my + 1) & prob.my == 0 else \
+            pint.Plan.from_problem(prob.with_(alpha=0.5)) as p:
+        p.iterate()
+        with pytest.raises(pint.PintError) as e:
+            p.residual()
+        assert e.value.status == pint.PINT_ERR_UNSUPPORTED
