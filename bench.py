@@ -394,6 +394,14 @@ def main():
                "what": f"set_problem(pinned host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
                        + ("final time level to host" if world == 1 else "each rank's modal slab of the final level to host")
                        + ", per step (max over ranks); unknowns/s per WR iteration"}
+        # self-check of the converged e2e solution against the scheme (pint_residual; outside
+        # every timed region): max |residual of eqn:BDF| / max |F_static|
+        try:
+            r_inf, f_inf = plan.residual()
+            e2e["self_check_residual_rel"] = r_inf / f_inf if f_inf > 0 else r_inf
+        except pint.PintError as exc:   # CQ / modal / FEM plans: not available
+            e2e["self_check_residual_rel"] = None
+            e2e["self_check_note"] = str(exc)[:80]
 
     cpu = None
     if rank == 0 and not args.no_cpu:
