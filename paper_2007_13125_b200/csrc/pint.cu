@@ -163,6 +163,8 @@ struct pint_plan_s {
   double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
   unsigned long long* updh = nullptr;   // pinned host copy of upd
+  char* stage = nullptr;                // pinned staging of the per-problem tables (set_problem)
+  size_t stage_cap = 0, stage_off = 0;
   bool upd_queued = false;              // the D2H copy of upd is already on the stream
   // fused heat iteration (fused.cuh): state = X (nk <= 8 levels) + window; no H/W arrays per iteration
   bool dst_iter = false;      // PINT_FLAG_DST_PER_ITER: physical-x arrays, DST-x around every S-pass
@@ -254,6 +256,31 @@ static pint_status h2d(pint_plan p, T* dst, const std::vector<T>& v) {
 
 static double2 d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
 
+// per-problem tables: copied through a plan-owned pinned staging buffer without a synchronisation
+// per table (set_problem synchronises once at its end, before the buffer can be reused)
+static pint_status stage_reserve(pint_plan p, size_t bytes) {
+  if (p->stage_off) CUDA_TRY(cudaStreamSynchronize(p->stream));   // an earlier call returned early
+  p->stage_off = 0;
+  if (bytes <= p->stage_cap) return PINT_OK;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (p->stage) CUDA_TRY(cudaFreeHost(p->stage));
+  p->stage = nullptr;
+  p->stage_cap = 0;
+  CUDA_TRY(cudaHostAlloc((void**)&p->stage, bytes, cudaHostAllocDefault));
+  p->stage_cap = bytes;
+  return PINT_OK;
+}
+template <class T>
+static pint_status h2d_async(pint_plan p, T* dst, const std::vector<T>& v) {
+  const size_t bytes = v.size() * sizeof(T);
+  const size_t off = (p->stage_off + 15) & ~(size_t)15;
+  if (off + bytes > p->stage_cap) return h2d(p, dst, v);          // (not reserved: synchronous copy)
+  std::memcpy(p->stage + off, v.data(), bytes);
+  CUDA_TRY(cudaMemcpyAsync(dst, p->stage + off, bytes, cudaMemcpyHostToDevice, p->stream));
+  p->stage_off = off + bytes;
+  return PINT_OK;
+}
+
 // in-place radix-2 DFT in long double (host plan tables): x_p <- sum_n x_n e^{sign 2 pi i n p / N}
 static void fft_ld(std::vector<cld>& x, int sign) {
   const size_t N = x.size();
@@ -325,6 +352,7 @@ static void free_plan(pint_plan p) {
   for (cudaGraphExec_t g : p->gexec) if (g) cudaGraphExecDestroy(g);
   for (auto& ev : p->gev) for (cudaEvent_t e : ev) if (e) cudaEventDestroy(e);
   if (p->updh) cudaFreeHost(p->updh);
+  if (p->stage) cudaFreeHost(p->stage);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -855,6 +883,7 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
 
   // sources: 0 = v, 1 = A v, 2.. = g_r
   const int S = 2 + R;
+  TRY(stage_reserve(p, (size_t)S * N * (2 * sizeof(double2) + sizeof(double)) + 2 * (size_t)S * sizeof(int) + 256));
   if (p->S != S) {
     if (p->src) return fail(PINT_ERR_STATE, "set_problem may be called again only with the same R");
     TRY(dalloc(p, &p->src, (size_t)S * p->ntiles * p->WB));
@@ -956,8 +985,8 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     p->ndense = S - p->nsparse;
     p->nk = nk;
     p->fused = p->fused_ok && nk <= 8;
-    TRY(h2d(p, p->srclist, lst));
-    if (!ch.empty()) TRY(h2d(p, p->chat, ch));
+    TRY(h2d_async(p, p->srclist, lst));
+    if (!ch.empty()) TRY(h2d_async(p, p->chat, ch));
   }
   if (p->cqhat) {
     // CQ split T-pass: H_static = V^{-1} Gamma F_static h^2/N is iteration-invariant and separable,
@@ -971,14 +1000,15 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
       fft_ld(x, -1);
       for (int64_t pp = 0; pp < N; ++pp) ch[(size_t)s * N + pp] = d2(x[pp]);
     }
-    TRY(h2d(p, p->cqhat, ch));
+    TRY(h2d_async(p, p->cqhat, ch));
   }
-  TRY(h2d(p, p->coef, coef));
-  TRY(h2d(p, p->nhi, nhi));
+  TRY(h2d_async(p, p->coef, coef));
+  TRY(h2d_async(p, p->nhi, nhi));
   p->problem_set = true;
   p->wcur = 0;
   if (boot) TRY(bootstrap(p));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->stage_off = 0;                        // the staged copies have completed
   return PINT_OK;
 }
 
