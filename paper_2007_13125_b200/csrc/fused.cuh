@@ -62,8 +62,10 @@ struct FusedArgs {
   int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
                            // 8 u-form recurrences on every line
   int reserved;            // zero: keeps the struct free of padding (the graph replay memcmp's it)
+  unsigned long long* upd_reset;   // iteration launches: the update monitor, zeroed by block 0 before
+                                   // the finish kernel accumulates into it (replaces a memset)
 };
-static_assert(sizeof(FusedArgs) == 168, "FusedArgs must stay padding-free");
+static_assert(sizeof(FusedArgs) == 176, "FusedArgs must stay padding-free");
 
 // smem row swizzle: lane l of the solve owns rows [lC, lC + C); XOR-ing the low bits with the
 // chunk index keeps its 16-byte accesses bank-conflict free, and consecutive rows (row phases)
@@ -581,6 +583,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
   constexpr bool TMA = TM && !STORE_W;                  // TMEM accumulators in use
+  if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
   __shared__ uint32_t tbase;
   double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
   double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums (shared-memory variant)
@@ -735,6 +738,7 @@ template <bool STORE_W>
 __global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const FusedArgs a) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
   if (gw >= a.Qb * (long)a.L) return;                       // warp-uniform
   const long q = gw / a.L;
   const int j = (int)(gw % a.L);

@@ -736,8 +736,9 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   return a;
 }
 
-static pint_status fused_pass(pint_plan p, const double2* X, bool store_w) {
+static pint_status fused_pass(pint_plan p, const double2* X, bool store_w, bool reset_upd = false) {
   FusedArgs a = fargs(p, X);
+  if (reset_upd) a.upd_reset = p->upd;
   if (store_w) {   // materialising variant: shared-memory layout without X, every frequency group
     a.xs = 0;
     a.half = 0;
@@ -1129,8 +1130,7 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // ------------------------------------------------------------------------------------------
 // one fused iteration: update monitor reset, Steps 1-3 (fused kernel), window / X / monitor (finish)
 static pint_status fused_step(pint_plan p) {
-  CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
-  TRY(fused_pass(p, p->X[p->xcur], false));                                       // Steps 1-3
+  TRY(fused_pass(p, p->X[p->xcur], false, true));   // Steps 1-3 (block 0 zeroes the update monitor)
   TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
   CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
   return PINT_OK;
