@@ -147,7 +147,9 @@ pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
 
 /* One WR iteration m-1 -> m.  *update_inf (may be NULL) receives the max over ranks of
  * max |U_m^n(x) - U_{m-1}^n(x)| over the monitored levels n = N-k+1..N (the wrap state,
- * which determines the next iterate for heat). */
+ * which determines the next iterate for heat).
+ * The fused heat iteration is replayed as a CUDA graph on the plan stream (captured on first use,
+ * re-captured when the problem changes; PINT_NO_GRAPH=1 in the environment: eager launches). */
 pint_status pint_wr_iterate(pint_plan plan, double* update_inf);
 
 /* Iterate until update < tol, or max_iters iterations (PINT_ERR_NOT_CONVERGED), or the update
@@ -178,7 +180,9 @@ pint_status pint_get_partition(pint_plan plan, int64_t* q_begin, int64_t* q_end)
 
 /* Per-pass timing with CUDA events on the plan stream (bench/profiling):
  * enable != 0 starts accumulating; pint_get_timing returns total milliseconds and launch
- * counts of the T-pass (time-axis kernel) and S-pass (shifted-solve kernel) since enabled. */
+ * counts of the T-pass (time-axis kernel) and S-pass (shifted-solve kernel) since enabled.
+ * Fused heat path: the S-pass slot holds the fused kernel, the T-pass slot the finish kernel
+ * (event nodes inside the replayed graph, which cost a few microseconds per iteration). */
 pint_status pint_set_timing(pint_plan plan, int32_t enable);
 pint_status pint_get_timing(pint_plan plan, double* tpass_ms, double* spass_ms,
                             int64_t* tpass_launches, int64_t* spass_launches);
