@@ -667,3 +667,30 @@ def test_gpu_residual_self_check(pint, make, kw):
         with pytest.raises(pint.PintError) as e:
             p.residual()
         assert e.value.status == pint.PINT_ERR_UNSUPPORTED
+
+
+def test_api_edge_cases(pint):
+    """Empty and out-of-range reads, zero-iteration solves, resets and state errors."""
+    P = pint
+    prob = inputs.random_complex_problem(31, 9, 64, 3, 0.1, 1.0, R=1, seed=41)
+    with P.Plan.from_problem(prob) as p:
+        with pytest.raises(P.PintError) as e:
+            p.residual()                                      # no iterate yet
+        assert e.value.status == P.PINT_ERR_STATE
+        it, u, st = p.solve(1e-12, 0, raise_on_fail=False)   # zero iterations allowed
+        assert it == 0 and st == P.PINT_ERR_NOT_CONVERGED
+        p.iterate()
+        assert p.get_levels(5, 0).shape == (0, prob.M)       # empty read
+        for n0, cnt in ((-1, 1), (prob.N, 1), (prob.N - 1, 2)):
+            with pytest.raises(P.PintError) as e:
+                p.get_levels(n0, cnt)
+            assert e.value.status == P.PINT_ERR_ARG
+        U = p.get_solution()
+        assert np.array_equal(p.get_levels(prob.N - 1, 1)[0], U[-1])
+        p.set_initial_guess(None)                             # back to U_0^n = v, m = 0
+        assert p.info()["m"] == 0
+        with pytest.raises(P.PintError) as e:
+            p.get_solution()
+        assert e.value.status == P.PINT_ERR_STATE
+        p.iterate()
+        assert rel(p.get_solution(), U) < 1e-14                # the same first iterate again
