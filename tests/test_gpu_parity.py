@@ -694,3 +694,21 @@ def test_api_edge_cases(pint):
         assert e.value.status == P.PINT_ERR_STATE
         p.iterate()
         assert rel(p.get_solution(), U) < 1e-14                # the same first iterate again
+
+
+@pytest.mark.parametrize("make,kw", [
+    (lambda: inputs.random_complex_problem(63, 1, 64, 2, 0.1, 1.0, R=1, seed=51).with_(space="fem"), {}),
+    (lambda: inputs.random_complex_problem(31, 63, 128, 4, 0.05, 1.0, R=1, seed=52), {"modal": True}),
+    (lambda: inputs.random_complex_problem(31, 63, 128, 4, 0.05, 1.0, R=1, seed=53).real_part(), {"modal": True, "real_data": True}),
+], ids=["fem_fused", "modal2d_fused", "modal2d_real"])
+def test_fused_modal_initial_guess(pint, make, kw):
+    """Fused modal plans (P1-FEM, 2D modal): the sequential solution as a user initial guess is a
+    fixed point (update at round-off from the first iteration on)."""
+    prob = make()
+    Us = sequential.sequential(prob)
+    with pint.Plan.from_problem(prob, **kw) as p:
+        assert p.path()["fused"]
+        p.set_initial_guess(np.ascontiguousarray(Us))
+        us = [p.iterate() for _ in range(2)]
+        assert max(us) < 1e-10 * np.abs(Us).max(), us
+        assert rel(p.get_solution(), Us) < 1e-10
