@@ -227,9 +227,9 @@ pint_status pint_get_path(pint_plan plan, int32_t* fused, int32_t* chunks, int32
  * |(1/tau) sum_j omega_j U^{n-j} + A U^n - F_static_n| (U^{<=0} = v; in the hoisted DST-x basis),
  * rhs_inf = max |F_static_n|.  At the WR fixed point the ratio is at round-off level; for an
  * unconverged iterate it measures the distance to the sequential BDF-k solution.  Materialises U_m
- * (as pint_get_levels).  UNSUPPORTED for CQ, P1-FEM, PINT_FLAG_MODAL, semilinear plans,
- * PINT_FLAG_DST_PER_ITER and dense forcing; STATE before the first iteration.  Multi-rank: max over
- * ranks (collective). */
+ * (as pint_get_levels; modal plans and P1-FEM: in the DST modes of both axes, A diagonal).
+ * UNSUPPORTED for CQ, semilinear plans, PINT_FLAG_DST_PER_ITER and dense forcing; STATE before the
+ * first iteration.  Multi-rank: max over ranks (collective). */
 pint_status pint_residual(pint_plan plan, double* residual_inf, double* rhs_inf);
 
 /* Introspection: iteration count m, total kernel launches issued by this plan, device bytes. */

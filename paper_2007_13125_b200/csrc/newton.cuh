@@ -47,6 +47,7 @@ struct ResidArgs {
   long N, NB, Qb;
   int WB, L, S, k;
   double ikappa, ih2;
+  const double* mu;          // modal plans (U in (q, j) modes): A_y = mu_j / h^2 instead of the stencil
 };
 
 #ifdef PINT_DEFINE_NEWTON_KERNELS
@@ -196,7 +197,8 @@ __global__ void resid_kernel(const ResidArgs a, long total) {
       return a.U[(ti * a.N + nn) * a.WB + yy % a.WB];
     };
     const double2 u = a.U[e];
-    double2 r = cscale(csub(cscale(u, 2.0), cadd(at(n, y - 1), at(n, y + 1))), a.ih2);
+    double2 r = a.mu ? cscale(u, a.mu[y] * a.ih2)
+                     : cscale(csub(cscale(u, 2.0), cadd(at(n, y - 1), at(n, y + 1))), a.ih2);
     r = cfmar(u, a.sig_q[q] * a.ih2, r);
     // levels >= 1 only: the history U^{<=0} = v is part of F_static (tau^-1 sum_{j<n} omega_j v)
     for (int j = 0; j <= a.k && j <= n; ++j) r = cfmar(at(n - j, y), a.wk[j] * a.ikappa, r);

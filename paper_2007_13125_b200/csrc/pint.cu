@@ -1621,15 +1621,21 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  if (p->alpha != 1.0 || p->fem || p->modal || p->nl || p->dst_iter || p->has_fd)
-    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: heat (alpha = 1), FD operator, line-solve paths, separable data");
+  if (p->alpha != 1.0 || p->nl || p->dst_iter || p->has_fd)
+    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: heat (alpha = 1) with separable data");
   CUDA_TRY(cudaSetDevice(p->device));
   TRY(materialize(p));                     // A: U_m, x in DST modes, y physical (tile layout)
+  const double2* U = p->A;
+  if (p->modal) {                          // back to (q, j) modes, where the sources live; B is free
+    TRY(dst_y(p, p->A, p->B, p->N, p->Qb));   // here (A keeps U_m, the next iteration re-derives from it)
+    U = p->B;
+  }
   if (!p->wstage) TRY(dalloc(p, &p->wstage, (size_t)p->k * p->M));
   unsigned long long* acc = (unsigned long long*)p->wstage;   // 2 words of scratch
   CUDA_TRY(cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), p->stream));
   ResidArgs a{};
-  a.U = p->A; a.src = p->src; a.coef = p->coef; a.wk = p->wk; a.sig_q = p->sig_q; a.out = acc;
+  a.U = U; a.src = p->src; a.coef = p->coef; a.wk = p->wk; a.sig_q = p->sig_q; a.out = acc;
+  a.mu = p->modal ? p->mu : nullptr;
   a.N = p->N; a.NB = p->NB; a.Qb = p->Qb; a.WB = p->WB; a.L = (int)p->L; a.S = p->S; a.k = p->k;
   a.ikappa = 1.0 / p->kappa; a.ih2 = 1.0 / (p->h * p->h);
   CUDA_TRY(launch_resid(a, p->stream));

@@ -635,7 +635,9 @@ def test_streaming_modal_and_initial_guess(pint, make):
     (lambda: inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=31), {}),
     (lambda: inputs.random_complex_problem(63, 40, 128, 4, 0.05, 1.0, R=1, seed=31), {"stream_path": True}),
     (lambda: inputs.random_complex_problem(100, 1, 256, 6, 0.01, 1.0, R=2, seed=33), {}),
-], ids=["C1", "2d_fused", "2d_stream", "1d_bdf6"])
+    (lambda: inputs.random_complex_problem(31, 63, 128, 3, 0.05, 1.0, R=1, seed=34), {"modal": True}),
+    (lambda: inputs.random_complex_problem(63, 1, 128, 2, 0.05, 1.0, R=1, seed=35).with_(space="fem"), {}),
+], ids=["C1", "2d_fused", "2d_stream", "1d_bdf6", "2d_modal", "fem"])
 def test_gpu_residual_self_check(pint, make, kw):
     """pint_residual: the GPU's own fixed-point residual of the BDF-k scheme equals
     the oracle residual of the same iterate at m = 1 (far from convergence) and drops to round-off
@@ -652,17 +654,21 @@ def test_gpu_residual_self_check(pint, make, kw):
         w = [float(x) for x in bdf.bdf_weights(prob.k)]
         fb = problem.fbar(prob)
         R = np.stack([sum((w[j] / prob.tau) * (U[n - j] if n - j >= 0 else prob.v) for j in range(prob.k + 1))
-                      + spatial.apply_A(U[n], prob.mx, prob.my) - fb[n] for n in range(prob.N)])
+                      + spatial.apply_A(U[n], prob.mx, prob.my, prob.space) - fb[n] for n in range(prob.N)])
+        modal_plan = kw.get("modal", False) or prob.space == "fem"
         if prob.my > 1:                                          # the plan works in the DST-x basis
             R = spatial.dst1(R.reshape(prob.N, prob.my, prob.mx), axis=-1)
+            if modal_plan:                                       # ... and DST-y on modal plans
+                R = spatial.dst1(R, axis=-2)
+        elif modal_plan:                                         # 1D modal / FEM: DST along the line
+            R = spatial.dst1(R, axis=-1)
         ro = float(np.abs(R).max())
         assert r1 > 1e-8 * f1                                      # not converged after one iteration
         assert abs(r1 - ro) <= 1e-9 * ro, (r1, ro)
         it, u, st = p.solve(1e-13, 60, raise_on_fail=False)
         r, f = p.residual()
         assert r <= 1e-9 * f, (r, f, it, u)
-    with pint.Plan.from_problem(prob, modal=True) if prob.my > 1 and (prob.my + 1) & prob.my == 0 else \
-            pint.Plan.from_problem(prob.with_(alpha=0.5)) as p:
+    with pint.Plan.from_problem(prob.with_(alpha=0.5)) as p:                # CQ: not available
         p.iterate()
         with pytest.raises(pint.PintError) as e:
             p.residual()
