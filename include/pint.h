@@ -222,14 +222,16 @@ pint_status pint_newton_solve(pint_plan plan, int32_t max_outer, double outer_to
  * of Gamma F (after pint_set_problem_separable).  Any pointer may be NULL. */
 pint_status pint_get_path(pint_plan plan, int32_t* fused, int32_t* chunks, int32_t* nk);
 
-/* Self-check of the current iterate U_m against the scheme it converges to (heat,
- * eqn:BDF P:281-288): residual_inf = max over all levels and points of
- * |(1/tau) sum_j omega_j U^{n-j} + A U^n - F_static_n| (U^{<=0} = v; in the hoisted DST-x basis),
+/* Self-check of the current iterate U_m against the scheme it converges to (
+ * eqn:BDF P:281-288, CQ eqn:CQ-1 P:946-950): residual_inf = max over all levels and points of
+ * |tau^-a sum_j omega_j U^{n-j} + A U^n - F_static_n| (all-at-once form: the v-history is in
+ * F_static; in the hoisted DST-x basis),
  * rhs_inf = max |F_static_n|.  At the WR fixed point the ratio is at round-off level; for an
  * unconverged iterate it measures the distance to the sequential BDF-k solution.  Materialises U_m
  * (as pint_get_levels; modal plans and P1-FEM: in the DST modes of both axes, A diagonal).
- * UNSUPPORTED for CQ, semilinear plans, PINT_FLAG_DST_PER_ITER and dense forcing; STATE before the
- * first iteration.  Multi-rank: max over ranks (collective). */
+ * CQ plans: the full history convolution, O(N) per unknown (a check, not a pass).  UNSUPPORTED
+ * for CQ on the modal path, semilinear plans, PINT_FLAG_DST_PER_ITER and dense forcing; STATE before
+ * the first iteration.  Multi-rank: max over ranks (collective). */
 pint_status pint_residual(pint_plan plan, double* residual_inf, double* rhs_inf);
 
 /* Introspection: iteration count m, total kernel launches issued by this plan, device bytes. */

@@ -46,6 +46,7 @@ cudaError_t launch_imag_max(const double2* A, long count, unsigned long long* up
 cudaError_t launch_modal_div(const SPassArgs& a, const double* mu, long Qb, cudaStream_t st);
 // fixed-point residual of the heat scheme for the materialised iterate (newton.cuh)
 cudaError_t launch_resid(const ResidArgs& a, cudaStream_t st);
+cudaError_t launch_resid_cq_time(const double2* U, double2* T, const double* w, long N, long ntiles, cudaStream_t st);
 // out[j] = in[j] mu[j] s, j < L (modal-basis operator application: P1-FEM A v)
 cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st);
 cudaError_t launch_nl_diffmax(const double2* A, const double2* B, long count, unsigned long long* upd,

@@ -53,6 +53,17 @@ cudaError_t launch_resid(const ResidArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_resid_cq_time(const double2* U, double2* T, const double* w, long N, long ntiles,
+                                 cudaStream_t st) {
+  const int smem = 4096 * (int)sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(resid_cq_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const long grid = std::min<long>(ntiles, 148L * 3);
+  if (grid <= 0) return cudaSuccess;
+  resid_cq_time_kernel<<<(unsigned)grid, 256, smem, st>>>(U, T, w, N, ntiles);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mode_scale(double2* out, const double2* in, const double* mu, double s, int L, cudaStream_t st) {
   mode_scale_kernel<<<grid_for(L, 256), 256, 0, st>>>(out, in, mu, s, L);
   return cudaGetLastError();

@@ -48,6 +48,7 @@ struct ResidArgs {
   int WB, L, S, k;
   double ikappa, ih2;
   const double* mu;          // modal plans (U in (q, j) modes): A_y = mu_j / h^2 instead of the stencil
+  const double2* tconv;      // CQ: the time term tau^-a sum_{j<=n} omega_j U^{n-j}, precomputed (same layout)
 };
 
 #ifdef PINT_DEFINE_NEWTON_KERNELS
@@ -200,8 +201,10 @@ __global__ void resid_kernel(const ResidArgs a, long total) {
     double2 r = a.mu ? cscale(u, a.mu[y] * a.ih2)
                      : cscale(csub(cscale(u, 2.0), cadd(at(n, y - 1), at(n, y + 1))), a.ih2);
     r = cfmar(u, a.sig_q[q] * a.ih2, r);
-    // levels >= 1 only: the history U^{<=0} = v is part of F_static (tau^-1 sum_{j<n} omega_j v)
-    for (int j = 0; j <= a.k && j <= n; ++j) r = cfmar(at(n - j, y), a.wk[j] * a.ikappa, r);
+    // levels >= 1 only: the history U^{<=0} = v is part of F_static (tau^-a sum_{j<n} omega_j v)
+    if (a.tconv) r = cadd(r, a.tconv[e]);
+    else
+      for (int j = 0; j <= a.k && j <= n; ++j) r = cfmar(at(n - j, y), a.wk[j] * a.ikappa, r);
     double2 F = make_double2(0.0, 0.0);
     const long ti = q * a.NB + yb;
     for (int s = 0; s < a.S; ++s) F = cfmar(a.src[((long)s * a.Qb * a.NB + ti) * a.WB + w], a.coef[(long)s * a.N + n], F);
@@ -216,6 +219,26 @@ __global__ void resid_kernel(const ResidArgs a, long total) {
   if ((threadIdx.x & 31) == 0) {
     atomicMax(&a.out[0], (unsigned long long)__double_as_longlong(rm));
     atomicMax(&a.out[1], (unsigned long long)__double_as_longlong(fm));
+  }
+}
+
+// CQ history term of the residual, one CTA per tile (all N levels of WB columns in shared memory):
+// T[n][c] = sum_{j=0}^{n} w_j U[n-j][c], w_j = tau^-a omega_j (eqn:CQ-1, in the
+// all-at-once form whose v-history sits in F_static).  O(N) per element: a self-check, not a pass.
+__global__ void resid_cq_time_kernel(const double2* U, double2* T, const double* w, long N, long ntiles) {
+  extern __shared__ double2 tile[];
+  const int WB = (int)(4096 / N);
+  for (long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long base = t * 4096;
+    for (int e = threadIdx.x; e < 4096; e += blockDim.x) tile[e] = U[base + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+      const int n = e / WB, c = e % WB;
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = 0; j <= n; ++j) s = cfmar(tile[(n - j) * WB + c], __ldg(&w[j]), s);
+      T[base + e] = s;
+    }
+    __syncthreads();
   }
 }
 

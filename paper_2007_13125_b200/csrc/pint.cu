@@ -156,6 +156,7 @@ struct pint_plan_s {
   double2* cqhat = nullptr;   // [S][N] CQ split T-pass: DFTs of Gamma h^2/N c_s(n) for every source
   double2 *tw = nullptr, *twE = nullptr;
   double *gsf = nullptr, *igs = nullptr, *gsN = nullptr, *wk = nullptr;
+  double* cqw = nullptr;      // [N] tau^-a omega_j (CQ plans)
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
   double2* sig_p = nullptr;
   double* sig_q = nullptr;
@@ -460,6 +461,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = dalloc(p, &p->igs, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->gsN, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->wk, k + 1)) != PINT_OK) return bail(st);
+  if (alpha != 1.0 && (st = dalloc(p, &p->cqw, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->dh, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->dpr, N)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->thp, N)) != PINT_OK) return bail(st);
@@ -589,6 +591,11 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->igs, igs)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->gsN, gsN)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->wk, wk)) != PINT_OK) return bail(st);
+  if (alpha != 1.0) {   // tau^-a omega_j, j < N (CQ weights; pint_residual's history convolution)
+    std::vector<double> cqw(N);
+    for (int64_t j = 0; j < N; ++j) cqw[j] = (double)(ta * w[j]);
+    if ((st = h2d(p, p->cqw, cqw)) != PINT_OK) return bail(st);
+  }
   if ((st = h2d(p, p->dh, dh)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->dpr, dpr)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->thp, thp)) != PINT_OK) return bail(st);
@@ -1621,8 +1628,8 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  if (p->alpha != 1.0 || p->nl || p->dst_iter || p->has_fd)
-    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: heat (alpha = 1) with separable data");
+  if (p->nl || p->dst_iter || p->has_fd || (p->alpha != 1.0 && p->modal))
+    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: separable data; CQ on the line-solve path");
   CUDA_TRY(cudaSetDevice(p->device));
   TRY(materialize(p));                     // A: U_m, x in DST modes, y physical (tile layout)
   const double2* U = p->A;
@@ -1636,6 +1643,11 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
   ResidArgs a{};
   a.U = U; a.src = p->src; a.coef = p->coef; a.wk = p->wk; a.sig_q = p->sig_q; a.out = acc;
   a.mu = p->modal ? p->mu : nullptr;
+  if (p->alpha != 1.0) {   // CQ: the full history convolution per column, tile by tile into B (free here)
+    CUDA_TRY(launch_resid_cq_time(p->A, p->B, p->cqw, p->N, p->ntiles, p->stream));
+    ++p->launches;
+    a.tconv = p->B;
+  }
   a.N = p->N; a.NB = p->NB; a.Qb = p->Qb; a.WB = p->WB; a.L = (int)p->L; a.S = p->S; a.k = p->k;
   a.ikappa = 1.0 / p->kappa; a.ih2 = 1.0 / (p->h * p->h);
   CUDA_TRY(launch_resid(a, p->stream));

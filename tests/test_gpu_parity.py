@@ -637,12 +637,14 @@ def test_streaming_modal_and_initial_guess(pint, make):
     (lambda: inputs.random_complex_problem(100, 1, 256, 6, 0.01, 1.0, R=2, seed=33), {}),
     (lambda: inputs.random_complex_problem(31, 63, 128, 3, 0.05, 1.0, R=1, seed=34), {"modal": True}),
     (lambda: inputs.random_complex_problem(63, 1, 128, 2, 0.05, 1.0, R=1, seed=35).with_(space="fem"), {}),
-], ids=["C1", "2d_fused", "2d_stream", "1d_bdf6", "2d_modal", "fem"])
+    (lambda: inputs.random_complex_problem(63, 1, 256, 2, 0.05, 0.5, R=1, seed=36), {}),
+    (lambda: inputs.config_c5(m=63), {}),
+], ids=["C1", "2d_fused", "2d_stream", "1d_bdf6", "2d_modal", "fem", "cq1d", "c5_63"])
 def test_gpu_residual_self_check(pint, make, kw):
     """pint_residual: the GPU's own fixed-point residual of the BDF-k scheme equals
     the oracle residual of the same iterate at m = 1 (far from convergence) and drops to round-off
     at the WR fixed point."""
-    from oracle import bdf, problem, spatial
+    from oracle import nonlinear, problem, spatial
     prob = make()
     with pint.Plan.from_problem(prob, **kw) as p:
         p.iterate()
@@ -651,10 +653,8 @@ def test_gpu_residual_self_check(pint, make, kw):
         # oracle residual of the same iterate in the scheme's own form, eqn:BDF: history
         # U^{<=0} = v on the left and f̄_n on the right (the GPU uses the all-at-once form with the
         # history moved into F_static, so the two agree only if both are right)
-        w = [float(x) for x in bdf.bdf_weights(prob.k)]
-        fb = problem.fbar(prob)
-        R = np.stack([sum((w[j] / prob.tau) * (U[n - j] if n - j >= 0 else prob.v) for j in range(prob.k + 1))
-                      + spatial.apply_A(U[n], prob.mx, prob.my, prob.space) - fb[n] for n in range(prob.N)])
+        R = nonlinear.dbar(prob, U) + np.stack([spatial.apply_A(U[n], prob.mx, prob.my, prob.space)
+                                                for n in range(prob.N)]) - problem.fbar(prob)
         modal_plan = kw.get("modal", False) or prob.space == "fem"
         if prob.my > 1:                                          # the plan works in the DST-x basis
             R = spatial.dst1(R.reshape(prob.N, prob.my, prob.mx), axis=-1)
@@ -668,11 +668,18 @@ def test_gpu_residual_self_check(pint, make, kw):
         it, u, st = p.solve(1e-13, 60, raise_on_fail=False)
         r, f = p.residual()
         assert r <= 1e-9 * f, (r, f, it, u)
-    with pint.Plan.from_problem(prob.with_(alpha=0.5)) as p:                # CQ: not available
-        p.iterate()
-        with pytest.raises(pint.PintError) as e:
-            p.residual()
-        assert e.value.status == pint.PINT_ERR_UNSUPPORTED
+
+
+def test_gpu_residual_unsupported(pint):
+    """pint_residual is not available for CQ on the modal path and for the DST ablation."""
+    cq = inputs.random_complex_problem(31, 15, 64, 2, 0.1, 0.5, R=1, seed=37)
+    heat = inputs.random_complex_problem(31, 15, 64, 2, 0.1, 1.0, R=1, seed=38)
+    for prob, kw in ((cq, {"modal": True}), (heat, {"dst_per_iter": True})):
+        with pint.Plan.from_problem(prob, **kw) as p:
+            p.iterate()
+            with pytest.raises(pint.PintError) as e:
+                p.residual()
+            assert e.value.status == pint.PINT_ERR_UNSUPPORTED
 
 
 def test_api_edge_cases(pint):
