@@ -41,7 +41,8 @@ def _newest_dep() -> float:
 
 
 def _compile(src: str, obj: str, defines: list[str]) -> tuple[str, str]:
-    cmd = [nvcc(), *ARCH, *FLAGS, *defines, "-c", src, "-o", obj]
+    extra = os.environ.get("PINT_NVCC_EXTRA", "").split()      # experiments only (variant builds)
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, *defines, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src} {defines}:\n{r.stderr}")
