@@ -210,6 +210,24 @@ def run_reference(args):
     return 0
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` (N > 1) started without torchrun: re-launch this script as N ranks on this
+    node (one process per GPU, 127.0.0.1 rendezvous), NCCL's INFO log on stderr so the communicator
+    lines show the N ranks.  Returns the launcher's exit code; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -232,6 +250,8 @@ def main():
                     help="ablation (SURVEY §8(a) A6): DST-x around every S-pass instead of hoisted (streaming)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)   # timing rule: at least 3 untimed warm-up steps (reported as run)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -242,11 +262,24 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    ndev = torch.cuda.device_count()
+    # one rank per GPU over NCCL; more ranks than GPUs (a 1-GPU box checking the launch path) time-slice
+    # one device and use gloo for the one-double all-reduce (NCCL refuses two ranks on one device);
+    # such a line is flagged "oversubscribed" and is not a scaling measurement
+    oversub = world > ndev
+    backend = "gloo" if oversub else "nccl"
+    local_dev = local % ndev
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    red = torch.zeros(1, dtype=torch.float64, device=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    rdev = dev if backend == "nccl" else torch.device("cpu")
+    red = torch.zeros(1, dtype=torch.float64, device=rdev)
 
     def allreduce_max(x: float) -> float:
         red.fill_(x)
@@ -255,7 +288,7 @@ def main():
 
     prob = make_problem(args.config, args.mx)
     stream = torch.cuda.Stream(device=dev)
-    plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local,
+    plan = pint.Plan(prob.mx, prob.my, prob.N, prob.k, prob.kappa, prob.tau, prob.alpha, device=local_dev,
                      stream=stream.cuda_stream, u0_zero=(prob.u0 == "zero"), rank=rank, nranks=world,
                      allreduce_max=allreduce_max if world > 1 else None, stream_path=(args.path == "stream"),
                      dst_per_iter=args.dst_per_iter, real_data=args.real, modal=args.modal)
@@ -272,7 +305,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         e0.record(stream)
         upd = []
         for _ in range(args.steps):
@@ -287,13 +320,13 @@ def main():
     # every kernel on the plan stream (event nodes inside the replayed graph; kept out of the timed
     # region above, where they would cost small problems several microseconds per iteration)
     plan.set_timing(True)
-    with ClockSampler(local) as clk_k:
+    with ClockSampler(local_dev) as clk_k:
         for _ in range(args.steps):
             plan.iterate()
         tm = plan.get_timing()
     plan.set_timing(False)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -368,6 +401,7 @@ def main():
             out = torch.empty((1, prob.M), dtype=torch.complex128, pin_memory=True).numpy()
         steps, t_tot, its = args.e2e_steps, 0.0, 0
         out_bytes = 0
+        statuses = []
         for i in range(steps + 1):
             torch.cuda.synchronize(dev)
             if world > 1:
@@ -381,25 +415,27 @@ def main():
                 plan.get_levels(prob.N - 1, 1, out)
             dt = time.perf_counter() - t0
             if world > 1:
-                tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+                tt = torch.tensor([dt], dtype=torch.float64, device=rdev)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 dt = float(tt.item())
             if i > 0:
                 t_tot += dt
                 its += it
+                statuses.append(int(st))
             out_bytes = out.nbytes
         e2e = {"value": total_unknowns * its / t_tot, "unit": UNIT,
                "h2d_bytes_per_step": int(vh.nbytes + (prob.g.nbytes if prob.R else 0)),
                "d2h_bytes_per_step": int(out_bytes + 8 * its // steps),
                "what": f"set_problem(pinned host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
                        + ("final time level to host" if world == 1 else "each rank's modal slab of the final level to host")
-                       + ", per step (max over ranks); unknowns/s per WR iteration"}
+                       + ", per step (max over ranks); unknowns/s per WR iteration",
+               "converged": all(x == pint.PINT_OK for x in statuses), "solve_status": statuses}
         # self-check of the converged e2e solution against the scheme (pint_residual; outside
         # every timed region): max |residual of eqn:BDF| / max |F_static|
         try:
             r_inf, f_inf = plan.residual()
             e2e["self_check_residual_rel"] = r_inf / f_inf if f_inf > 0 else r_inf
-        except pint.PintError as exc:   # CQ / modal / FEM plans: not available
+        except pint.PintError as exc:   # CQ on the modal path, dense forcing, DST ablation: not available
             e2e["self_check_residual_rel"] = None
             e2e["self_check_note"] = str(exc)[:80]
 
@@ -422,7 +458,10 @@ def main():
                                  " > L2 126 MB, no flush needed" if path["fused"] else
                                  f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-               "comm": ({"collective": "NCCL all_reduce(max) of the update norm, one double per iteration",
+               "comm": ({"collective": f"{backend} all_reduce(max) of the update norm, one double per iteration",
+                         "backend": backend, "oversubscribed": oversub,
+                         "note": (f"{world} ranks time-slice {ndev} GPU(s): launch-path check, not a scaling "
+                                  "measurement") if oversub else "one rank per GPU",
                          "data_path_bytes_per_step": 0, "allreduce_bytes_per_step": 8,
                          "partition": f"x-mode slabs (rank 0: q in [{q0}, {q1}))"} if world > 1 else None),
                "clocks": clk.summary(), "last_update": upd[-1] if upd else None}

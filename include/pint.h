@@ -32,6 +32,10 @@
  *     DST-I basis (pint_get_partition).  The WR iteration needs no data exchange between
  *     slabs (the x-modes decouple exactly); the only collective is the all-reduce(max) of
  *     the update norm, done through the caller-supplied allreduce_max callback.
+ *     The collective calls (pint_wr_iterate, pint_wr_solve, pint_residual) make the same
+ *     allreduce_max calls on every rank even when the local part fails on one rank: that rank
+ *     returns its own error, the others see a non-finite update (wr_solve: DIVERGED) or
+ *     PINT_ERR_COMM (residual) instead of blocking in the collective.
  */
 #ifndef PINT_H_
 #define PINT_H_
@@ -78,13 +82,23 @@ enum {
   PINT_FLAG_REAL_DATA = 16,    /* heat, fused path: v, g_r (and U_0) are real, so W_{N-p} = conj(W_p)
                                   and only the frequencies p <= N/2 are solved (SURVEY §8(f) item
                                   2b); pint_set_problem_separable returns ARG for complex data */
-  PINT_FLAG_MODAL = 32         /* fully modal variant — the DST is applied
+  PINT_FLAG_MODAL = 32,        /* fully modal variant — the DST is applied
                                   along the line axis as well (2D: y; 1D: x; hoisted), every mode is
                                   a scalar problem and the shifted solves are divisions (heat: the
                                   fused modal kernel; CQ or PINT_FLAG_STREAM: the streaming path with
                                   an elementwise division pass); needs 2(L+1) a power of two, L = my
                                   (2D) or mx (1D) (UNSUPPORTED otherwise); excludes
                                   PINT_FLAG_DST_PER_ITER (ARG) */
+  PINT_FLAG_FULL_UPDATE_NORM = 64  /* update monitor over ALL N levels and points: the paper's stopping
+                                  rule max_n |U_m^n - U_{m-1}^n|_inf.
+                                  Always on for CQ plans (alpha < 1: the kappa-wrap reads every level
+                                  of U_{m-1}, so the k-level window does not bound
+                                  the update).  Heat: opt-in; selects the streaming path with unpruned
+                                  time FFTs.  Costs one more space-time array (U_{m-1}, N*M*16 B) and
+                                  32 B of HBM traffic per unknown per iteration; pint_get_levels then
+                                  reads U_m from it without re-materialising.  2D: the norm is taken in
+                                  the hoisted DST-x basis (orthonormal in x; reading R-norm2D),
+                                  fully modal plans in the DST basis of both axes. */
 };
 
 typedef struct {
@@ -146,8 +160,9 @@ pint_status pint_set_problem(pint_plan plan, const void* v, const void* f, const
 pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
 
 /* One WR iteration m-1 -> m.  *update_inf (may be NULL) receives the max over ranks of
- * max |U_m^n(x) - U_{m-1}^n(x)| over the monitored levels n = N-k+1..N (the wrap state,
- * which determines the next iterate for heat).
+ * max |U_m^n(x) - U_{m-1}^n(x)| over the monitored levels: every level n = 1..N for CQ plans and
+ * with PINT_FLAG_FULL_UPDATE_NORM, else the window n = N-k+1..N (the wrap
+ * state, which determines the next iterate for heat).
  * The fused heat iteration is replayed as a CUDA graph on the plan stream (captured on first use,
  * re-captured when the problem changes; PINT_NO_GRAPH=1 in the environment: eager launches). */
 pint_status pint_wr_iterate(pint_plan plan, double* update_inf);

@@ -15,6 +15,7 @@ from __future__ import annotations
 import time
 
 import numpy as np
+import scipy.fft
 
 from . import bdf, problem, spatial
 
@@ -60,7 +61,9 @@ def wrap_cq_fft(U_prev: np.ndarray, w: np.ndarray) -> np.ndarray:
     Up = np.zeros((2 * N,) + U_prev.shape[1:], np.complex128)
     Up[:N] = U_prev
     # y_n = sum_{s>=1} c_s U^{n+s}  (0-based: y[i] = sum_s c[s] U[i+s])
-    y = np.fft.ifft(np.conj(np.fft.fft(c))[:, None] * np.fft.fft(Up, axis=0), axis=0)[:N]
+    cf = np.conj(np.fft.fft(c))
+    y = scipy.fft.ifft(cf.reshape((2 * N,) + (1,) * (Up.ndim - 1)) * scipy.fft.fft(Up, axis=0, workers=-1),
+                       axis=0, workers=-1)[:N]
     return y
 
 
@@ -99,8 +102,8 @@ def wr_naive(prob, iters: int, U0: np.ndarray | None = None, dft: str = "naive",
     """Run `iters` WR iterations; returns [U_0, U_1, ..., U_iters] (each [N][M]).
 
     dft="naive": explicit N x N DFT matrices applied by zgemm (the default, obviously correct);
-    dft="fft": numpy.fft library primitive for the same two products (large sizes; pinned equal
-    to "naive" in tests).  Eigenvalues d_p from oracle.bdf.eigenvalues (long double)."""
+    dft="fft": library FFT (scipy.fft, pocketfft, all host threads) for the same two products (large
+    sizes; pinned equal to "naive" in tests).  Eigenvalues d_p from oracle.bdf.eigenvalues (long double)."""
     N = prob.N
     w = bdf.time_weights(prob.k, prob.alpha, N)
     gam = bdf.gamma_scale(N, prob.kappa)
@@ -118,9 +121,9 @@ def wr_naive(prob, iters: int, U0: np.ndarray | None = None, dft: str = "naive",
         t0 = time.perf_counter()
         F = rhs(prob, U, F_static, w, wrap)
         X = gam[:, None] * F                              # Step 1a: Gamma F
-        H = (Vinv @ X) if dft == "naive" else np.fft.fft(X, axis=0) / N   # Step 1b
+        H = (Vinv @ X) if dft == "naive" else scipy.fft.fft(X, axis=0, workers=-1) / N   # Step 1b
         Q = op.solve(shifts, H)                           # Step 2
-        Y = (V @ Q) if dft == "naive" else np.fft.ifft(Q, axis=0) * N     # Step 3: V Q
+        Y = (V @ Q) if dft == "naive" else scipy.fft.ifft(Q, axis=0, workers=-1) * N     # Step 3: V Q
         U = Y / gam[:, None]                              # Step 3: Gamma^{-1}
         if timings is not None:
             timings.append(time.perf_counter() - t0)

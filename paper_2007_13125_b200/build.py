@@ -55,7 +55,15 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
     defines = defines or []
     LIB = os.path.join(HERE, lib) if lib else globals()["LIB"]
     build_dir = BUILD + ("_" + os.path.splitext(lib)[0] if lib else "")
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_dep():
+    extra = os.environ.get("PINT_NVCC_EXTRA", "").split()
+    if extra and not lib:
+        raise RuntimeError("PINT_NVCC_EXTRA is for variant builds only: pass lib=<variant name>")
+    # the full flag set is stamped next to the library: a change of flags or defines rebuilds it
+    stamp = " ".join([nvcc(), *ARCH, *FLAGS, *extra, *defines])
+    stamp_path = LIB + ".flags"
+    fresh = (os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_dep() and os.path.exists(stamp_path)
+             and open(stamp_path).read() == stamp)
+    if not force and fresh:
         return LIB
     os.makedirs(build_dir, exist_ok=True)
     units = [(os.path.join(CSRC, "inst_n.cu"), os.path.join(build_dir, f"inst_{n}.o"), [f"-DPINT_N={n}", *defines])
@@ -77,6 +85,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    with open(stamp_path, "w") as f:
+        f.write(stamp)
     if verbose:
         print(f"built {LIB}")
     return LIB

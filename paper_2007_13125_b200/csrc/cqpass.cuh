@@ -1,0 +1,316 @@
+// cqpass.cuh — the CQ (subdiffusion) T-pass of one WR iteration as ONE kernel per iteration.
+//
+// Per tile (all N levels of WB = 4096/N adjacent spatial columns, 64 KB, contiguous in HBM):
+//   W_m --V--> u                      U_m = Gamma^{-1} u: full-array update monitor,
+//                                     U_m -> ufull, window levels -> wrap state        (Step 3)
+//   u --Theta/N, V^{-1}--> z --D'--> --V--> s --C Theta^{-1}, V^{-1}--> H'
+//   H_{m+1} = H' + D W_m + sum_s chat_s src_s                       (kappa-wrap + Step 1)
+// i.e. the circulant +- skew-circulant form of the kappa-wrap of eq:BDF-subdiff-F (DESIGN.md §5.2,
+// "CQ wrap"): four length-N transforms per column, all on chip.
+//
+// B200 design (replaces the two-kernel split of tpass.cuh, which moved 80 B/unknown and ran each
+// transform as three radix-16 passes with two shared-memory exchanges):
+//  * N = N1 * N1 (N1 = 32: N = 1024, the C5 configuration; N1 = 16: N = 256) as a 4-step transform:
+//    thread (i, c) owns the N1 values i + N1 t of column c; pass A = DFT_N1 over t in registers, twiddle
+//    w^{i k2}, ONE shared-memory exchange (row-padded: conflict-free 16-byte accesses), pass B = DFT_N1.
+//    Input and output mappings are the same (thread i holds index i + N1 t), so the four transforms
+//    chain without further exchanges: 4 exchanges per tile instead of 8 (+2 for the split halves).
+//  * The diagonal Theta/N and C Theta^{-1} factors are folded into the forward transforms: the
+//    per-thread part theta^i into the pass-A twiddle table, the per-register part e^{+-i pi t/N1} into
+//    compile-time rotations (no table loads for them).
+//  * The tile arrives by a 1D TMA bulk copy (cp.async.bulk, completion on an mbarrier) into the same
+//    shared buffer the exchanges use; the next tile's copy is issued as soon as the last exchange of
+//    the current tile has been read, and lands while the current tile finishes its last DFT, the
+//    monitor-free epilogue and the stores.  The next tile (and this tile's U_{m-1}) are prefetched
+//    into L2 at the start of each tile.
+//  * D W + H_static (the iteration-invariant static spectrum) is formed when W arrives and parked in
+//    tensor memory (TMEM, otherwise idle: 128 columns per CTA) until the end of the tile, instead of
+//    re-reading W from HBM/L2.
+// HBM per unknown: W in 16 B, H out 16 B, U_{m-1} in + U_m out 32 B (full monitor) = 64 B.
+#pragma once
+#include "tpass.cuh"
+
+namespace pint {
+
+// cos(pi n / 32), n = 0..16 (quarter wave; the rest by symmetry; literals: no table in device code)
+__host__ __device__ constexpr double cosq32(int n) {
+  switch (n) {
+    case 0: return 1.0;
+    case 1: return 0.9951847266721968862448;
+    case 2: return 0.9807852804032304491262;
+    case 3: return 0.9569403357322088649358;
+    case 4: return 0.9238795325112867561282;
+    case 5: return 0.8819212643483550297128;
+    case 6: return 0.8314696123025452370788;
+    case 7: return 0.7730104533627369608109;
+    case 8: return 0.7071067811865475244008;
+    case 9: return 0.6343932841636454982152;
+    case 10: return 0.5555702330196022247428;
+    case 11: return 0.4713967368259976485564;
+    case 12: return 0.3826834323650897717285;
+    case 13: return 0.2902846772544623676362;
+    case 14: return 0.1950903220161282678483;
+    case 15: return 0.0980171403295606019942;
+    case 16: return 0.0;
+  }
+  return 0.0;
+}
+__host__ __device__ constexpr double cos32(int n) {   // cos(pi n / 32), any integer n
+  n = ((n % 64) + 64) % 64;
+  return n <= 16 ? cosq32(n) : (n <= 32 ? -cosq32(32 - n) : (n <= 48 ? -cosq32(n - 32) : cosq32(64 - n)));
+}
+__host__ __device__ constexpr double sin32(int n) { return cos32(n - 16); }
+
+// a * e^{i pi m / 32} (m a compile-time constant after unrolling)
+__device__ __forceinline__ double2 crot32(double2 a, int m) {
+  m = ((m % 64) + 64) % 64;
+  if (m == 0) return a;
+  if (m == 16) return make_double2(-a.y, a.x);
+  if (m == 32) return make_double2(-a.x, -a.y);
+  if (m == 48) return make_double2(a.y, -a.x);
+  const double c = cos32(m), s = sin32(m);
+  return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+}
+
+// b_s = sum_t a_t exp(DIR 2 pi i s t / 32): radix-2 step over two DFT16s (decimation in time)
+template <int DIR> __device__ __forceinline__ void dft32(double2* a) {
+  double2 e[16], o[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    e[t] = a[2 * t];
+    o[t] = a[2 * t + 1];
+  }
+  dft16<DIR>(e);
+  dft16<DIR>(o);
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const double2 w = crot32(o[s], 2 * DIR * s);
+    a[s] = cadd(e[s], w);
+    a[s + 16] = csub(e[s], w);
+  }
+}
+template <int N1, int DIR> __device__ __forceinline__ void dft_n1(double2* a) {
+  if constexpr (N1 == 32) dft32<DIR>(a);
+  else dft16<DIR>(a);
+}
+
+template <int N1> struct CQCfg {
+  static constexpr int N = N1 * N1;
+  static constexpr int WB = TILE / N;                       // columns per tile
+  static constexpr int THREADS = N1 * WB;                   // thread (i, c) = (tid / WB, tid % WB)
+  static constexpr int ROW = N1 * WB + (WB == 4 ? 4 : 0);   // exchange row stride (complex), padded
+  static constexpr int BUF = (N1 * ROW > TILE ? N1 * ROW : TILE);
+  static constexpr int SMEM = BUF * 16;
+  static constexpr int MINB = N1 == 32 ? 3 : 2;
+  static constexpr int TCOLS = 128;                         // TMEM columns per CTA (stash of D W + H_static)
+};
+
+struct CQArgs {
+  const double2* in;          // W_m, tile layout [ntiles][N][WB]
+  double2* out;               // H_{m+1} (may alias in: a tile is read into shared memory first)
+  double2* ufull;             // U_{m-1} -> U_m, every level (tile layout)
+  double2* wrap_new;          // [ntiles][k][WB] window levels of U_m
+  unsigned long long* upd;    // max |U_m - U_{m-1}| as ordered bits
+  const double2* twi;         // [N] e^{+2 pi i (i k2 mod N)/N} at [i N1 + k2]          (inverse transforms)
+  const double2* twz;         // [N] theta^i / N e^{-2 pi i i k2/N}                     (forward, Theta/N)
+  const double2* twx;         // [N] c_x theta^{-i} e^{-2 pi i i k2/N}, c_x = -h^2/(2 N tau^a)
+  const double2* dpr;         // [N] d'_p, eigenvalues of C(-kappa)
+  const double2* dh;          // [N] (h^2/(2 tau^a)) d_p
+  const double2* chat;        // [S][N] DFT of kappa^{n/N} h^2/N c_s(n)  (static right-hand side)
+  const double2* src;         // [S][ntiles][WB] spatial sources (DST-x basis)
+  const double* igs;          // [N] kappa^{-n/N}
+  int S, k;
+  long ntiles;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tile_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+  } while (!done);
+}
+
+// 4 complex doubles <-> 16 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st4c(uint32_t addr, const double2* x) {
+  uint32_t w[16];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    w[4 * j + 0] = (uint32_t)__double2loint(x[j].x); w[4 * j + 1] = (uint32_t)__double2hiint(x[j].x);
+    w[4 * j + 2] = (uint32_t)__double2loint(x[j].y); w[4 * j + 3] = (uint32_t)__double2hiint(x[j].y);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+               ::"r"(addr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                 "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld4c(uint32_t addr, double2* x) {
+  uint32_t w[16];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                 "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    x[j] = make_double2(__hiloint2double((int)w[4 * j + 1], (int)w[4 * j + 0]),
+                        __hiloint2double((int)w[4 * j + 3], (int)w[4 * j + 2]));
+}
+
+// One length-N transform on the register set v (thread (i, c): v[t] = x[i + N1 t] on entry and
+// X[i + N1 t] on exit).  PRE = +1/-1: the input is first rotated by e^{PRE i pi t / N1} (the
+// per-register part of a folded Theta^{+-1}); the pass-A table tw[i N1 + k2] carries the
+// twiddle w^{DIR i k2} (and the per-thread folded factor).  LAST: after the exchange has been read,
+// barrier and call on_free() (the buffer is free: the next tile's copy may be issued).
+template <int N1, int DIR, int PRE, bool LAST = false, class F>
+__device__ __forceinline__ void cq_xform(double2 (&v)[N1], double2* xb, const double2* __restrict__ tw, int i, int c,
+                                         F&& on_free) {
+  using G = CQCfg<N1>;
+  if constexpr (PRE != 0) {
+#pragma unroll
+    for (int t = 1; t < N1; ++t) v[t] = crot32(v[t], PRE * t * (32 / N1));
+  }
+  dft_n1<N1, DIR>(v);
+  const double2* tr = tw + i * N1;
+#pragma unroll
+  for (int k2 = (PRE != 0 ? 0 : 1); k2 < N1; ++k2) v[k2] = cmul(v[k2], __ldg(&tr[k2]));
+  __syncthreads();                       // the buffer is free (previous exchange / tile input read)
+#pragma unroll
+  for (int k2 = 0; k2 < N1; ++k2) xb[k2 * G::ROW + i * G::WB + c] = v[k2];
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < N1; ++t) v[t] = xb[i * G::ROW + t * G::WB + c];
+  if constexpr (LAST) {
+    __syncthreads();
+    on_free();
+  }
+  dft_n1<N1, DIR>(v);
+}
+
+template <int N1>
+__global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_fused_kernel(const CQArgs a) {
+  using G = CQCfg<N1>;
+  constexpr int N = G::N, WB = G::WB, NW = G::THREADS / 32;
+  extern __shared__ __align__(128) double2 buf[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ uint32_t tbase;
+  __shared__ double red[NW];
+  const int tid = threadIdx.x, i = tid / WB, c = tid % WB, warp = tid / 32;
+  const uint32_t sbuf = smem_u32(buf), sbar = smem_u32(&bar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"(smem_u32(&tbase)), "n"(G::TCOLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // this thread's stash columns: lane 32 (warp % 4) + lane, N1 * 4 columns (N1 complex doubles)
+  const uint32_t tst = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * N1 * 4);
+  const long ntiles = a.ntiles;
+  long tile = blockIdx.x;
+  uint32_t phase = 0;
+  if (tid == 0 && tile < ntiles) tile_bulk_load(sbuf, a.in + tile * (long)TILE, TILE * 16, sbar);
+  double upd = 0.0;
+  bool nonfinite = false;
+  for (; tile < ntiles; tile += gridDim.x) {
+    const long base = tile * (long)TILE, nt = tile + gridDim.x;
+    if (tid < 4) {
+      if (nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
+    } else if (tid < 8) {
+      prefetch_l2_t(a.ufull + base + (tid - 4) * (TILE / 4), TILE / 4 * 16);
+    }
+    mbar_wait(sbar, phase);
+    phase ^= 1;
+    double2 v[N1];
+#pragma unroll
+    for (int t = 0; t < N1; ++t) v[t] = buf[(i + N1 * t) * WB + c];
+    // stash = D W + H_static (frequency p = i + N1 t) -> TMEM, 4 values per tcgen05.st
+    {
+      const double2* srcp = a.src + tile * WB + c;
+      const long sstr = ntiles * WB;
+      const double2 g0 = a.S > 0 ? __ldg(&srcp[0]) : make_double2(0.0, 0.0);
+      const double2 g1 = a.S > 1 ? __ldg(&srcp[sstr]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < N1 / 4; ++q) {
+        double2 x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int p = i + N1 * (4 * q + j);
+          double2 h = cmul(v[4 * q + j], __ldg(&a.dh[p]));
+          if (a.S > 0) h = cfma(__ldg(&a.chat[p]), g0, h);
+          if (a.S > 1) h = cfma(__ldg(&a.chat[N + p]), g1, h);
+          for (int s = 2; s < a.S; ++s) h = cfma(__ldg(&a.chat[(long)s * N + p]), __ldg(&srcp[s * sstr]), h);
+          x[j] = h;
+        }
+        tmem_st4c(tst + 16 * q, x);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+    auto none = [] {};
+    // ---- u = V W ----
+    cq_xform<N1, +1, 0>(v, buf, a.twi, i, c, none);
+    // ---- U_m = Gamma^{-1} u: full-array monitor, U_m -> ufull, window -> wrap state ----
+#pragma unroll
+    for (int t = 0; t < N1; ++t) {
+      const int n = i + N1 * t;
+      const double2 U = cscale(v[t], __ldg(&a.igs[n]));
+      const long e = base + (long)n * WB + c;
+      const double d = sqrt(cabs2(csub(U, a.ufull[e])));
+      if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+      upd = fmax(upd, d);
+      a.ufull[e] = U;
+      if (t == N1 - 1 && i >= N1 - a.k) a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
+    }
+    // ---- z = V^{-1} Theta u  (Theta / N folded), Z = D' z ----
+    cq_xform<N1, -1, +1>(v, buf, a.twz, i, c, none);
+#pragma unroll
+    for (int t = 0; t < N1; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[i + N1 * t]));
+    // ---- s = V Z ----
+    cq_xform<N1, +1, 0>(v, buf, a.twi, i, c, none);
+    // ---- H' = V^{-1} (c_x Theta^{-1} s); the buffer is free once its exchange is read ----
+    cq_xform<N1, -1, -1, true>(v, buf, a.twx, i, c, [&] {
+      if (tid == 0 && nt < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        tile_bulk_load(sbuf, a.in + nt * (long)TILE, TILE * 16, sbar);
+      }
+    });
+    // ---- H = H' + D W + H_static ----
+    const unsigned long long ef = l2_evict_first();
+#pragma unroll
+    for (int q = 0; q < N1 / 4; ++q) {
+      double2 x[4];
+      tmem_ld4c(tst + 16 * q, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int p = i + N1 * (4 * q + j);
+        st_hint(&a.out[base + (long)p * WB + c], cadd(v[4 * q + j], x[j]), ef);
+      }
+    }
+  }
+  // ---- update monitor: block max, one atomic per CTA; TMEM release ----
+  if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
+  for (int o = 16; o > 0; o >>= 1) upd = fmax(upd, __shfl_xor_sync(0xffffffffu, upd, o));
+  if ((tid & 31) == 0) red[warp] = upd;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    double m = red[0];
+    for (int w = 1; w < NW; ++w) m = fmax(m, red[w]);
+    atomicMax(a.upd, (unsigned long long)__double_as_longlong(m));
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(G::TCOLS) : "memory");
+}
+
+}  // namespace pint

@@ -47,6 +47,14 @@ cudaError_t launch_tpass_cq_split(int N, int half, const TPassArgs& a, long ntil
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_tpass_cq_fused(int N, const CQArgs& a, cudaStream_t st) {
+  switch (N) {
+    case 256: return launch_tpass_cq_fused_256(a, st);
+    case 1024: return launch_tpass_cq_fused_1024(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_dst(int NE, const DstArgs& a, int mode, cudaStream_t st) {
   switch (NE) {
     case 16: return launch_dst_16(a, mode, st);

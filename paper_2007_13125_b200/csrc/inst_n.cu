@@ -10,12 +10,12 @@
 namespace pint {
 
 // opt in to `smem` bytes of dynamic shared memory and return SMs x resident CTAs (0 on error)
-static long persistent_grid(const void* kern, int smem) {
+static long persistent_grid(const void* kern, int smem, int threads = TPB) {
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
   int dev = 0, nsm = 148, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, TPB, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem);
   return (long)nsm * (per > 0 ? per : 1);
 }
 
@@ -57,6 +57,23 @@ static cudaError_t go_cq_split(const TPassArgs& a, long ntiles, cudaStream_t st)
   const long grid = ntiles < resident ? ntiles : resident;
   kern<<<(unsigned)grid, TPB, smem, st>>>(a, ntiles);
   return cudaGetLastError();
+}
+
+cudaError_t PINT_CAT(launch_tpass_cq_fused_, PINT_N)(const CQArgs& a, cudaStream_t st) {
+#if PINT_N == 1024 || PINT_N == 256
+  constexpr int N1 = PINT_N == 1024 ? 32 : 16;
+  using G = CQCfg<N1>;
+  auto kern = tpass_cq_fused_kernel<N1>;
+  static const long resident = persistent_grid((const void*)kern, G::SMEM, G::THREADS);
+  if (resident <= 0) return cudaErrorInvalidValue;
+  if (a.ntiles <= 0) return cudaSuccess;
+  const long grid = a.ntiles < resident ? a.ntiles : resident;
+  kern<<<(unsigned)grid, G::THREADS, G::SMEM, st>>>(a);
+  return cudaGetLastError();
+#else
+  (void)a; (void)st;
+  return cudaErrorInvalidValue;
+#endif
 }
 
 cudaError_t PINT_CAT(launch_tpass_cq_split_, PINT_N)(int half, const TPassArgs& a, long ntiles, cudaStream_t st) {

@@ -6,6 +6,7 @@
 #include "dst.cuh"
 #include "fused.cuh"
 #include "newton.cuh"
+#include "cqpass.cuh"
 #include <algorithm>
 
 namespace pint {
@@ -21,6 +22,8 @@ cudaError_t launch_spass_const(SPassConst* out, const double2* sig_p, const doub
 cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStream_t st);
 // CQ FREQ -> H as two kernels (half 0: W -> Z, half 1: Z, W -> H; tpass.cuh)
 cudaError_t launch_tpass_cq_split(int N, int half, const TPassArgs& a, long ntiles, cudaStream_t st);
+// CQ FREQ -> H as one kernel (cqpass.cuh), N in {256, 1024}; UNSUPPORTED lengths return cudaErrorInvalidValue
+cudaError_t launch_tpass_cq_fused(int N, const CQArgs& a, cudaStream_t st);
 // layout remaps and the FD stencil (dispatch.cu)
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);
@@ -59,7 +62,8 @@ cudaError_t launch_line_const(LineConst* lc, const double2* sig_p, const double*
                                 cudaStream_t st);                                                  \
   cudaError_t launch_dst_##NN(const DstArgs& a, int mode, cudaStream_t st);                    \
   cudaError_t launch_tpass_pruned_##NN(const TPassArgs& a, long ntiles, cudaStream_t st);        \
-  cudaError_t launch_tpass_cq_split_##NN(int half, const TPassArgs& a, long ntiles, cudaStream_t st);
+  cudaError_t launch_tpass_cq_split_##NN(int half, const TPassArgs& a, long ntiles, cudaStream_t st);  \
+  cudaError_t launch_tpass_cq_fused_##NN(const CQArgs& a, cudaStream_t st);
 PINT_DECLARE_N(16)
 PINT_DECLARE_N(32)
 PINT_DECLARE_N(64)

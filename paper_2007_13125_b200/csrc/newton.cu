@@ -55,7 +55,7 @@ cudaError_t launch_resid(const ResidArgs& a, cudaStream_t st) {
 
 cudaError_t launch_resid_cq_time(const double2* U, double2* T, const double* w, long N, long ntiles,
                                  cudaStream_t st) {
-  const int smem = 4096 * (int)sizeof(double2);
+  const int smem = TILE * (int)sizeof(double2);   // one whole tile (fft.cuh TILE) in shared memory
   cudaError_t e = cudaFuncSetAttribute(resid_cq_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const long grid = std::min<long>(ntiles, 148L * 3);

@@ -227,12 +227,12 @@ __global__ void resid_kernel(const ResidArgs a, long total) {
 // all-at-once form whose v-history sits in F_static).  O(N) per element: a self-check, not a pass.
 __global__ void resid_cq_time_kernel(const double2* U, double2* T, const double* w, long N, long ntiles) {
   extern __shared__ double2 tile[];
-  const int WB = (int)(4096 / N);
+  const int WB = (int)(TILE / N);   // tile = all N levels of WB columns (fft.cuh layout)
   for (long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long base = t * 4096;
-    for (int e = threadIdx.x; e < 4096; e += blockDim.x) tile[e] = U[base + e];
+    const long base = t * (long)TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) tile[e] = U[base + e];
     __syncthreads();
-    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
       const int n = e / WB, c = e % WB;
       double2 s = make_double2(0.0, 0.0);
       for (int j = 0; j <= n; ++j) s = cfmar(tile[(n - j) * WB + c], __ldg(&w[j]), s);

@@ -177,6 +177,8 @@ struct pint_plan_s {
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
   double2* wtmp = nullptr;    // [ntiles][k][WB] modal window -> (q, y) staging
   double2* fd = nullptr;      // dense forcing f(t_1..t_N) in the tile layout (pint_set_problem)
+  bool full = false;          // full-array update monitor (CQ plans, PINT_FLAG_FULL_UPDATE_NORM)
+  double2* ufull = nullptr;   // [ntiles][N][WB]: U_m of every level (tile layout) when `full`
   bool has_fd = false;
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
@@ -199,7 +201,8 @@ struct pint_plan_s {
   std::vector<VmmAlloc> vallocs;
   // state
   bool problem_set = false;
-  int stateA = 0;            // 0: A holds H_{m+1} (B holds W_m); 1: A holds U_m (time domain)
+  int stateA = 0;            // 0: A holds H_{m+1} (B holds W_m); 1: A holds U_m (time domain);
+                             // 3: U_m read from `ufull` (full-array monitor; A still holds H_{m+1})
   int wcur = 0;              // wrap[wcur] = last-k levels of the current U_m
   int64_t m = 0, launches = 0;
   double last_upd = -1.0;
@@ -489,7 +492,12 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   }
   const size_t fsmem = fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
   p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
-  p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && fsmem <= 232448u - 64u;
+  // full-array update monitor: the paper's stopping rule; always for CQ plans,
+  // whose kappa-wrap reads every level of U_{m-1}
+  p->full = alpha != 1.0 || (p->flags & PINT_FLAG_FULL_UPDATE_NORM) != 0;
+  if (p->full && (st = dalloc(p, &p->ufull, arr)) != PINT_OK) return bail(st);
+  p->fused_ok = alpha == 1.0 && !(p->flags & (PINT_FLAG_STREAM | PINT_FLAG_DST_PER_ITER)) && !p->full &&
+                fsmem <= 232448u - 64u;
   p->modal = (p->flags & PINT_FLAG_MODAL) != 0;
   if (p->modal) {
     p->Lf = (int)(p->NB * p->WB);    // X / partials indexed by the y-mode j < my
@@ -655,6 +663,7 @@ static TPassArgs targs(pint_plan p) {
   a.nk = p->nk;
   a.nsparse = p->nsparse; a.spar = p->srclist;
   a.ndense = p->ndense; a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat;
+  a.ufull = p->full ? p->ufull : nullptr;
   static const bool nopf = getenv("PINT_NO_PREFETCH") != nullptr;   // A/B switch (profiling)
   a.prefetch = nopf ? 0 : 1;
   if (p->has_fd) {   // dense forcing: F_static += f(t_n) at every level (streaming path, unpruned)
@@ -675,7 +684,7 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
     CUDA_TRY(cudaEventRecord(e0, p->stream));
   }
   const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 256 &&
-                      p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT) && !p->has_fd;
+                      p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT) && !p->has_fd && !p->full;
   // CQ iteration: two kernels of two transforms each (tpass.cuh "CQ T-pass split"); PINT_CQ_MONO=1
   // keeps the single four-transform kernel (A/B)
   static const bool mono = getenv("PINT_CQ_MONO") != nullptr;
@@ -1227,16 +1236,28 @@ static pint_status iterate_async(pint_plan p) {
   return PINT_OK;
 }
 
-static pint_status read_update(pint_plan p, double* out) {
+static pint_status read_update_local(pint_plan p, double* out) {
   if (!p->upd_queued) CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
   p->upd_queued = false;
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   TRY(graph_timing_collect(p));
-  double u;
-  std::memcpy(&u, p->updh, sizeof(u));
+  std::memcpy(out, p->updh, sizeof(double));
+  return PINT_OK;
+}
+
+// One iteration and its update norm, max over ranks.  A local error still takes part in the
+// all-reduce (contributing +inf), so the other ranks never block in the collective: they see a
+// non-finite update (pint_wr_solve: DIVERGED) while this rank returns its own error.
+static pint_status step_collective(pint_plan p, double* out) {
+  pint_status st = iterate_async(p);
+  double u = INFINITY;
+  if (st == PINT_OK) st = read_update_local(p, &u);
   if (p->nranks > 1) {
-    if (p->allreduce(&u, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
+    double x = st == PINT_OK ? u : INFINITY;
+    if (p->allreduce(&x, p->actx) != 0) return st != PINT_OK ? st : fail(PINT_ERR_COMM, "allreduce_max callback failed");
+    u = x;
   }
+  if (st != PINT_OK) return st;
   *out = u;
   return PINT_OK;
 }
@@ -1246,9 +1267,8 @@ extern "C" pint_status pint_wr_iterate(pint_plan p, double* update_inf) {
   if (p->nl) return fail(PINT_ERR_STATE, "semilinear plan: use pint_newton_solve");
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   CUDA_TRY(cudaSetDevice(p->device));
-  TRY(iterate_async(p));
   double u;
-  TRY(read_update(p, &u));
+  TRY(step_collective(p, &u));
   if (update_inf) *update_inf = u;
   return PINT_OK;
 }
@@ -1263,8 +1283,7 @@ extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters,
   double u = INFINITY;
   pint_status result = PINT_ERR_NOT_CONVERGED;
   while (it < max_iters) {
-    TRY(iterate_async(p));
-    TRY(read_update(p, &u));
+    TRY(step_collective(p, &u));
     ++it;
     if (!std::isfinite(u)) { result = PINT_ERR_DIVERGED; g_last_error = "update is not finite"; break; }
     if (p->last_upd >= 0.0 && u > p->last_upd) {
@@ -1337,6 +1356,7 @@ static pint_status tpass_nl(pint_plan p, int mode_in, int mode_out, const double
   a.in = in; a.out = out; a.wrap_old = wold; a.wrap_new = wnew;
   a.S = 0; a.nmax = (int)p->N; a.nsparse = 0; a.ndense = 0;
   a.fdense = p->nlR;
+  a.ufull = nullptr;   // the inner WR has its own full-array monitor (nl_diffmax)
   CUDA_TRY(launch_tpass((int)p->N, mode_in, mode_out, p->alpha != 1.0, a, p->ntiles, p->stream));
   ++p->launches;
   return PINT_OK;
@@ -1419,7 +1439,17 @@ extern "C" pint_status pint_newton_solve(pint_plan p, int32_t max_outer, double 
 // output
 // ------------------------------------------------------------------------------------------
 static pint_status materialize(pint_plan p) {
-  if (p->stateA == 1) return PINT_OK;
+  if (p->stateA == 1 || p->stateA == 3) return PINT_OK;
+  if (p->full && !p->fused && !p->nl) {
+    // the full-array monitor keeps U_m of every level in `ufull` (tile layout): no Step-3 pass
+    if (p->modal) {                          // (q, j) modes -> (q, y) into A (H is re-derived later)
+      TRY(dst_y(p, p->ufull, p->A, p->N, p->Qb));
+      p->stateA = 1;
+    } else {
+      p->stateA = 3;
+    }
+    return PINT_OK;
+  }
   if (p->fused && p->modal) {
     // W_m per (q, j) mode into A, U_m = Gamma^{-1} V W_m into B, DST-y back to (q, y) into A
     FusedArgs a = fargs(p, p->X[1 - p->xcur]);
@@ -1439,6 +1469,9 @@ static pint_status materialize(pint_plan p) {
   p->stateA = 1;
   return PINT_OK;
 }
+
+// the materialised U_m (tile layout): A, or the full-array monitor's copy
+static const double2* ucur(pint_plan p) { return p->stateA == 3 ? p->ufull : p->A; }
 
 extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_count, void* U, int32_t mem) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
@@ -1489,20 +1522,21 @@ extern "C" pint_status pint_get_levels(pint_plan p, int64_t n_begin, int64_t n_c
     return PINT_OK;
   }
   TRY(materialize(p));
-  double2* dst = mem == PINT_DEVICE ? (double2*)U : p->B;   // B is free once U_m is in A
+  const double2* usrc = ucur(p);
+  double2* dst = mem == PINT_DEVICE ? (double2*)U : p->B;   // B is free once U_m is in A (or ufull)
   if (p->dim == 1) {
     RemapArgs r{};
-    r.in = p->A; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
+    r.in = usrc; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
     r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = 1;
     CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
   } else if (p->dst_iter) {
     RemapArgs r{};
-    r.in = p->A; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = (int)p->my; r.NB = p->NB;
+    r.in = usrc; r.out = dst; r.count = n_count * p->M; r.WB = p->WB; r.my = (int)p->my; r.NB = p->NB;
     r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = p->Qb;
     CUDA_TRY(launch_remap(r, RM_INT_TO_2D_LEVELS, p->stream));
   } else {
     DstArgs a = dargs(p);
-    a.in = p->A; a.out = dst; a.rows = n_count * p->my; a.n0 = n_begin;
+    a.in = usrc; a.out = dst; a.rows = n_count * p->my; a.n0 = n_begin;
     CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
   }
   ++p->launches;
@@ -1529,7 +1563,7 @@ extern "C" pint_status pint_get_modal_levels(pint_plan p, int64_t n_begin, int64
   TRY(materialize(p));
   double2* dst = mem == PINT_DEVICE ? (double2*)Uq : p->B;
   RemapArgs r{};
-  r.in = p->A; r.out = dst; r.count = n_count * p->my * p->Qb; r.WB = p->WB; r.my = (int)p->my;
+  r.in = ucur(p); r.out = dst; r.count = n_count * p->my * p->Qb; r.WB = p->WB; r.my = (int)p->my;
   r.NB = p->NB; r.N = p->N; r.n0 = n_begin; r.M = p->M; r.Qb = p->Qb;
   CUDA_TRY(launch_remap(r, RM_INT_TO_MODAL, p->stream));
   ++p->launches;
@@ -1624,15 +1658,34 @@ extern "C" pint_status pint_get_timing(pint_plan p, double* tpass_ms, double* sp
   return PINT_OK;
 }
 
+static pint_status residual_local(pint_plan p, double* r_out, double* f_out);
+
 extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* rhs_inf) {
   if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  double r = 0.0, f = 0.0;
+  const pint_status st = residual_local(p, &r, &f);
+  if (p->nranks > 1) {
+    // collective: every rank makes the same all-reduce calls even when its local part failed
+    double bad = st == PINT_OK ? 0.0 : 1.0;
+    if (p->allreduce(&bad, p->actx) != 0) return st != PINT_OK ? st : fail(PINT_ERR_COMM, "allreduce_max callback failed");
+    if (st != PINT_OK) return st;
+    if (bad != 0.0) return fail(PINT_ERR_COMM, "pint_residual failed on another rank");
+    if (p->allreduce(&r, p->actx) != 0 || p->allreduce(&f, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
+  }
+  if (st != PINT_OK) return st;
+  if (residual_inf) *residual_inf = r;
+  if (rhs_inf) *rhs_inf = f;
+  return PINT_OK;
+}
+
+static pint_status residual_local(pint_plan p, double* r_out, double* f_out) {
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
   if (p->nl || p->dst_iter || p->has_fd || (p->alpha != 1.0 && p->modal))
     return fail(PINT_ERR_UNSUPPORTED, "pint_residual: separable data; CQ on the line-solve path");
   CUDA_TRY(cudaSetDevice(p->device));
-  TRY(materialize(p));                     // A: U_m, x in DST modes, y physical (tile layout)
-  const double2* U = p->A;
+  TRY(materialize(p));                     // U_m, x in DST modes, y physical (tile layout)
+  const double2* U = ucur(p);
   if (p->modal) {                          // back to (q, j) modes, where the sources live; B is free
     TRY(dst_y(p, p->A, p->B, p->N, p->Qb));   // here (A keeps U_m, the next iteration re-derives from it)
     U = p->B;
@@ -1644,7 +1697,7 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
   a.U = U; a.src = p->src; a.coef = p->coef; a.wk = p->wk; a.sig_q = p->sig_q; a.out = acc;
   a.mu = p->modal ? p->mu : nullptr;
   if (p->alpha != 1.0) {   // CQ: the full history convolution per column, tile by tile into B (free here)
-    CUDA_TRY(launch_resid_cq_time(p->A, p->B, p->cqw, p->N, p->ntiles, p->stream));
+    CUDA_TRY(launch_resid_cq_time(U, p->B, p->cqw, p->N, p->ntiles, p->stream));
     ++p->launches;
     a.tconv = p->B;
   }
@@ -1655,14 +1708,8 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
   unsigned long long bits[2];
   CUDA_TRY(cudaMemcpyAsync(bits, acc, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
-  double r, f;
-  std::memcpy(&r, &bits[0], sizeof(r));
-  std::memcpy(&f, &bits[1], sizeof(f));
-  if (p->nranks > 1) {
-    if (p->allreduce(&r, p->actx) != 0 || p->allreduce(&f, p->actx) != 0) return fail(PINT_ERR_COMM, "allreduce_max callback failed");
-  }
-  if (residual_inf) *residual_inf = r;
-  if (rhs_inf) *rhs_inf = f;
+  std::memcpy(r_out, &bits[0], sizeof(double));
+  std::memcpy(f_out, &bits[1], sizeof(double));
   return PINT_OK;
 }
 

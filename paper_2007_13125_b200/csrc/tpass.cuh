@@ -70,7 +70,21 @@ struct TPassArgs {
   int nk;                   // X_n = 0 for n >= nk (nk = max(k, max sparse nhi) <= 16)
   const double2* fdense;    // optional dense right-hand side [N][M] in the tile layout, added to
                             // F_static (Newton inner solves: the residual R; set nmax = N)
+  double2* ufull;           // full-array update monitor (PINT_FLAG_FULL_UPDATE_NORM, CQ plans): U_{m-1}
+                            // of every level in the tile layout; FREQ mode compares U_m with it and
+                            // overwrites it with U_m, time-domain (bootstrap) modes store U_0
 };
+
+// |U - ufull[e]| into (upd, nonfinite) and ufull[e] = U (FREQ mode); store only (bootstrap modes)
+template <bool CMP>
+__device__ __forceinline__ void full_monitor(double2* ufull, long e, double2 U, double& upd, bool& nonfinite) {
+  if constexpr (CMP) {
+    const double d = sqrt(cabs2(csub(U, ufull[e])));
+    if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+    upd = fmax(upd, d);
+  }
+  ufull[e] = U;
+}
 
 // table load that the compiler may not hoist above barriers (bounds live ranges in the CQ path)
 template <class T> __device__ __forceinline__ T ldt(const T* p) { return *(volatile const T*)p; }
@@ -219,6 +233,17 @@ __global__ void __launch_bounds__(TPB, CQ ? PINT_CQ_MINB : PINT_TPASS_MINB) tpas
     continue;
   }
 
+  if (a.ufull) {   // full-array monitor: every level of U_m
+#pragma unroll
+    for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+      for (int s = 0; s < TM::RL; ++s) {
+        const int r = j * TM::RL + s;
+        const double2 U = HAVE_U_DIRECT ? v[r] : cscale(v[r], ldt(&a.igs[TM::n(j, s, tid)]));
+        full_monitor<MODE_IN == IN_FREQ>(a.ufull, base + TM::e(j, s, tid), U, upd, nonfinite);
+      }
+  }
+
   __syncthreads();   // sm free: all readers of the last exchange are done
   double2* sW = sm;  // [k][WB] wrap window values of U_m
 #pragma unroll
@@ -357,6 +382,14 @@ __global__ void __launch_bounds__(TPB, PINT_TPASS_MINB) tpass_cq_a_kernel(const 
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = a.in[base + FM::e(t, tid)];
     run_passes<N, +1, false>(v, sm, a.tw, tid);          // u = V W
+    if (a.ufull) {   // full-array monitor: every level of U_m
+#pragma unroll
+      for (int j = 0; j < TM::NJ; ++j)
+#pragma unroll
+        for (int s2 = 0; s2 < TM::RL; ++s2)
+          full_monitor<true>(a.ufull, base + TM::e(j, s2, tid), cscale(v[j * TM::RL + s2], __ldg(&a.igs[TM::n(j, s2, tid)])),
+                             upd, nonfinite);
+    }
     // window levels of U_m = Gamma^{-1} u: monitor and new wrap state
 #pragma unroll
     for (int j = 0; j < TM::NJ; ++j)

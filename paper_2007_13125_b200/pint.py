@@ -25,6 +25,7 @@ PINT_FLAG_DST_PER_ITER = 8
 PINT_NL_ALLEN_CAHN = 1
 PINT_FLAG_REAL_DATA = 16
 PINT_FLAG_MODAL = 32
+PINT_FLAG_FULL_UPDATE_NORM = 64
 
 EXPORTED = [
     "pint_plan_create", "pint_set_problem_separable", "pint_set_initial_guess", "pint_wr_iterate",
@@ -146,7 +147,7 @@ class Plan:
                  device: int = 0, stream: int | None = None, u0_zero: bool = False,
                  rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False,
                  stream_path: bool = False, dst_per_iter: bool = False, real_data: bool = False,
-                 modal: bool = False, fem: bool = False):
+                 modal: bool = False, fem: bool = False, full_update_norm: bool = False):
         """fem=True: 1D P1 finite elements (PINT_OP_FEM1D_DIRICHLET; nodal coefficient vectors)."""
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
@@ -164,7 +165,8 @@ class Plan:
             self._cb = ALLREDUCE_FN(_cb)
         flags = (PINT_FLAG_U0_ZERO if u0_zero else 0) | (PINT_FLAG_FULL_FFT if full_fft else 0) | \
             (PINT_FLAG_STREAM if stream_path else 0) | (PINT_FLAG_DST_PER_ITER if dst_per_iter else 0) | \
-            (PINT_FLAG_REAL_DATA if real_data else 0) | (PINT_FLAG_MODAL if modal else 0)
+            (PINT_FLAG_REAL_DATA if real_data else 0) | (PINT_FLAG_MODAL if modal else 0) | \
+            (PINT_FLAG_FULL_UPDATE_NORM if full_update_norm else 0)
         opt = pint_options(alpha, device, stream or 0, flags, rank, nranks,
                            self._cb, None)
         h = ctypes.c_void_p()
@@ -272,7 +274,9 @@ class Plan:
         return {"tpass_ms": t.value, "spass_ms": s.value, "tpass_launches": tn.value, "spass_launches": sn.value}
 
     def residual(self) -> tuple[float, float]:
-        """(max |residual of the BDF-k scheme at U_m|, max |F_static|) — pint_residual (heat, FD)."""
+        """(max |residual of the BDF-k scheme at U_m|, max |F_static|) — pint_residual: heat and CQ,
+        FD, fully modal and P1-FEM plans (not: CQ on the modal path, semilinear plans,
+        PINT_FLAG_DST_PER_ITER, dense forcing; include/pint.h)."""
         r, f = ctypes.c_double(), ctypes.c_double()
         _check(lib().pint_residual(self._h, ctypes.byref(r), ctypes.byref(f)))
         return r.value, f.value
