@@ -158,7 +158,7 @@ class ClockSampler:
                 "source": "nvml" if self.nv else "nvidia-smi"}
 
 
-def cpu_baseline(prob_name: str, budget_s: float = 30.0):
+def cpu_baseline(prob_name: str, budget_s: float = 30.0, fast: bool = True):
     """The oracle (oracle.wr.wr_naive, as it stands) on host cores, one WR iteration on a bounded
     sample of the workload: same N, k, kappa, alpha and recipe on a reduced spatial grid."""
     from oracle import wr
@@ -182,8 +182,17 @@ def cpu_baseline(prob_name: str, budget_s: float = 30.0):
         sample = f"oracle O2 1 iteration on {prob_name} (full size)"
     t = []
     wr.wr_naive(prob, 1, keep=False, timings=t)
-    return {"value": prob.M * prob.N / t[0], "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": sample, "seconds": t[0]}
+    out = {"value": prob.M * prob.N / t[0], "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": sample, "seconds": t[0], "os_cpu_count": os.cpu_count()}
+    if fast:
+        # SURVEY §8(d) "fast CPU" comparator: the same iteration with library FFTs for the time DFTs and
+        # the CQ wrap (scipy.fft, all host threads; O(MN log N)) and the DST eigen-solves (workers=-1)
+        tf = []
+        wr.wr_naive(prob, 1, keep=False, timings=tf, dft="fft", wrap="fft")
+        out["fast_cpu"] = {"value": prob.M * prob.N / tf[0], "unit": UNIT, "threads": os.cpu_count(),
+                           "kind": "oracle O2 with dft='fft', wrap='fft' (scipy.fft workers=-1)",
+                           "sample": sample, "seconds": tf[0]}
+    return out
 
 
 def run_reference(args):
@@ -193,7 +202,7 @@ def run_reference(args):
     vals, secs = [], []
     base = None
     for _ in range(args.warmup + args.steps):
-        base = cpu_baseline(args.config)
+        base = cpu_baseline(args.config, fast=False)
         vals.append(base["value"])
         secs.append(base["seconds"])
     v = vals[args.warmup:]
@@ -239,6 +248,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-full", action="store_true",
+                    help="e2e reads the FULL converged U (all N levels, pint_get_solution) to the host")
     ap.add_argument("--path", default="fused", choices=["fused", "stream"],
                     help="heat: fused one-kernel iteration (default) or the two-pass streaming one")
     ap.add_argument("--modal", action="store_true",
@@ -307,9 +318,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_dev) as clk:
         e0.record(stream)
-        upd = []
-        for _ in range(args.steps):
-            upd.append(plan.iterate())
+        upd = [plan.run(args.steps)]     # K iterations enqueued back to back, one synchronisation (pint_wr_run)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
@@ -321,8 +330,7 @@ def main():
     # region above, where they would cost small problems several microseconds per iteration)
     plan.set_timing(True)
     with ClockSampler(local_dev) as clk_k:
-        for _ in range(args.steps):
-            plan.iterate()
+        plan.run(args.steps)
         tm = plan.get_timing()
     plan.set_timing(False)
     if world > 1:
@@ -383,6 +391,21 @@ def main():
                                "iteration_frac": 2 * bytes_launch / (ms_step / 1e3) / 1e9 / hbm,
                                "timing_pass_clocks": clk_k.summary()}}
 
+    # materialisation cost: the full U_m = Gamma^{-1} V W_m of all N levels (fused: the STORE_W pass +
+    # the inverse T-pass; CQ: read from the full monitor's copy), measured as pint_get_levels of one
+    # non-window level into device memory (CUDA events on the plan stream; outside the timed region)
+    mat = None
+    if world == 1:
+        lvl = torch.empty((1, prob.M), dtype=torch.complex128, device=dev)
+        plan.iterate()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        plan.get_levels(0, 1, out=lvl)
+        m1.record(stream)
+        torch.cuda.synchronize(dev)
+        mat = {"ms": m0.elapsed_time(m1), "what": "materialise U_m (all N levels) + level 1 through the DST, device"}
+        del lvl
+
     # e2e: the public API with HOST buffers: set_problem(host v) + wr_solve(tol) + final level to host.
     # N > 1: every rank reads its own x-mode slab of the final level (pint_get_modal_levels); the
     # time is the max over ranks.
@@ -394,11 +417,12 @@ def main():
             return t.numpy()
         vh = pinned(prob.v)
         gh = pinned(np.ascontiguousarray(prob.g)) if prob.R else None
+        nlev = prob.N if args.e2e_full else 1
         if world > 1:
             qb, qe = plan.partition()
-            out = torch.empty((1, prob.my, qe - qb), dtype=torch.complex128, pin_memory=True).numpy()
+            out = torch.empty((nlev, prob.my, qe - qb), dtype=torch.complex128, pin_memory=True).numpy()
         else:
-            out = torch.empty((1, prob.M), dtype=torch.complex128, pin_memory=True).numpy()
+            out = torch.empty((nlev, prob.M), dtype=torch.complex128, pin_memory=True).numpy()
         steps, t_tot, its = args.e2e_steps, 0.0, 0
         out_bytes = 0
         statuses = []
@@ -410,9 +434,9 @@ def main():
             plan.set_problem(vh, gh, prob.phi if prob.R else None, prob.dphi if prob.R else None)
             it, u, st = plan.solve(prob.tol, 20, raise_on_fail=False)
             if world > 1:
-                plan.get_modal_levels(prob.N - 1, 1, out)
+                plan.get_modal_levels(prob.N - nlev, nlev, out)
             else:
-                plan.get_levels(prob.N - 1, 1, out)
+                plan.get_levels(prob.N - nlev, nlev, out)
             dt = time.perf_counter() - t0
             if world > 1:
                 tt = torch.tensor([dt], dtype=torch.float64, device=rdev)
@@ -427,7 +451,8 @@ def main():
                "h2d_bytes_per_step": int(vh.nbytes + (prob.g.nbytes if prob.R else 0)),
                "d2h_bytes_per_step": int(out_bytes + 8 * its // steps),
                "what": f"set_problem(pinned host v) + wr_solve(tol={prob.tol:g}) ({its / steps:.1f} iterations) + "
-                       + ("final time level to host" if world == 1 else "each rank's modal slab of the final level to host")
+                       + (("all N levels (pint_get_solution)" if args.e2e_full else "final time level")
+                          + " to host" if world == 1 else "each rank's modal slab of the final level to host")
                        + ", per step (max over ranks); unknowns/s per WR iteration",
                "converged": all(x == pint.PINT_OK for x in statuses), "solve_status": statuses}
         # self-check of the converged e2e solution against the scheme (pint_residual; outside
@@ -458,6 +483,7 @@ def main():
                                  " > L2 126 MB, no flush needed" if path["fused"] else
                                  f"inputs > L2 ({2 * 16 * total_unknowns / 1e9:.1f} GB resident), no flush needed")},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+               "materialize": mat,
                "comm": ({"collective": f"{backend} all_reduce(max) of the update norm, one double per iteration",
                          "backend": backend, "oversubscribed": oversub,
                          "note": (f"{world} ranks time-slice {ndev} GPU(s): launch-path check, not a scaling "

@@ -168,9 +168,17 @@ pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
 pint_status pint_wr_iterate(pint_plan plan, double* update_inf);
 
 /* Iterate until update < tol, or max_iters iterations (PINT_ERR_NOT_CONVERGED), or the update
- * grows 3 consecutive times / is not finite (PINT_ERR_DIVERGED).  *iters, *update_inf may be NULL. */
+ * grows 3 consecutive times / is not finite (PINT_ERR_DIVERGED).  *iters, *update_inf may be NULL.
+ * Fused heat path on one rank: the whole loop runs on the device (a CUDA graph with a while-conditional
+ * node; the stopping rule is evaluated by a kernel after every iteration) — one host synchronisation
+ * per call; same iterates and stop count as the host loop (other paths, timing mode, several ranks). */
 pint_status pint_wr_solve(pint_plan plan, double tol, int32_t max_iters, int32_t* iters,
                           double* update_inf);
+
+/* Run exactly `iters` >= 1 WR iterations (no stopping rule, no divergence guard) with one host
+ * synchronisation at the end; *update_inf (may be NULL) receives the last iteration's update (max over
+ * ranks: one all-reduce per call).  The throughput call of bench.py. */
+pint_status pint_wr_run(pint_plan plan, int32_t iters, double* update_inf);
 
 /* Copy the current iterate U_m, time levels n_begin+1 .. n_begin+n_count (0-based row
  * n_begin .. n_begin+n_count-1 of the [N][M] array), into U [n_count][M] complex in mem.

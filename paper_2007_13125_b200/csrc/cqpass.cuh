@@ -101,7 +101,10 @@ template <int N1> struct CQCfg {
   static constexpr int ROW = N1 * WB + (WB == 4 ? 4 : 0);   // exchange row stride (complex), padded
   static constexpr int BUF = (N1 * ROW > TILE ? N1 * ROW : TILE);
   static constexpr int SMEM = BUF * 16;
-  static constexpr int MINB = N1 == 32 ? 3 : 2;
+#ifndef PINT_CQF_MINB
+#define PINT_CQF_MINB 2
+#endif
+  static constexpr int MINB = N1 == 32 ? PINT_CQF_MINB : 2;
   static constexpr int TCOLS = 128;                         // TMEM columns per CTA (stash of D W + H_static)
 };
 
@@ -111,10 +114,12 @@ struct CQArgs {
   double2* ufull;             // U_{m-1} -> U_m, every level (tile layout)
   double2* wrap_new;          // [ntiles][k][WB] window levels of U_m
   unsigned long long* upd;    // max |U_m - U_{m-1}| as ordered bits
-  const double2* twi;         // [N] e^{+2 pi i (i k2 mod N)/N} at [i N1 + k2]          (inverse transforms)
-  const double2* twz;         // [N] theta^i / N e^{-2 pi i i k2/N}                     (forward, Theta/N)
-  const double2* twx;         // [N] c_x theta^{-i} e^{-2 pi i i k2/N}, c_x = -h^2/(2 N tau^a)
-  const double2* dpr;         // [N] d'_p, eigenvalues of C(-kappa)
+  const double2 *tw0, *tw1, *tw2;   // [N] pass-A tables at [i N1 + k2], all in the inverse direction:
+                              //   0: w^{+i k2}                (u = V W and s = V Z)
+                              //   1: theta^{-i} w^{+i k2}     (z = V^{-1} Theta u = conj V conj(.)  )
+                              //   2: theta^{+i} w^{+i k2}     (H' = V^{-1} Theta^{-1} s, likewise)
+  const double2* dpr;         // [N] (c_x / N) d'_p: d'_p the eigenvalues of C(-kappa), c_x = -h^2/(2 tau^a N)
+                              //     (the 1/N of V^{-1} and c_x of the Theta^{-1} factor, moved onto D')
   const double2* dh;          // [N] (h^2/(2 tau^a)) d_p
   const double2* chat;        // [S][N] DFT of kappa^{n/N} h^2/N c_s(n)  (static right-hand side)
   const double2* src;         // [S][ntiles][WB] spatial sources (DST-x basis)
@@ -136,6 +141,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
                  : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   } while (!done);
+}
+
+// read-only table load that is re-issued at every use (asm volatile: no CSE, no hoisting)
+__device__ __forceinline__ double2 ldg_nc_v(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
 }
 
 // 4 complex doubles <-> 16 TMEM columns of this thread's lane
@@ -163,35 +175,32 @@ __device__ __forceinline__ void tmem_ld4c(uint32_t addr, double2* x) {
                         __hiloint2double((int)w[4 * j + 3], (int)w[4 * j + 2]));
 }
 
-// One length-N transform on the register set v (thread (i, c): v[t] = x[i + N1 t] on entry and
-// X[i + N1 t] on exit).  PRE = +1/-1: the input is first rotated by e^{PRE i pi t / N1} (the
-// per-register part of a folded Theta^{+-1}); the pass-A table tw[i N1 + k2] carries the
-// twiddle w^{DIR i k2} (and the per-thread folded factor).  LAST: after the exchange has been read,
-// barrier and call on_free() (the buffer is free: the next tile's copy may be issued).
-template <int N1, int DIR, int PRE, bool LAST = false, class F>
-__device__ __forceinline__ void cq_xform(double2 (&v)[N1], double2* xb, const double2* __restrict__ tw, int i, int c,
-                                         F&& on_free) {
-  using G = CQCfg<N1>;
-  if constexpr (PRE != 0) {
+// a <- conj(a) for all N1 values: the sign bit of the imaginary parts (integer pipe)
+template <int N1> __device__ __forceinline__ void conj_all(double2 (&v)[N1]) {
 #pragma unroll
-    for (int t = 1; t < N1; ++t) v[t] = crot32(v[t], PRE * t * (32 / N1));
-  }
-  dft_n1<N1, DIR>(v);
-  const double2* tr = tw + i * N1;
-#pragma unroll
-  for (int k2 = (PRE != 0 ? 0 : 1); k2 < N1; ++k2) v[k2] = cmul(v[k2], __ldg(&tr[k2]));
-  __syncthreads();                       // the buffer is free (previous exchange / tile input read)
-#pragma unroll
-  for (int k2 = 0; k2 < N1; ++k2) xb[k2 * G::ROW + i * G::WB + c] = v[k2];
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < N1; ++t) v[t] = xb[i * G::ROW + t * G::WB + c];
-  if constexpr (LAST) {
-    __syncthreads();
-    on_free();
-  }
-  dft_n1<N1, DIR>(v);
+  for (int t = 0; t < N1; ++t) v[t].y = __longlong_as_double(__double_as_longlong(v[t].y) ^ (long long)0x8000000000000000ULL);
 }
+
+// rotations e^{-+ i pi t / N1} of the pre-pass of transforms 1 and 3 (uniform across the warp:
+// constant-cache broadcast)
+static __constant__ double2 cq_rot[2][32] = {
+    {{1.0, 0.0}, {0.995184726672196886245, -0.0980171403295606019942}, {0.980785280403230449126, -0.195090322016128267848}, {0.956940335732208864936, -0.290284677254462367636},
+     {0.923879532511286756128, -0.382683432365089771728}, {0.881921264348355029713, -0.471396736825997648556}, {0.831469612302545237079, -0.555570233019602224743}, {0.773010453362736960811, -0.634393284163645498215},
+     {0.707106781186547524401, -0.707106781186547524401}, {0.634393284163645498215, -0.773010453362736960811}, {0.555570233019602224743, -0.831469612302545237079}, {0.471396736825997648556, -0.881921264348355029713},
+     {0.382683432365089771728, -0.923879532511286756128}, {0.290284677254462367636, -0.956940335732208864936}, {0.195090322016128267848, -0.980785280403230449126}, {0.0980171403295606019942, -0.995184726672196886245},
+     {0.0, -1.0}, {-0.0980171403295606019942, -0.995184726672196886245}, {-0.195090322016128267848, -0.980785280403230449126}, {-0.290284677254462367636, -0.956940335732208864936},
+     {-0.382683432365089771728, -0.923879532511286756128}, {-0.471396736825997648556, -0.881921264348355029713}, {-0.555570233019602224743, -0.831469612302545237079}, {-0.634393284163645498215, -0.773010453362736960811},
+     {-0.707106781186547524401, -0.707106781186547524401}, {-0.773010453362736960811, -0.634393284163645498215}, {-0.831469612302545237079, -0.555570233019602224743}, {-0.881921264348355029713, -0.471396736825997648556},
+     {-0.923879532511286756128, -0.382683432365089771728}, {-0.956940335732208864936, -0.290284677254462367636}, {-0.980785280403230449126, -0.195090322016128267848}, {-0.995184726672196886245, -0.0980171403295606019942}},
+    {{1.0, 0.0}, {0.995184726672196886245, 0.0980171403295606019942}, {0.980785280403230449126, 0.195090322016128267848}, {0.956940335732208864936, 0.290284677254462367636},
+     {0.923879532511286756128, 0.382683432365089771728}, {0.881921264348355029713, 0.471396736825997648556}, {0.831469612302545237079, 0.555570233019602224743}, {0.773010453362736960811, 0.634393284163645498215},
+     {0.707106781186547524401, 0.707106781186547524401}, {0.634393284163645498215, 0.773010453362736960811}, {0.555570233019602224743, 0.831469612302545237079}, {0.471396736825997648556, 0.881921264348355029713},
+     {0.382683432365089771728, 0.923879532511286756128}, {0.290284677254462367636, 0.956940335732208864936}, {0.195090322016128267848, 0.980785280403230449126}, {0.0980171403295606019942, 0.995184726672196886245},
+     {0.0, 1.0}, {-0.0980171403295606019942, 0.995184726672196886245}, {-0.195090322016128267848, 0.980785280403230449126}, {-0.290284677254462367636, 0.956940335732208864936},
+     {-0.382683432365089771728, 0.923879532511286756128}, {-0.471396736825997648556, 0.881921264348355029713}, {-0.555570233019602224743, 0.831469612302545237079}, {-0.634393284163645498215, 0.773010453362736960811},
+     {-0.707106781186547524401, 0.707106781186547524401}, {-0.773010453362736960811, 0.634393284163645498215}, {-0.831469612302545237079, 0.555570233019602224743}, {-0.881921264348355029713, 0.471396736825997648556},
+     {-0.923879532511286756128, 0.382683432365089771728}, {-0.956940335732208864936, 0.290284677254462367636}, {-0.980785280403230449126, 0.195090322016128267848}, {-0.995184726672196886245, 0.0980171403295606019942}},
+};
 
 template <int N1>
 __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_fused_kernel(const CQArgs a) {
@@ -257,44 +266,68 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     }
-    auto none = [] {};
-    // ---- u = V W ----
-    cq_xform<N1, +1, 0>(v, buf, a.twi, i, c, none);
-    // ---- U_m = Gamma^{-1} u: full-array monitor, U_m -> ufull, window -> wrap state ----
+    // ---- the four length-N transforms, ONE code body (instruction-cache footprint), all run as
+    // inverse 4-step transforms (a forward one is conj . inverse . conj):
+    //   x = 0: u = V W                      -> U_m = Gamma^{-1} u: monitor, U_m -> ufull, window
+    //   x = 1: z = V^{-1} Theta u           -> Z = (c_x / N) D' z
+    //   x = 2: s = V Z
+    //   x = 3: H' = V^{-1} Theta^{-1} s     -> + stash; the buffer is free after its exchange
+#pragma unroll 1
+    for (int x = 0; x < 4; ++x) {
+      const bool fwd = (x & 1) != 0;
+      if (fwd) {
+        conj_all<N1>(v);
 #pragma unroll
-    for (int t = 0; t < N1; ++t) {
-      const int n = i + N1 * t;
-      const double2 U = cscale(v[t], __ldg(&a.igs[n]));
-      const long e = base + (long)n * WB + c;
-      const double d = sqrt(cabs2(csub(U, a.ufull[e])));
-      if (!(d <= 1.7976931348623157e308)) nonfinite = true;
-      upd = fmax(upd, d);
-      a.ufull[e] = U;
-      if (t == N1 - 1 && i >= N1 - a.k) a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
-    }
-    // ---- z = V^{-1} Theta u  (Theta / N folded), Z = D' z ----
-    cq_xform<N1, -1, +1>(v, buf, a.twz, i, c, none);
-#pragma unroll
-    for (int t = 0; t < N1; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[i + N1 * t]));
-    // ---- s = V Z ----
-    cq_xform<N1, +1, 0>(v, buf, a.twi, i, c, none);
-    // ---- H' = V^{-1} (c_x Theta^{-1} s); the buffer is free once its exchange is read ----
-    cq_xform<N1, -1, -1, true>(v, buf, a.twx, i, c, [&] {
-      if (tid == 0 && nt < ntiles) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        tile_bulk_load(sbuf, a.in + nt * (long)TILE, TILE * 16, sbar);
+        for (int t = 1; t < N1; ++t) v[t] = cmul(v[t], cq_rot[x >> 1][t * (32 / N1)]);
       }
-    });
+      dft_n1<N1, +1>(v);
+      {
+        const double2* tr = (fwd ? (x == 1 ? a.tw1 : a.tw2) : a.tw0) + i * N1;   // (no runtime index into
+                                                                                 //  the parameter struct)
+#pragma unroll
+        for (int k2 = 0; k2 < N1; ++k2) v[k2] = cmul(v[k2], ldg_nc_v(&tr[k2]));
+      }
+      __syncthreads();                       // the buffer is free (previous exchange / tile input read)
+#pragma unroll
+      for (int k2 = 0; k2 < N1; ++k2) buf[k2 * G::ROW + i * G::WB + c] = v[k2];
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < N1; ++t) v[t] = buf[i * G::ROW + t * G::WB + c];
+      if (x == 3) {
+        __syncthreads();
+        if (tid == 0 && nt < ntiles) {       // the next tile lands while this one finishes
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          tile_bulk_load(sbuf, a.in + nt * (long)TILE, TILE * 16, sbar);
+        }
+      }
+      dft_n1<N1, +1>(v);
+      if (fwd) conj_all<N1>(v);
+      if (x == 0) {
+#pragma unroll
+        for (int t = 0; t < N1; ++t) {
+          const int n = i + N1 * t;
+          const double2 U = cscale(v[t], __ldg(&a.igs[n]));
+          const double d = sqrt(cabs2(csub(U, a.ufull[base + (long)n * WB + c])));
+          if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+          upd = fmax(upd, d);
+          a.ufull[base + (long)n * WB + c] = U;
+          if (t == N1 - 1 && i >= N1 - a.k) a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
+        }
+      } else if (x == 1) {
+#pragma unroll
+        for (int t = 0; t < N1; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[i + N1 * t]));
+      }
+    }
     // ---- H = H' + D W + H_static ----
     const unsigned long long ef = l2_evict_first();
 #pragma unroll
     for (int q = 0; q < N1 / 4; ++q) {
-      double2 x[4];
-      tmem_ld4c(tst + 16 * q, x);
+      double2 xs[4];
+      tmem_ld4c(tst + 16 * q, xs);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int p = i + N1 * (4 * q + j);
-        st_hint(&a.out[base + (long)p * WB + c], cadd(v[4 * q + j], x[j]), ef);
+        st_hint(&a.out[base + (long)p * WB + c], cadd(v[4 * q + j], xs[j]), ef);
       }
     }
   }

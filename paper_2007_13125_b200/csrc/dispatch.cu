@@ -130,8 +130,7 @@ cudaError_t launch_spass_const(SPassConst* out, const double2* sig_p, const doub
 }
 
 cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
-  static const bool staged = getenv("PINT_SPASS_STAGED") != nullptr;   // A/B switches for profiling
-  static const bool direct = getenv("PINT_SPASS_DIRECT") != nullptr;
+  constexpr bool staged = false, direct = false;   // (the staged strip kernel serves C = 1 and WB = 1)
   // two warps per line (C/2 rows per lane) when the line needs C >= 4 rows per lane
   if (!staged && !direct && a.WB >= 2 && C >= 4 && a.lc) {
     switch (C) {

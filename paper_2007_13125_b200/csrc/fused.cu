@@ -49,17 +49,20 @@ static cudaError_t fused_c(int C, const FusedArgs& a, long grid, cudaStream_t st
 }
 
 cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st) {
+  // one warp per line; iteration launches keep the window sums in TMEM, the materialising launch
+  // (store_w) has no window
+  if (lanes != 32 || !(tm || store_w)) return cudaErrorInvalidValue;
   const long grid = a.Qb * a.nch;
-  if (store_w) return lanes == 64 ? fused_c<64, true, false>(C, a, grid, st) : fused_c<32, true, false>(C, a, grid, st);
-  if (lanes == 64) return tm ? fused_c<64, false, true>(C, a, grid, st) : fused_c<64, false, false>(C, a, grid, st);
-  return tm ? fused_c<32, false, true>(C, a, grid, st) : fused_c<32, false, false>(C, a, grid, st);
+  if (store_w) return fused_c<32, true, false>(C, a, grid, st);
+  return fused_c<32, false, true>(C, a, grid, st);
 }
 
 template <int C, int LANES>
 static int fused_occ(int k, bool tm) {
   int per = 0;
   const size_t smem = fused_smem_bytes(LANES, C, k, tm);
-  auto kern = tm ? wr_fused_kernel<C, LANES, false, true> : wr_fused_kernel<C, LANES, false, false>;
+  if (!tm) return 0;
+  auto kern = wr_fused_kernel<C, LANES, false, true>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FCfg<LANES>::THREADS, smem) != cudaSuccess) return 0;
   return per;
@@ -81,7 +84,8 @@ static int fused_occ_c(int C, int k, bool tm) {
 // resident CTAs per SM; with the window sums (and X) in TMEM each CTA allocates its columns, so at
 // most 512 / columns of them (C <= 16: 256 columns, two CTAs)
 int fused_ctas_per_sm(int lanes, int C, int k, bool tm) {
-  const int per = lanes == 64 ? fused_occ_c<64>(C, k, tm) : fused_occ_c<32>(C, k, tm);
+  if (lanes != 32) return 0;
+  const int per = fused_occ_c<32>(C, k, tm);
   if (!tm) return per;
   const int cols = lanes == 32 && C <= 16 ? 256 : 512;
   return std::min(per, 512 / cols);
@@ -103,23 +107,60 @@ cudaError_t launch_modal(bool store_w, const FusedArgs& a, cudaStream_t st) {
 
 cudaError_t launch_finish(const FinishArgs& a0, int mode, cudaStream_t st) {
   FinishArgs a = a0;
-  static const bool two = getenv("PINT_FINISH_TWO_KERNELS") != nullptr;   // A/B: reduce, then finish
-  if (mode == FIN_PARTIALS && a.nch > 16 && !two) {   // many chunks: warp per row, reduce + finish
+  if (mode == FIN_PARTIALS && a.nch > 16) {   // many chunks: warp per row, reduce + finish
     const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
     wr_reduce_finish_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);
     return cudaGetLastError();
-  }
-  if (mode == FIN_PARTIALS && a.nch > 16) {  // many chunks: reduce them first, warp-parallel
-    const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
-    wr_reduce_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    a.nch = 1;                 // the sums sit in chunk 0; the chunk stride stays a0.nch
   }
   const long total = a.Qb * a.Lf;
   const long blocks = std::min<long>((total + TPB - 1) / TPB, 148L * 8);
   if (blocks <= 0) return cudaSuccess;
   wr_finish_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a, mode);
+  return cudaGetLastError();
+}
+
+// one thread: the host loop's stopping rule (pint.cu, pint_wr_solve), then the while-node condition
+__global__ void wr_loop_ctl_kernel(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h) {
+  if (s->done) {
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
+  const double u = __longlong_as_double((long long)*upd);
+  s->u = u;
+  s->it += 1;
+  int stop = 0;
+  if (s->guard) {
+    if (!(u <= 1.7976931348623157e308)) {
+      s->status = 2;
+      stop = 1;
+    } else {
+      if (s->last >= 0.0 && u > s->last) {
+        if (++s->inc >= 3) {
+          s->status = 3;
+          stop = 1;
+        }
+      } else {
+        s->inc = 0;
+      }
+      s->last = u;
+      if (!stop && u < s->tol) {
+        s->status = 0;
+        stop = 1;
+      }
+    }
+  }
+  if (!stop && s->it >= s->max_it) {
+    s->status = 1;
+    stop = 1;
+  }
+  if (stop) {
+    s->done = 1;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+cudaError_t launch_loop_ctl(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h, cudaStream_t st) {
+  wr_loop_ctl_kernel<<<1, 1, 0, st>>>(s, upd, h);
   return cudaGetLastError();
 }
 

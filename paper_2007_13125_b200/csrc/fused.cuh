@@ -59,9 +59,8 @@ struct FusedArgs {
   const double* mu;        // fully modal path (PINT_FLAG_MODAL): [L] mu_j = 4 sin^2(j pi h_y / 2)
   const double2* sig_p;    // modal path: [N] h^2 d_p / tau^a
   const double* sig_q;     // modal path: [Qb] h^2 lambda_q
-  int dbg;                 // profiling only (PINT_FUSED_DBG): 1 skip solves, 2 skip window, 4 skip synthesis,
-                           // 8 u-form recurrences on every line
-  int reserved;            // zero: keeps the struct free of padding (the graph replay memcmp's it)
+  const int* skip;         // device-side WR loop (pint_wr_solve / pint_wr_run graphs): the kernel returns
+                           // at once when *skip != 0 (the loop stopped inside an unrolled pair)
   unsigned long long* upd_reset;   // iteration launches: the update monitor, zeroed by block 0 before
                                    // the finish kernel accumulates into it (replaces a memset)
 };
@@ -427,7 +426,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
   const int NG = N / FG;
   const int i1 = i + 1;
   // ---- Step 3 (window of group i) for all rows of this thread ----
-  if (WINDOW && !(a.dbg & 2)) {
+  if (WINDOW) {
     const double hw = (i == 0 || 16 * i == N) ? 1.0 : 2.0;      // half spectrum: pair weight
     double2 tww[8];
 #pragma unroll
@@ -482,7 +481,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
     }
   }
   // ---- Step 1 (synthesis of group i + 1) in place ----
-  if (next && !(a.dbg & 4)) {
+  if (next) {
     double2 xv[RPT][8];
     if constexpr (XT) {
       constexpr int XC = 4 * NKC;
@@ -559,8 +558,17 @@ struct FinishArgs {
   long N, Qb;
   int L, Lf, Lpad, WB, NB, k, nk, nsparse, nch;
   int pstride;             // chunks per x-mode in the memory layout of P; nch = how many are summed
+  const int* skip;         // device-side WR loop: return at once when *skip != 0 (see FusedArgs)
 };
-static_assert(sizeof(FinishArgs) == 144, "FinishArgs must stay padding-free");
+static_assert(sizeof(FinishArgs) == 152, "FinishArgs must stay padding-free");
+
+// Device-side WR loop (pint_wr_solve without a host round trip per iteration): the state of the
+// stopping rule of pint_wr_solve (update < tol, max_iters, 3 consecutive increases or a non-finite
+// update: PAPER.md:1747-1748), advanced by wr_loop_ctl_kernel after every iteration.
+struct LoopCtl {
+  int it, max_it, status, done, inc, guard;   // status: 0 OK, 1 max_iters, 2 non-finite, 3 three increases
+  double tol, last, u;                        // last < 0: no previous update
+};
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
 
@@ -583,6 +591,7 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr
   extern __shared__ double2 fsm[];
   constexpr int LF = LANES * C;
   constexpr bool TMA = TM && !STORE_W;                  // TMEM accumulators in use
+  if (a.skip && *(volatile const int*)a.skip) return;   // device-side loop already stopped
   if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
   __shared__ uint32_t tbase;
   double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
@@ -651,9 +660,9 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr
 #endif
   for (int i = g0; i < g1; ++i) {
     PINT_TS(t0);
-    if (!(a.dbg & 1)) {
+    {
       const LineConst& lcl = slc[line];
-      if (cabs2(lcl.u) >= FUSED_AF_U2 && !(a.dbg & 8))
+      if (cabs2(lcl.u) >= FUSED_AF_U2)
         fused_solve<C, LANES, STORE_W, true>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
       else
         fused_solve<C, LANES, STORE_W, false>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
@@ -738,6 +747,7 @@ template <bool STORE_W>
 __global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const FusedArgs a) {
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  if (a.skip && *(volatile const int*)a.skip) return;   // device-side loop already stopped
   if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
   if (gw >= a.Qb * (long)a.L) return;                       // warp-uniform
   const long q = gw / a.L;
@@ -847,6 +857,7 @@ __device__ __forceinline__ void finish_row(const FinishArgs& a, long q, int y, c
 // many chunks (nch > 16, 1D problems): one warp per row sums the chunks' window sums (lanes over
 // chunks, shuffle tree), then lane 0 runs the finish step — one kernel instead of reduce + finish
 __global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs a) {
+  if (a.skip && *(volatile const int*)a.skip) return;
   const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   double updl = 0.0;
@@ -872,25 +883,9 @@ __global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs 
   block_max_atomic(updl, a.upd);
 }
 
-__global__ void __launch_bounds__(TPB) wr_reduce_kernel(const FinishArgs a) {
-  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= a.Qb * (long)a.Lf) return;
-  const long q = gw / a.Lf;
-  const int y = (int)(gw % a.Lf);
-  for (int j = 0; j < a.k; ++j) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int c = lane; c < a.nch; c += 32) s = cadd(s, a.P[((q * a.pstride + c) * a.k + j) * a.Lf + y]);
-    for (int o = 16; o > 0; o >>= 1) {
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-    }
-    __syncwarp();
-    if (lane == 0) const_cast<double2*>(a.P)[((q * a.pstride) * a.k + j) * a.Lf + y] = s;
-  }
-}
 
 __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int mode) {
+  if (a.skip && *(volatile const int*)a.skip) return;
   double updl = 0.0;
   bool nonfinite = false;
   const long total = a.Qb * a.Lf;

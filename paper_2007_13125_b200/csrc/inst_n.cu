@@ -64,7 +64,17 @@ cudaError_t PINT_CAT(launch_tpass_cq_fused_, PINT_N)(const CQArgs& a, cudaStream
   constexpr int N1 = PINT_N == 1024 ? 32 : 16;
   using G = CQCfg<N1>;
   auto kern = tpass_cq_fused_kernel<N1>;
-  static const long resident = persistent_grid((const void*)kern, G::SMEM, G::THREADS);
+  // persistent grid of MINB CTAs per SM (the kernel's launch bound; three 67 KB exchange buffers and
+  // 3 x 128 TMEM columns per SM), with the full shared-memory carve-out
+  static const long resident = [&]() -> long {
+    if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess) return 0;
+    if (persistent_grid((const void*)kern, G::SMEM, G::THREADS) <= 0) return 0;   // sets the smem attribute
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return (long)nsm * G::MINB;
+  }();
   if (resident <= 0) return cudaErrorInvalidValue;
   if (a.ntiles <= 0) return cudaSuccess;
   const long grid = a.ntiles < resident ? a.ntiles : resident;

@@ -101,36 +101,6 @@ static std::vector<ld> cq_weights(int k, ld alpha, long n) {
 // ------------------------------------------------------------------------------------------
 // plan
 // ------------------------------------------------------------------------------------------
-// ---- driver VMM allocation with an explicit compression type (space-time buffers) ----
-struct VmmApi {
-  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
-  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
-  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
-  CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
-  CUresult (*gran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
-  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
-  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
-  CUresult (*vfree)(CUdeviceptr, size_t) = nullptr;
-  bool ok = false;
-};
-static VmmApi& vmm() {
-  static VmmApi v;
-  static bool init = false;
-  if (!init) {
-    init = true;
-    auto get = [](const char* n, void** f) {
-      cudaDriverEntryPointQueryResult q;
-      return cudaGetDriverEntryPoint(n, f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess;
-    };
-    v.ok = get("cuMemCreate", (void**)&v.create) && get("cuMemAddressReserve", (void**)&v.reserve) &&
-           get("cuMemMap", (void**)&v.map) && get("cuMemSetAccess", (void**)&v.access) &&
-           get("cuMemGetAllocationGranularity", (void**)&v.gran) && get("cuMemUnmap", (void**)&v.unmap) &&
-           get("cuMemRelease", (void**)&v.release) && get("cuMemAddressFree", (void**)&v.vfree);
-  }
-  return v;
-}
-struct VmmAlloc { CUdeviceptr ptr; size_t size; CUmemGenericAllocationHandle h; };
-
 struct pint_plan_s {
   int64_t M, N, mx, my;
   int k, dim, flags, rank, nranks;
@@ -160,6 +130,8 @@ struct pint_plan_s {
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
   double2* sig_p = nullptr;
   double* sig_q = nullptr;
+  double2 *cq_twi = nullptr, *cq_twz = nullptr, *cq_twx = nullptr;   // one-kernel CQ T-pass (cqpass.cuh):
+  double2* cq_dpr = nullptr;                                         // pass-A tables, (c_x / N) d'_p
   double2* phys = nullptr;   // [2][M] physical staging (v, A v)
   double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
@@ -183,8 +155,8 @@ struct pint_plan_s {
   bool fused_ok = false;      // plan-level eligibility (alpha = 1, smem fits, not PINT_FLAG_STREAM)
   bool fused = false;         // active for the current problem (also needs nk <= 8)
   int Cf = 0, Lf = 0, nch = 1, gpc = 1;
-  int flanes = 32;            // fused kernel lanes per line: 32 (one warp) or 64 (PINT_FUSED_LANES=64, radix-8 only)
-  bool ftm = true;            // window partial sums in TMEM (PINT_FUSED_TMEM=0: shared memory)
+  int flanes = 32;            // fused kernel lanes per line (one warp)
+  bool ftm = true;            // window partial sums in TMEM
   double2* X[2] = {nullptr, nullptr};   // [Qb][8][Lf]
   int xcur = 0;               // X[xcur] feeds the next iteration; X[1-xcur] produced W_m
   LineConst* lc = nullptr;    // [Qb][N]
@@ -198,7 +170,6 @@ struct pint_plan_s {
   double2 *nlU = nullptr, *nlR = nullptr, *nlC = nullptr, *nlPiv = nullptr, *nlT[2] = {nullptr, nullptr};
   double *nlWt = nullptr, *nlAnl = nullptr;
   std::vector<void*> allocs;
-  std::vector<VmmAlloc> vallocs;
   // state
   bool problem_set = false;
   int stateA = 0;            // 0: A holds H_{m+1} (B holds W_m); 1: A holds U_m (time domain);
@@ -222,6 +193,14 @@ struct pint_plan_s {
   FinishArgs gfin[8];
   cudaEvent_t gev[8][4] = {};
   cudaEvent_t* cap_ev = nullptr;   // during a timing capture: the slot's events
+  // device-side WR loop (pint_wr_solve on the fused path): a graph with a while-conditional node whose
+  // body runs two iterations (both ping-pong parities) each followed by the stopping-rule kernel
+  const int* cap_skip = nullptr;   // during its capture: the kernels' early-exit flag (LoopCtl::done)
+  LoopCtl* lctl = nullptr;         // device state of the loop
+  LoopCtl* lctl_h = nullptr;       // pinned host copy
+  cudaGraphExec_t lexec[4] = {};   // per (wcur, xcur) at loop entry
+  FusedArgs lfa[4][2];
+  FinishArgs lfin[4][2];
   int gpending = -1;          // slot whose event nodes ran last and are not yet accumulated
   int64_t glaunch = 0;        // kernels per graph replay
 };
@@ -230,9 +209,6 @@ struct pint_plan_s {
 
 template <class T>
 static pint_status dalloc(pint_plan p, T** ptr, size_t count);
-
-// comp: 0 = CU_MEM_ALLOCATION_COMP_NONE, 1 = CU_MEM_ALLOCATION_COMP_GENERIC
-static pint_status valloc(pint_plan p, double2** ptr, size_t count, int comp);
 
 template <class T>
 static pint_status dalloc(pint_plan p, T** ptr, size_t count) {
@@ -306,34 +282,6 @@ static void fft_ld(std::vector<cld>& x, int sign) {
   }
 }
 
-static pint_status valloc(pint_plan p, double2** ptr, size_t count, int comp) {
-  VmmApi& v = vmm();
-  if (!v.ok) return dalloc(p, ptr, count);
-  CUmemAllocationProp prop{};
-  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  prop.location.id = p->device;
-  prop.allocFlags.compressionType = comp ? CU_MEM_ALLOCATION_COMP_GENERIC : CU_MEM_ALLOCATION_COMP_NONE;
-  size_t g = 0;
-  if (v.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || g == 0) return dalloc(p, ptr, count);
-  const size_t bytes = ((std::max<size_t>(count, 1) * sizeof(double2) + g - 1) / g) * g;
-  VmmAlloc a{0, bytes, 0};
-  if (v.create(&a.h, bytes, &prop, 0) != CUDA_SUCCESS) return fail(PINT_ERR_ALLOC, "cuMemCreate failed");
-  if (v.reserve(&a.ptr, bytes, g, 0, 0) != CUDA_SUCCESS) { v.release(a.h); return fail(PINT_ERR_ALLOC, "cuMemAddressReserve failed"); }
-  if (v.map(a.ptr, bytes, 0, a.h, 0) != CUDA_SUCCESS) { v.vfree(a.ptr, bytes); v.release(a.h); return fail(PINT_ERR_ALLOC, "cuMemMap failed"); }
-  CUmemAccessDesc d{};
-  d.location = prop.location;
-  d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (v.access(a.ptr, bytes, &d, 1) != CUDA_SUCCESS) {
-    v.unmap(a.ptr, bytes); v.vfree(a.ptr, bytes); v.release(a.h);
-    return fail(PINT_ERR_ALLOC, "cuMemSetAccess failed");
-  }
-  p->vallocs.push_back(a);
-  p->dev_bytes += (int64_t)bytes;
-  *ptr = (double2*)a.ptr;
-  return PINT_OK;
-}
-
 static void free_plan(pint_plan p) {
   if (!p) return;
   cudaSetDevice(p->device);
@@ -349,11 +297,12 @@ static void free_plan(pint_plan p) {
               (double)h[5 + 4 * w], (double)h[6 + 4 * w], (double)h[7 + 4 * w]);
   }
   for (void* q : p->allocs) cudaFree(q);
-  for (auto& a : p->vallocs) { vmm().unmap(a.ptr, a.size); vmm().vfree(a.ptr, a.size); vmm().release(a.h); }
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   for (auto& e : p->tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : p->sev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (cudaGraphExec_t g : p->gexec) if (g) cudaGraphExecDestroy(g);
+  for (cudaGraphExec_t g : p->lexec) if (g) cudaGraphExecDestroy(g);
+  if (p->lctl_h) cudaFreeHost(p->lctl_h);
   for (auto& ev : p->gev) for (cudaEvent_t e : ev) if (e) cudaEventDestroy(e);
   if (p->updh) cudaFreeHost(p->updh);
   if (p->stage) cudaFreeHost(p->stage);
@@ -445,18 +394,8 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
 
   const size_t arr = (size_t)p->ntiles * TILE;
   pint_status st;
-  {
-    // space-time buffers: PINT_ALLOC=vmm (no compression) | vmm_comp (generic compression) | default cudaMalloc
-    const char* al = getenv("PINT_ALLOC");
-    const int mode = al ? (std::string(al) == "vmm" ? 1 : (std::string(al) == "vmm_comp" ? 2 : 0)) : 0;
-    if (mode) {
-      if ((st = valloc(p, &p->A, arr, mode == 2)) != PINT_OK) return bail(st);
-      if ((st = valloc(p, &p->B, arr, mode == 2)) != PINT_OK) return bail(st);
-    } else {
-      if ((st = dalloc(p, &p->A, arr)) != PINT_OK) return bail(st);
-      if ((st = dalloc(p, &p->B, arr)) != PINT_OK) return bail(st);
-    }
-  }
+  if ((st = dalloc(p, &p->A, arr)) != PINT_OK) return bail(st);   // space-time buffers (H / W, U staging)
+  if ((st = dalloc(p, &p->B, arr)) != PINT_OK) return bail(st);
   for (int i = 0; i < 2; ++i)
     if ((st = dalloc(p, &p->wrap[i], (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
   if ((st = dalloc(p, &p->tw, N)) != PINT_OK) return bail(st);
@@ -476,19 +415,14 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (ce != cudaSuccess) { p->updh = nullptr; return bail(fail(PINT_ERR_ALLOC, std::string("cudaHostAlloc: ") + cudaGetErrorString(ce))); }
   if ((st = dalloc(p, &p->phys, 2 * (size_t)M)) != PINT_OK) return bail(st);
   if (dim == 2 && (st = dalloc(p, &p->twE, NE)) != PINT_OK) return bail(st);
-  // fused heat iteration: v2 = two warps per line (64 lanes x Cf rows), v1 = one warp (32 x Cf);
-  // 8 lines + k window rows in smem
+  // fused heat iteration: one warp per line (32 lanes x Cf rows), window sums in TMEM; 8 lines in smem
   {
-    const char* fl = getenv("PINT_FUSED_LANES");
-    p->flanes = (fl && std::string(fl) == "64") ? 64 : 32;
+    p->flanes = 32;
     int Cf = 1;
     while (p->flanes * Cf < L) Cf *= 2;
     p->Cf = Cf;
     p->Lf = p->flanes * Cf;
-  }
-  {
-    const char* ft = getenv("PINT_FUSED_TMEM");
-    p->ftm = !(ft && std::string(ft) == "0");
+    p->ftm = true;
   }
   const size_t fsmem = fused_smem_bytes(p->flanes, p->Cf, k, p->ftm);
   p->dst_iter = (p->flags & PINT_FLAG_DST_PER_ITER) != 0;
@@ -533,10 +467,6 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
       if (eff > beff + 1e-9) { beff = eff; best = c; }
       if (eff >= 0.9) { best = c; break; }
     }
-    if (const char* ov = getenv("PINT_FUSED_NCH")) {   // A/B override (power of two <= NG)
-      const long v = atol(ov);
-      if (v >= 1 && v <= NG && (v & (v - 1)) == 0) best = v;
-    }
     p->nch = (int)best;
     p->gpc = (int)((NG + best - 1) / best);
     for (int i = 0; i < 2; ++i)
@@ -558,6 +488,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   std::vector<ld> w = (alpha == 1.0) ? bdf_weights(k) : cq_weights(k, al, N + 1);
   if (alpha == 1.0) w.resize(N + 1, 0.0L);
   std::vector<double2> tw(N), thp(N), thm(N), dh(N), dpr(N), sigp(N);
+  std::vector<cld> dprl(N);
   std::vector<double> gsf(N), igs(N), gsN(N), wk(k + 1), sigq(p->Qb);
   for (int64_t n = 0; n < N; ++n) {
     const ld ang = 2.0L * PI_L * (ld)n / Nl;
@@ -587,6 +518,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     sigp[pp] = d2(d * ta * hl * hl);
     dh[pp] = d2(d * (hl * hl) * ta / 2.0L);
     dpr[pp] = d2(dq);
+    dprl[pp] = dq;
   }
   for (int64_t ql = 0; ql < p->Qb; ++ql) {
     if (dim == 1) { sigq[ql] = 0.0; continue; }
@@ -610,6 +542,29 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if ((st = h2d(p, p->thm, thm)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_p, sigp)) != PINT_OK) return bail(st);
   if ((st = h2d(p, p->sig_q, sigq)) != PINT_OK) return bail(st);
+  if (alpha != 1.0 && (N == 1024 || N == 256)) {
+    // one-kernel CQ T-pass (cqpass.cuh): 4-step transforms N = N1 x N1; pass-A tables [i][k2] with the
+    // Theta / N and c_x Theta^{-1} factors of the skew-circulant wrap folded in (per-thread part theta^i)
+    const int64_t N1 = N == 1024 ? 32 : 16;
+    // all four transforms run as inverse 4-step transforms (forward = conj . inverse . conj), so the
+    // tables of the forward ones are conjugated: theta^{-+i} w^{+i k2}
+    std::vector<double2> twi(N), twz(N), twx(N), dps(N);
+    for (int64_t i = 0; i < N1; ++i)
+      for (int64_t k2 = 0; k2 < N1; ++k2) {
+        const ld a = 2.0L * PI_L * (ld)((i * k2) % N) / Nl, th = PI_L * (ld)i / Nl;
+        twi[i * N1 + k2] = d2(cld(cosl(a), sinl(a)));                 // w^{+i k2}
+        twz[i * N1 + k2] = d2(cld(cosl(a - th), sinl(a - th)));       // conj(theta^i w^{-i k2})
+        twx[i * N1 + k2] = d2(cld(cosl(a + th), sinl(a + th)));       // conj(theta^{-i} w^{-i k2})
+      }
+    const ld cx = -(hl * hl) * ta / (2.0L * Nl);                     // the chain is linear: 1/N and c_x on D'
+    for (int64_t pp = 0; pp < N; ++pp) dps[pp] = d2(dprl[pp] * (cx / Nl));
+    double2** tabs[4] = {&p->cq_twi, &p->cq_twz, &p->cq_twx, &p->cq_dpr};
+    const std::vector<double2>* vals[4] = {&twi, &twz, &twx, &dps};
+    for (int t = 0; t < 4; ++t) {
+      if ((st = dalloc(p, tabs[t], N)) != PINT_OK) return bail(st);
+      if ((st = h2d(p, *tabs[t], *vals[t])) != PINT_OK) return bail(st);
+    }
+  }
   if (p->C >= 4 && p->WB >= 2) {   // the pair S-pass (C/2 rows per lane) reads its line constants
     if ((st = dalloc(p, &p->slc, (size_t)p->Qb * N)) != PINT_OK) return bail(st);
     ce = launch_spass_const(p->slc, p->sig_p, p->sig_q, N, p->Qb, p->C / 2, (int)L, p->stream);
@@ -664,8 +619,7 @@ static TPassArgs targs(pint_plan p) {
   a.nsparse = p->nsparse; a.spar = p->srclist;
   a.ndense = p->ndense; a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat;
   a.ufull = p->full ? p->ufull : nullptr;
-  static const bool nopf = getenv("PINT_NO_PREFETCH") != nullptr;   // A/B switch (profiling)
-  a.prefetch = nopf ? 0 : 1;
+  a.prefetch = 1;
   if (p->has_fd) {   // dense forcing: F_static += f(t_n) at every level (streaming path, unpruned)
     a.fdense = p->fd;
     a.nmax = (int)p->N;
@@ -685,12 +639,19 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
   }
   const bool pruned = mode_in == IN_FREQ && mode_out == OUT_H && p->alpha == 1.0 && p->N >= 256 &&
                       p->nk <= 16 && p->k <= 8 && !(p->flags & PINT_FLAG_FULL_FFT) && !p->has_fd && !p->full;
-  // CQ iteration: two kernels of two transforms each (tpass.cuh "CQ T-pass split"); PINT_CQ_MONO=1
-  // keeps the single four-transform kernel (A/B)
-  static const bool mono = getenv("PINT_CQ_MONO") != nullptr;
-  const bool split = !mono && p->alpha != 1.0 && mode_in == IN_FREQ && mode_out == OUT_H && !a.fdense && in != out;
+  // CQ iteration: one kernel (cqpass.cuh) for N in {256, 1024}, else two kernels of two transforms each
+  // (tpass.cuh "CQ T-pass split"); dense right-hand sides keep the four-transform tpass_kernel
+  const bool split = p->alpha != 1.0 && mode_in == IN_FREQ && mode_out == OUT_H && !a.fdense && in != out;
   if (pruned) CUDA_TRY(launch_tpass_pruned((int)p->N, a, p->ntiles, p->stream));
-  else if (split) {
+  else if (split && p->cq_twi && p->full) {
+    // one kernel: W -> U_m (full monitor) -> four on-chip transforms -> H (cqpass.cuh)
+    CQArgs c{};
+    c.in = in; c.out = out; c.ufull = p->ufull; c.wrap_new = wnew; c.upd = p->upd;
+    c.tw0 = p->cq_twi; c.tw1 = p->cq_twz; c.tw2 = p->cq_twx; c.dpr = p->cq_dpr; c.dh = p->dh; c.chat = p->cqhat; c.src = p->src;
+    c.igs = p->igs;
+    c.S = p->S; c.k = p->k; c.ntiles = p->ntiles;
+    CUDA_TRY(launch_tpass_cq_fused((int)p->N, c, p->stream));
+  } else if (split) {
     CUDA_TRY(launch_tpass_cq_split((int)p->N, 0, a, p->ntiles, p->stream));      // W -> Z (into out)
     TPassArgs b = a;
     b.in = out; b.vsrc = in; b.chat = p->cqhat;                                   // Z, W -> H
@@ -733,16 +694,14 @@ static FusedArgs fargs(pint_plan p, const double2* X) {
   a.X = X; a.lc = p->lc; a.tw = p->tw; a.src = p->src;
   a.dsrc = p->srclist ? p->srclist + p->nsparse : nullptr; a.chat = p->chat; a.ndense = p->ndense;
   a.P = p->Pp; a.W = p->B;
+  a.skip = p->cap_skip;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.gpc = p->gpc;
   a.half = p->half ? 1 : 0;
   a.mu = p->mu; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
   // X staged in shared memory when it fits next to the lines (TMEM variant: no window sums in smem)
-  static const bool noxs = getenv("PINT_FUSED_NO_XS") != nullptr;   // A/B switch
-  a.xs = (!noxs && p->ftm &&
+  a.xs = (p->ftm &&
           fused_smem_bytes(p->flanes, p->Cf, p->k, true) + (size_t)p->nk * p->Lf * sizeof(double2) <= 232448u - 64u) ? 1 : 0;
-  static const int dbg = getenv("PINT_FUSED_DBG") ? atoi(getenv("PINT_FUSED_DBG")) : 0;   // profiling only
-  a.dbg = dbg;
 #ifdef PINT_FUSED_PROF
   static unsigned long long* prof = nullptr;
   if (!prof) { cudaMalloc(&prof, 256 * 8); cudaMemset(prof, 0, 256 * 8); }
@@ -788,6 +747,7 @@ static FinishArgs finargs(pint_plan p, const double2* wold, double2* wnew, doubl
   a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->upd;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.pstride = p->nch;
+  a.skip = p->cap_skip;
   return a;
 }
 
@@ -1145,10 +1105,99 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // iteration
 // ------------------------------------------------------------------------------------------
 // one fused iteration: update monitor reset, Steps 1-3 (fused kernel), window / X / monitor (finish)
-static pint_status fused_step(pint_plan p) {
+static pint_status fused_kernels(pint_plan p) {
   TRY(fused_pass(p, p->X[p->xcur], false, true));   // Steps 1-3 (block 0 zeroes the update monitor)
   TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
+  return PINT_OK;
+}
+
+static pint_status fused_step(pint_plan p) {
+  TRY(fused_kernels(p));
   CUDA_TRY(cudaMemcpyAsync(p->updh, p->upd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
+  return PINT_OK;
+}
+
+// The device-side WR loop: ONE graph launch and one synchronisation per pint_wr_solve instead of one
+// per iteration.  Graph = while node; body = [fused, finish, ctl] for parity (w, x) and again for
+// the flipped parity; ctl (wr_loop_ctl_kernel) applies pint_wr_solve's stopping rule and clears the
+// condition, and sets `done`, which makes the rest of the body return at once.  Results (iterations,
+// last update, divergence-guard state) are read back from the LoopCtl state.
+static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool guard, int32_t* iters, double* u_out,
+                              int* status) {
+  if (!p->lctl) {
+    TRY(dalloc(p, &p->lctl, 1));
+    CUDA_TRY(cudaHostAlloc((void**)&p->lctl_h, sizeof(LoopCtl), cudaHostAllocDefault));
+  }
+  const int key = p->wcur * 2 + p->xcur;
+  FusedArgs fa[2];
+  FinishArgs fin[2];
+  p->cap_skip = &p->lctl->done;
+  for (int h = 0; h < 2; ++h) {
+    const int w = p->wcur ^ h, x = p->xcur ^ h;
+    fa[h] = fargs(p, p->X[x]);
+    fa[h].upd_reset = p->upd;
+    fin[h] = finargs(p, p->wrap[w], p->wrap[1 - w], p->X[1 - x]);
+  }
+  p->cap_skip = nullptr;
+  if (!p->lexec[key] || memcmp(fa, p->lfa[key], sizeof fa) != 0 || memcmp(fin, p->lfin[key], sizeof fin) != 0) {
+    if (p->lexec[key]) { CUDA_TRY(cudaGraphExecDestroy(p->lexec[key])); p->lexec[key] = nullptr; }
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hnd;
+    cudaError_t e = cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = hnd;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(p->stream, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                           cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) { cudaGraphDestroy(g); return fail(PINT_ERR_CUDA, std::string("loop graph: ") + cudaGetErrorString(e)); }
+    const int64_t l0 = p->launches;
+    const int w0 = p->wcur, x0 = p->xcur;
+    p->cap_skip = &p->lctl->done;
+    pint_status st = PINT_OK;
+    for (int h = 0; h < 2 && st == PINT_OK; ++h) {
+      p->wcur = w0 ^ h;
+      p->xcur = x0 ^ h;
+      st = fused_kernels(p);
+      if (st == PINT_OK) {
+        const cudaError_t ec = launch_loop_ctl(p->lctl, p->upd, hnd, p->stream);
+        if (ec != cudaSuccess) st = fail(PINT_ERR_CUDA, std::string("loop ctl: ") + cudaGetErrorString(ec));
+      }
+    }
+    p->cap_skip = nullptr;
+    p->wcur = w0;
+    p->xcur = x0;
+    p->launches = l0;
+    cudaGraph_t body = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(p->stream, &body);
+    if (st != PINT_OK) { cudaGraphDestroy(g); return st; }
+    if (ec != cudaSuccess) { cudaGraphDestroy(g); return fail(PINT_ERR_CUDA, std::string("loop capture: ") + cudaGetErrorString(ec)); }
+    const cudaError_t ei = cudaGraphInstantiate(&p->lexec[key], g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(ei);
+    memcpy(p->lfa[key], fa, sizeof fa);
+    memcpy(p->lfin[key], fin, sizeof fin);
+  }
+  LoopCtl* hs = p->lctl_h;
+  *hs = LoopCtl{0, max_iters, 1, 0, p->increases, guard ? 1 : 0, tol, p->last_upd, 0.0};
+  CUDA_TRY(cudaMemcpyAsync(p->lctl, hs, sizeof(LoopCtl), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaGraphLaunch(p->lexec[key], p->stream));
+  CUDA_TRY(cudaMemcpyAsync(hs, p->lctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  const int it = hs->it;
+  if (it & 1) { p->wcur ^= 1; p->xcur ^= 1; }
+  p->m += it;
+  p->launches += 3 * (int64_t)it;          // fused + finish + ctl per iteration
+  p->stateA = 0;
+  p->upd_queued = false;
+  if (guard) { p->last_upd = hs->last; p->increases = hs->inc; }
+  *iters = it;
+  *u_out = it > 0 ? hs->u : INFINITY;
+  *status = hs->status;
   return PINT_OK;
 }
 
@@ -1282,6 +1331,18 @@ extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters,
   int it = 0;
   double u = INFINITY;
   pint_status result = PINT_ERR_NOT_CONVERGED;
+  if (p->fused && p->graphs && p->nranks == 1 && !p->timing && max_iters > 0) {
+    // the same stopping rule on the device: one graph launch, one synchronisation (fused_loop)
+    int status = 1;
+    TRY(fused_loop(p, tol, max_iters, true, &it, &u, &status));
+    result = status == 0 ? PINT_OK : (status == 1 ? PINT_ERR_NOT_CONVERGED : PINT_ERR_DIVERGED);
+    if (status == 2) g_last_error = "update is not finite";
+    if (status == 3) g_last_error = "update grew 3 consecutive times";
+    if (status == 1) g_last_error = "max_iters reached before update < tol";
+    if (iters) *iters = it;
+    if (update_inf) *update_inf = u;
+    return result;
+  }
   while (it < max_iters) {
     TRY(step_collective(p, &u));
     ++it;
@@ -1298,6 +1359,30 @@ extern "C" pint_status pint_wr_solve(pint_plan p, double tol, int32_t max_iters,
   if (iters) *iters = it;
   if (update_inf) *update_inf = u;
   return result;
+}
+
+extern "C" pint_status pint_wr_run(pint_plan p, int32_t iters, double* update_inf) {
+  if (!p) return fail(PINT_ERR_ARG, "plan is NULL");
+  if (p->nl) return fail(PINT_ERR_STATE, "semilinear plan: use pint_newton_solve");
+  if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
+  if (iters < 1) return fail(PINT_ERR_ARG, "need iters >= 1");
+  CUDA_TRY(cudaSetDevice(p->device));
+  // enqueue all iterations (fused path: one graph replay each), read (and all-reduce) the last update only
+  for (int32_t i = 0; i < iters - 1; ++i) {
+    const pint_status st = iterate_async(p);
+    if (st != PINT_OK) {
+      if (p->nranks > 1) { double x = INFINITY; p->allreduce(&x, p->actx); }   // keep the collective matched
+      return st;
+    }
+    if (p->timing) {   // timing mode: the replayed graph's event nodes are read after each iteration
+      double x;
+      TRY(read_update_local(p, &x));
+    }
+  }
+  double u;
+  TRY(step_collective(p, &u));
+  if (update_inf) *update_inf = u;
+  return PINT_OK;
 }
 
 // ------------------------------------------------------------------------------------------

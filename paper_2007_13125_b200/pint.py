@@ -33,7 +33,7 @@ EXPORTED = [
     "pint_modal_to_physical", "pint_partition", "pint_get_partition", "pint_set_timing", "pint_get_timing",
     "pint_get_info", "pint_plan_destroy", "pint_status_string", "pint_last_error",
     "pint_kappa_log_rule", "pint_get_path", "pint_set_nonlinearity", "pint_newton_solve", "pint_set_problem",
-    "pint_residual",
+    "pint_residual", "pint_wr_run",
 ]
 
 
@@ -87,6 +87,7 @@ def lib(path: str = LIB_PATH):
         "pint_set_problem": [P, VP, VP, VP, VP, I32],
         "pint_newton_solve": [P, I32, D, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(I32)],
         "pint_residual": [P, ctypes.POINTER(D), ctypes.POINTER(D)],
+        "pint_wr_run": [P, I32, ctypes.POINTER(D)],
     }
     for name, args in sig.items():
         if not hasattr(L, name) and "PINT_LIB" in os.environ:
@@ -220,6 +221,12 @@ class Plan:
     def iterate(self) -> float:
         u = ctypes.c_double()
         _check(lib().pint_wr_iterate(self._h, ctypes.byref(u)))
+        return u.value
+
+    def run(self, iters: int) -> float:
+        """Exactly `iters` iterations, one synchronisation (pint_wr_run); returns the last update."""
+        u = ctypes.c_double()
+        _check(lib().pint_wr_run(self._h, iters, ctypes.byref(u)))
         return u.value
 
     def solve(self, tol: float = 1e-12, max_iters: int = 50, raise_on_fail: bool = True):

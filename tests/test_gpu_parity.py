@@ -504,17 +504,25 @@ def test_dense_forcing_newton(pint):
     assert rel(res[1][1], res[0][1]) < 1e-12
 
 
-def test_wr_solve_divergence_guard(pint):
+def test_wr_solve_divergence_guard(pint, monkeypatch):
     """S:406 / SURVEY §8(b): the WR iteration diverges when kappa R / (1 - kappa R) > 1 (BDF1
     contraction factor) — a scalar problem with a tiny T (R ~ 1) and kappa = 0.9 —
-    and pint_wr_solve reports PINT_ERR_DIVERGED after 3 consecutive increases."""
+    and pint_wr_solve reports PINT_ERR_DIVERGED after 3 consecutive increases: on the device loop
+    (default) after the same number of iterations as on the host loop (PINT_NO_GRAPH=1)."""
     prob = inputs.random_complex_problem(1, 1, 64, 1, 0.9, 1.0, R=0, seed=3, T=1e-3)
     from oracle import theory
     assert theory.bdf1_closed_form(prob.N, prob.kappa, prob.tau, 8.0) > 1.0     # lambda = 2/h^2, h = 1/2
-    with pint.Plan.from_problem(prob) as p:
-        it, u, st = p.solve(1e-12, 100, raise_on_fail=False)
-        assert st == pint.PINT_ERR_DIVERGED, (it, u, st)
-        assert it < 100
+    res = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("PINT_NO_GRAPH", "1")
+        with pint.Plan.from_problem(prob) as p:
+            it, u, st = p.solve(1e-12, 100, raise_on_fail=False)
+            assert st == pint.PINT_ERR_DIVERGED, (it, u, st)
+            assert it < 100
+            res.append((it, u))
+    monkeypatch.delenv("PINT_NO_GRAPH")
+    assert res[0] == res[1], res
 
 
 @pytest.mark.parametrize("mx,my,N,k", [(63, 1, 64, 2), (63, 30, 256, 3), (1023, 1, 1024, 4)])
@@ -725,3 +733,60 @@ def test_fused_modal_initial_guess(pint, make, kw):
         us = [p.iterate() for _ in range(2)]
         assert max(us) < 1e-10 * np.abs(Us).max(), us
         assert rel(p.get_solution(), Us) < 1e-10
+
+
+@pytest.mark.parametrize("make,tol", [
+    (lambda: inputs.config_c1(), 1e-12),
+    (lambda: inputs.config_c2(k=3, kappa=1e-2), 1e-12),
+    (lambda: inputs.config_c2(k=6, kappa=1e-3), 1e-10),
+    (lambda: inputs.random_complex_problem(63, 30, 256, 3, 0.05, 1.0, R=1, seed=41), 1e-11),
+])
+def test_device_loop_matches_host_loop(pint, monkeypatch, make, tol):
+    """pint_wr_solve on the fused path runs its loop on the device (while-conditional graph node, the
+    stopping rule in a kernel): same iteration count, update norm and iterate as the host loop
+    (PINT_NO_GRAPH=1), in one or several calls, and pint_wr_run(K) equals K pint_wr_iterate calls."""
+    prob = make()
+    monkeypatch.setenv("PINT_NO_GRAPH", "1")
+    host = pint.Plan.from_problem(prob)
+    monkeypatch.delenv("PINT_NO_GRAPH")
+    dev = pint.Plan.from_problem(prob)
+    try:
+        assert dev.path()["fused"]
+        l0 = dev.info()["kernel_launches"]
+        ih, uh, sh = host.solve(tol, 30, raise_on_fail=False)
+        idv, ud, sd = dev.solve(tol, 30, raise_on_fail=False)
+        print(f"{prob.name}: host loop {ih} it (update {uh:.3e}, status {sh}); device loop {idv} it ({ud:.3e}, {sd})")
+        assert (ih, sh) == (idv, sd) and sh == pint.PINT_OK
+        assert ud == uh
+        assert dev.info()["m"] == idv and dev.info()["kernel_launches"] - l0 == 3 * idv
+        assert np.array_equal(host.get_solution(), dev.get_solution())
+        # a second solve continues from the converged state (parity and guard state carried over)
+        assert host.solve(tol, 5, raise_on_fail=False)[:2] == dev.solve(tol, 5, raise_on_fail=False)[:2]
+        # max_iters bound on the device: NOT_CONVERGED after exactly 2 iterations
+        it2, _, st2 = dev.solve(0.0, 2, raise_on_fail=False)
+        assert (it2, st2) == (2, pint.PINT_ERR_NOT_CONVERGED)
+    finally:
+        host.close()
+        dev.close()
+    # pint_wr_run: K iterations with one synchronisation == K pint_wr_iterate calls
+    with pint.Plan.from_problem(prob) as a, pint.Plan.from_problem(prob) as b:
+        ua = [a.iterate() for _ in range(5)][-1]
+        ub = b.run(5)
+        assert ua == ub and b.info()["m"] == 5
+        assert np.array_equal(a.get_solution(), b.get_solution())
+        b.run(1)
+        a.iterate()
+        assert np.array_equal(a.get_solution(), b.get_solution())
+
+
+def test_wr_run_streaming_and_args(pint):
+    """pint_wr_run on the streaming (CQ) path: K iterations enqueued, one synchronisation; argument checks."""
+    prob = inputs.random_complex_problem(31, 20, 256, 2, 0.1, 0.6, R=1, seed=21)
+    with pint.Plan.from_problem(prob) as a, pint.Plan.from_problem(prob) as b:
+        ua = [a.iterate() for _ in range(3)][-1]
+        ub = b.run(3)
+        assert ua == ub
+        assert np.array_equal(a.get_solution(), b.get_solution())
+        with pytest.raises(pint.PintError) as e:
+            b.run(0)
+        assert e.value.status == pint.PINT_ERR_ARG
