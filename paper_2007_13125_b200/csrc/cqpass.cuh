@@ -23,9 +23,13 @@
 //    the current tile has been read, and lands while the current tile finishes its last DFT, the
 //    monitor-free epilogue and the stores.  The next tile (and this tile's U_{m-1}) are prefetched
 //    into L2 at the start of each tile.
+//  * U_{m-1} of the tile (the full-array monitor's copy) is bulk-copied into the same buffer right
+//    after the first transform's exchange and lands during its second DFT pass.
 //  * D W + H_static (the iteration-invariant static spectrum) is formed when W arrives and parked in
-//    tensor memory (TMEM, otherwise idle: 128 columns per CTA) until the end of the tile, instead of
-//    re-reading W from HBM/L2.
+//    tensor memory (TMEM, otherwise idle) until the end of the tile, instead of re-reading W from
+//    HBM/L2; the thread's (c_x/N) d'_p values sit in TMEM for the whole kernel (256 columns per CTA).
+//  * The four transforms share ONE code body (a forward transform is conj . inverse . conj): a fully
+//    unrolled four-transform tile was 13k instructions and stalled on instruction fetch.
 // HBM per unknown: W in 16 B, H out 16 B, U_{m-1} in + U_m out 32 B (full monitor) = 64 B.
 #pragma once
 #include "tpass.cuh"
@@ -100,12 +104,12 @@ template <int N1> struct CQCfg {
   static constexpr int THREADS = N1 * WB;                   // thread (i, c) = (tid / WB, tid % WB)
   static constexpr int ROW = N1 * WB + (WB == 4 ? 4 : 0);   // exchange row stride (complex), padded
   static constexpr int BUF = (N1 * ROW > TILE ? N1 * ROW : TILE);
-  static constexpr int SMEM = BUF * 16;
-#ifndef PINT_CQF_MINB
-#define PINT_CQF_MINB 2
-#endif
-  static constexpr int MINB = N1 == 32 ? PINT_CQF_MINB : 2;
-  static constexpr int TCOLS = 128;                         // TMEM columns per CTA (stash of D W + H_static)
+  static constexpr int TWROW = N1 + 1;                      // twiddle rows in shared memory, padded
+  static constexpr int SMEM = (BUF + N1 * TWROW + N) * 16;   // exchange / tile buffer + twiddles + Theta
+  // two CTAs per SM: 255 registers (no spills of the 32 values per thread), 2 x 256 TMEM columns
+  static constexpr int MINB = 2;
+  static constexpr int TCOLS = 256;                         // TMEM columns per CTA: the stash of D W + H_static
+                                                            // (128) and this thread's (c_x/N) D' values (128)
 };
 
 struct CQArgs {
@@ -114,16 +118,16 @@ struct CQArgs {
   double2* ufull;             // U_{m-1} -> U_m, every level (tile layout)
   double2* wrap_new;          // [ntiles][k][WB] window levels of U_m
   unsigned long long* upd;    // max |U_m - U_{m-1}| as ordered bits
-  const double2 *tw0, *tw1, *tw2;   // [N] pass-A tables at [i N1 + k2], all in the inverse direction:
-                              //   0: w^{+i k2}                (u = V W and s = V Z)
-                              //   1: theta^{-i} w^{+i k2}     (z = V^{-1} Theta u = conj V conj(.)  )
-                              //   2: theta^{+i} w^{+i k2}     (H' = V^{-1} Theta^{-1} s, likewise)
+  const double2* tw;          // [N] pass-A twiddles w^{+i k2} at [i N1 + k2] (every transform runs as an
+                              //     inverse 4-step transform; a forward one as conj . inverse . conj)
+  const double2* th;          // [N] theta^n = e^{i pi n / N} (the skew-circulant rotation Theta)
   const double2* dpr;         // [N] (c_x / N) d'_p: d'_p the eigenvalues of C(-kappa), c_x = -h^2/(2 tau^a N)
                               //     (the 1/N of V^{-1} and c_x of the Theta^{-1} factor, moved onto D')
   const double2* dh;          // [N] (h^2/(2 tau^a)) d_p
   const double2* chat;        // [S][N] DFT of kappa^{n/N} h^2/N c_s(n)  (static right-hand side)
   const double2* src;         // [S][ntiles][WB] spatial sources (DST-x basis)
-  const double* igs;          // [N] kappa^{-n/N}
+  const double* igs;          // [N] kappa^{-n/N}: Gamma^{-1} = igs[i] * gt[t] (separable, n = i + N1 t)
+  double gt[32];              // kappa^{-N1 t/N}, t < N1 (parameter space; compile-time index)
   int S, k;
   long ntiles;
 };
@@ -141,13 +145,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
                  : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   } while (!done);
-}
-
-// read-only table load that is re-issued at every use (asm volatile: no CSE, no hoisting)
-__device__ __forceinline__ double2 ldg_nc_v(const double2* p) {
-  double2 r;
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
 }
 
 // 4 complex doubles <-> 16 TMEM columns of this thread's lane
@@ -181,39 +178,19 @@ template <int N1> __device__ __forceinline__ void conj_all(double2 (&v)[N1]) {
   for (int t = 0; t < N1; ++t) v[t].y = __longlong_as_double(__double_as_longlong(v[t].y) ^ (long long)0x8000000000000000ULL);
 }
 
-// rotations e^{-+ i pi t / N1} of the pre-pass of transforms 1 and 3 (uniform across the warp:
-// constant-cache broadcast)
-static __constant__ double2 cq_rot[2][32] = {
-    {{1.0, 0.0}, {0.995184726672196886245, -0.0980171403295606019942}, {0.980785280403230449126, -0.195090322016128267848}, {0.956940335732208864936, -0.290284677254462367636},
-     {0.923879532511286756128, -0.382683432365089771728}, {0.881921264348355029713, -0.471396736825997648556}, {0.831469612302545237079, -0.555570233019602224743}, {0.773010453362736960811, -0.634393284163645498215},
-     {0.707106781186547524401, -0.707106781186547524401}, {0.634393284163645498215, -0.773010453362736960811}, {0.555570233019602224743, -0.831469612302545237079}, {0.471396736825997648556, -0.881921264348355029713},
-     {0.382683432365089771728, -0.923879532511286756128}, {0.290284677254462367636, -0.956940335732208864936}, {0.195090322016128267848, -0.980785280403230449126}, {0.0980171403295606019942, -0.995184726672196886245},
-     {0.0, -1.0}, {-0.0980171403295606019942, -0.995184726672196886245}, {-0.195090322016128267848, -0.980785280403230449126}, {-0.290284677254462367636, -0.956940335732208864936},
-     {-0.382683432365089771728, -0.923879532511286756128}, {-0.471396736825997648556, -0.881921264348355029713}, {-0.555570233019602224743, -0.831469612302545237079}, {-0.634393284163645498215, -0.773010453362736960811},
-     {-0.707106781186547524401, -0.707106781186547524401}, {-0.773010453362736960811, -0.634393284163645498215}, {-0.831469612302545237079, -0.555570233019602224743}, {-0.881921264348355029713, -0.471396736825997648556},
-     {-0.923879532511286756128, -0.382683432365089771728}, {-0.956940335732208864936, -0.290284677254462367636}, {-0.980785280403230449126, -0.195090322016128267848}, {-0.995184726672196886245, -0.0980171403295606019942}},
-    {{1.0, 0.0}, {0.995184726672196886245, 0.0980171403295606019942}, {0.980785280403230449126, 0.195090322016128267848}, {0.956940335732208864936, 0.290284677254462367636},
-     {0.923879532511286756128, 0.382683432365089771728}, {0.881921264348355029713, 0.471396736825997648556}, {0.831469612302545237079, 0.555570233019602224743}, {0.773010453362736960811, 0.634393284163645498215},
-     {0.707106781186547524401, 0.707106781186547524401}, {0.634393284163645498215, 0.773010453362736960811}, {0.555570233019602224743, 0.831469612302545237079}, {0.471396736825997648556, 0.881921264348355029713},
-     {0.382683432365089771728, 0.923879532511286756128}, {0.290284677254462367636, 0.956940335732208864936}, {0.195090322016128267848, 0.980785280403230449126}, {0.0980171403295606019942, 0.995184726672196886245},
-     {0.0, 1.0}, {-0.0980171403295606019942, 0.995184726672196886245}, {-0.195090322016128267848, 0.980785280403230449126}, {-0.290284677254462367636, 0.956940335732208864936},
-     {-0.382683432365089771728, 0.923879532511286756128}, {-0.471396736825997648556, 0.881921264348355029713}, {-0.555570233019602224743, 0.831469612302545237079}, {-0.634393284163645498215, 0.773010453362736960811},
-     {-0.707106781186547524401, 0.707106781186547524401}, {-0.773010453362736960811, 0.634393284163645498215}, {-0.831469612302545237079, 0.555570233019602224743}, {-0.881921264348355029713, 0.471396736825997648556},
-     {-0.923879532511286756128, 0.382683432365089771728}, {-0.956940335732208864936, 0.290284677254462367636}, {-0.980785280403230449126, 0.195090322016128267848}, {-0.995184726672196886245, 0.0980171403295606019942}},
-};
-
 template <int N1>
 __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_fused_kernel(const CQArgs a) {
   using G = CQCfg<N1>;
   constexpr int N = G::N, WB = G::WB, NW = G::THREADS / 32;
   extern __shared__ __align__(128) double2 buf[];
-  __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bar, ubar;   // W tile landed / U_{m-1} tile landed
   __shared__ uint32_t tbase;
   __shared__ double red[NW];
   const int tid = threadIdx.x, i = tid / WB, c = tid % WB, warp = tid / 32;
-  const uint32_t sbuf = smem_u32(buf), sbar = smem_u32(&bar);
+  const uint32_t sbuf = smem_u32(buf), sbar = smem_u32(&bar), subar = smem_u32(&ubar);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sbar) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(subar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -224,19 +201,36 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // the pass-A twiddles and Theta, staged once per CTA (persistent kernel): conflict-free shared loads
+  double2* stw = buf + G::BUF;                 // [N1][N1 + 1]
+  double2* sth = stw + N1 * G::TWROW;          // [N]
+  for (int e = tid; e < N; e += G::THREADS) {
+    stw[(e / N1) * G::TWROW + e % N1] = __ldg(&a.tw[e]);
+    sth[e] = __ldg(&a.th[e]);
+  }
+  __syncthreads();
   // this thread's stash columns: lane 32 (warp % 4) + lane, N1 * 4 columns (N1 complex doubles)
   const uint32_t tst = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * N1 * 4);
+  const uint32_t tdp = tst + 128;      // this thread's (c_x/N) d'_p, p = i + N1 t: fixed for the whole kernel
+#pragma unroll
+  for (int q = 0; q < N1 / 4; ++q) {
+    double2 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = __ldg(&a.dpr[i + N1 * (4 * q + j)]);
+    tmem_st4c(tdp + 16 * q, x);
+  }
+  const double gi0 = __ldg(&a.igs[i]);
   const long ntiles = a.ntiles;
   long tile = blockIdx.x;
   uint32_t phase = 0;
   if (tid == 0 && tile < ntiles) tile_bulk_load(sbuf, a.in + tile * (long)TILE, TILE * 16, sbar);
-  double upd = 0.0;
+  double upd2 = 0.0;                   // max |U_m - U_{m-1}|^2 (one square root at the end)
   bool nonfinite = false;
   for (; tile < ntiles; tile += gridDim.x) {
     const long base = tile * (long)TILE, nt = tile + gridDim.x;
     if (tid < 4) {
       if (nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
-    } else if (tid < 8) {
+    } else if (tid < 8) {                    // this tile's U_{m-1}: its bulk copy (after u = V W) hits L2
       prefetch_l2_t(a.ufull + base + (tid - 4) * (TILE / 4), TILE / 4 * 16);
     }
     mbar_wait(sbar, phase);
@@ -275,17 +269,20 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
 #pragma unroll 1
     for (int x = 0; x < 4; ++x) {
       const bool fwd = (x & 1) != 0;
-      if (fwd) {
+      if (fwd) {   // conj(Theta^{+-1} y) = Theta^{-+1} conj(y): x = 1 multiplies by theta^{-n}, x = 3 by theta^{+n}
         conj_all<N1>(v);
+        const double sg = x == 1 ? -1.0 : 1.0;
 #pragma unroll
-        for (int t = 1; t < N1; ++t) v[t] = cmul(v[t], cq_rot[x >> 1][t * (32 / N1)]);
+        for (int t = 0; t < N1; ++t) {
+          const double2 r = sth[i + N1 * t];
+          v[t] = cmul(v[t], make_double2(r.x, sg * r.y));
+        }
       }
       dft_n1<N1, +1>(v);
       {
-        const double2* tr = (fwd ? (x == 1 ? a.tw1 : a.tw2) : a.tw0) + i * N1;   // (no runtime index into
-                                                                                 //  the parameter struct)
+        const double2* tr = stw + i * G::TWROW;
 #pragma unroll
-        for (int k2 = 0; k2 < N1; ++k2) v[k2] = cmul(v[k2], ldg_nc_v(&tr[k2]));
+        for (int k2 = 1; k2 < N1; ++k2) v[k2] = cmul(v[k2], tr[k2]);
       }
       __syncthreads();                       // the buffer is free (previous exchange / tile input read)
 #pragma unroll
@@ -293,7 +290,13 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < N1; ++t) v[t] = buf[i * G::ROW + t * G::WB + c];
-      if (x == 3) {
+      if (x == 0) {                          // U_{m-1} of this tile lands during the pass-B DFT
+        __syncthreads();
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          tile_bulk_load(sbuf, a.ufull + base, TILE * 16, subar);
+        }
+      } else if (x == 3) {
         __syncthreads();
         if (tid == 0 && nt < ntiles) {       // the next tile lands while this one finishes
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -303,19 +306,27 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
       dft_n1<N1, +1>(v);
       if (fwd) conj_all<N1>(v);
       if (x == 0) {
+        double gi;   // kappa^{-i/N}, through an opaque move per tile: its 32 products with gt[t] would
+        asm volatile("mov.b64 %0, %1;" : "=d"(gi) : "d"(gi0));   // otherwise be hoisted and kept live
+        mbar_wait(subar, phase ^ 1);         // (phase was flipped after the W wait of this tile)
 #pragma unroll
         for (int t = 0; t < N1; ++t) {
           const int n = i + N1 * t;
-          const double2 U = cscale(v[t], __ldg(&a.igs[n]));
-          const double d = sqrt(cabs2(csub(U, a.ufull[base + (long)n * WB + c])));
-          if (!(d <= 1.7976931348623157e308)) nonfinite = true;
-          upd = fmax(upd, d);
+          const double2 U = cscale(v[t], gi * a.gt[t]);
+          const double d2 = cabs2(csub(U, buf[n * WB + c]));
+          if (!(d2 <= 1.7976931348623157e308)) nonfinite = true;
+          upd2 = fmax(upd2, d2);
           a.ufull[base + (long)n * WB + c] = U;
           if (t == N1 - 1 && i >= N1 - a.k) a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
         }
       } else if (x == 1) {
 #pragma unroll
-        for (int t = 0; t < N1; ++t) v[t] = cmul(v[t], __ldg(&a.dpr[i + N1 * t]));
+        for (int q = 0; q < N1 / 4; ++q) {   // (c_x/N) D' from tensor memory
+          double2 dq[4];
+          tmem_ld4c(tdp + 16 * q, dq);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[4 * q + j] = cmul(v[4 * q + j], dq[j]);
+        }
       }
     }
     // ---- H = H' + D W + H_static ----
@@ -332,6 +343,7 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
     }
   }
   // ---- update monitor: block max, one atomic per CTA; TMEM release ----
+  double upd = sqrt(upd2);
   if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
   for (int o = 16; o > 0; o >>= 1) upd = fmax(upd, __shfl_xor_sync(0xffffffffu, upd, o));
   if ((tid & 31) == 0) red[warp] = upd;

@@ -64,11 +64,14 @@ cudaError_t PINT_CAT(launch_tpass_cq_fused_, PINT_N)(const CQArgs& a, cudaStream
   constexpr int N1 = PINT_N == 1024 ? 32 : 16;
   using G = CQCfg<N1>;
   auto kern = tpass_cq_fused_kernel<N1>;
-  // persistent grid of MINB CTAs per SM (the kernel's launch bound; three 67 KB exchange buffers and
-  // 3 x 128 TMEM columns per SM), with the full shared-memory carve-out
+  // persistent grid of MINB CTAs per SM (the kernel's launch bound; MINB 67 KB exchange buffers and
+  // MINB x 256 TMEM columns per SM) with a shared-memory carve-out of just what they need: the rest of
+  // the 256 KB stays L1 for the pass-A twiddle and eigenvalue tables
   static const long resident = [&]() -> long {
-    if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared) != cudaSuccess) return 0;
+    const int need = G::MINB * (G::SMEM + 1024 + 256);
+    const int pct = (int)((100LL * need + 233471) / 233472);
+    if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct) != cudaSuccess)
+      return 0;
     if (persistent_grid((const void*)kern, G::SMEM, G::THREADS) <= 0) return 0;   // sets the smem attribute
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

@@ -140,8 +140,13 @@ __global__ void nl_update_kernel(double2* U, const double2* W, long N, int L, in
 // max |A - B| over count elements -> upd (inner WR monitor on the full space-time array)
 __global__ void nl_diffmax_kernel(const double2* A, const double2* B, long count, unsigned long long* upd) {
   double m = 0.0;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x)
-    m = fmax(m, sqrt(cabs2(csub(A[e], B[e]))));
+  bool nonfinite = false;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x) {
+    const double d = sqrt(cabs2(csub(A[e], B[e])));
+    if (!(d <= 1.7976931348623157e308)) nonfinite = true;
+    m = fmax(m, d);
+  }
+  if (nonfinite) m = __longlong_as_double(0x7ff0000000000000LL);   // fmax drops NaN: report +inf
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(upd, (unsigned long long)__double_as_longlong(m));
 }

@@ -130,8 +130,9 @@ struct pint_plan_s {
   double2 *dh = nullptr, *dpr = nullptr, *thp = nullptr, *thm = nullptr;
   double2* sig_p = nullptr;
   double* sig_q = nullptr;
-  double2 *cq_twi = nullptr, *cq_twz = nullptr, *cq_twx = nullptr;   // one-kernel CQ T-pass (cqpass.cuh):
-  double2* cq_dpr = nullptr;                                         // pass-A tables, (c_x / N) d'_p
+  double2 *cq_twi = nullptr, *cq_th = nullptr;   // one-kernel CQ T-pass (cqpass.cuh): pass-A twiddles, theta^n,
+  double2* cq_dpr = nullptr;                      // (c_x / N) d'_p
+  double cq_gt[32] = {};                                             // kappa^{-N1 t/N}
   double2* phys = nullptr;   // [2][M] physical staging (v, A v)
   double2* wstage = nullptr; // [k][M] staging for window-level reads (lazy)
   unsigned long long* upd = nullptr;
@@ -148,6 +149,9 @@ struct pint_plan_s {
   double2* twEy = nullptr;    // [NEy] DST-y twiddles
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
   double2* wtmp = nullptr;    // [ntiles][k][WB] modal window -> (q, y) staging
+  bool pmon = false;          // fused modal plan, one rank: update monitor on the PHYSICAL window levels
+  double2* pwin[2] = {nullptr, nullptr};   // [k][M] physical window of U_m (ping-pong with wcur)
+  unsigned long long* upd_sink = nullptr;  // the finish kernel's (modal-basis) monitor goes here then
   double2* fd = nullptr;      // dense forcing f(t_1..t_N) in the tile layout (pint_set_problem)
   bool full = false;          // full-array update monitor (CQ plans, PINT_FLAG_FULL_UPDATE_NORM)
   double2* ufull = nullptr;   // [ntiles][N][WB]: U_m of every level (tile layout) when `full`
@@ -201,6 +205,7 @@ struct pint_plan_s {
   cudaGraphExec_t lexec[4] = {};   // per (wcur, xcur) at loop entry
   FusedArgs lfa[4][2];
   FinishArgs lfin[4][2];
+  int64_t llaunch[4] = {};         // kernels per iteration of the loop body (incl. the ctl kernel)
   int gpending = -1;          // slot whose event nodes ran last and are not yet accumulated
   int64_t glaunch = 0;        // kernels per graph replay
 };
@@ -442,6 +447,16 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     if ((st = dalloc(p, &p->mu, (size_t)L)) != PINT_OK) return bail(st);
   }
   if (p->fused_ok && p->modal) {
+    // physical-space window monitor (one rank: the DST-x back needs every x-mode): the orthonormal
+    // DSTs scale the modal coefficients of a smooth field by up to sqrt(M) against the grid values, so
+    // a modal-basis max-norm would sit ~sqrt(M) above the grid update (its round-off floor 1.7e-12 at C4)
+    p->pmon = nranks == 1;
+    if (p->pmon) {
+      for (int i = 0; i < 2; ++i)
+        if ((st = dalloc(p, &p->pwin[i], (size_t)k * M)) != PINT_OK) return bail(st);
+      if ((st = dalloc(p, &p->wtmp, (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
+      if ((st = dalloc(p, &p->upd_sink, 1)) != PINT_OK) return bail(st);
+    }
     p->half = (p->flags & PINT_FLAG_REAL_DATA) != 0;
     p->nch = 1;
     p->gpc = (int)(N / 8);
@@ -546,21 +561,21 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     // one-kernel CQ T-pass (cqpass.cuh): 4-step transforms N = N1 x N1; pass-A tables [i][k2] with the
     // Theta / N and c_x Theta^{-1} factors of the skew-circulant wrap folded in (per-thread part theta^i)
     const int64_t N1 = N == 1024 ? 32 : 16;
-    // all four transforms run as inverse 4-step transforms (forward = conj . inverse . conj), so the
-    // tables of the forward ones are conjugated: theta^{-+i} w^{+i k2}
-    std::vector<double2> twi(N), twz(N), twx(N), dps(N);
+    // all four transforms run as inverse 4-step transforms (forward = conj . inverse . conj): one
+    // twiddle table w^{+i k2} [i][k2], and theta^n for the skew-circulant rotations
+    std::vector<double2> twi(N), thn(N), dps(N);
     for (int64_t i = 0; i < N1; ++i)
       for (int64_t k2 = 0; k2 < N1; ++k2) {
-        const ld a = 2.0L * PI_L * (ld)((i * k2) % N) / Nl, th = PI_L * (ld)i / Nl;
+        const ld a = 2.0L * PI_L * (ld)((i * k2) % N) / Nl;
         twi[i * N1 + k2] = d2(cld(cosl(a), sinl(a)));                 // w^{+i k2}
-        twz[i * N1 + k2] = d2(cld(cosl(a - th), sinl(a - th)));       // conj(theta^i w^{-i k2})
-        twx[i * N1 + k2] = d2(cld(cosl(a + th), sinl(a + th)));       // conj(theta^{-i} w^{-i k2})
       }
+    for (int64_t n = 0; n < N; ++n) thn[n] = d2(cld(cosl(PI_L * (ld)n / Nl), sinl(PI_L * (ld)n / Nl)));
+    for (int64_t t = 0; t < N1; ++t) p->cq_gt[t] = (double)powl(kap, -(ld)(N1 * t) / Nl);
     const ld cx = -(hl * hl) * ta / (2.0L * Nl);                     // the chain is linear: 1/N and c_x on D'
     for (int64_t pp = 0; pp < N; ++pp) dps[pp] = d2(dprl[pp] * (cx / Nl));
-    double2** tabs[4] = {&p->cq_twi, &p->cq_twz, &p->cq_twx, &p->cq_dpr};
-    const std::vector<double2>* vals[4] = {&twi, &twz, &twx, &dps};
-    for (int t = 0; t < 4; ++t) {
+    double2** tabs[3] = {&p->cq_twi, &p->cq_th, &p->cq_dpr};
+    const std::vector<double2>* vals[3] = {&twi, &thn, &dps};
+    for (int t = 0; t < 3; ++t) {
       if ((st = dalloc(p, tabs[t], N)) != PINT_OK) return bail(st);
       if ((st = h2d(p, *tabs[t], *vals[t])) != PINT_OK) return bail(st);
     }
@@ -647,8 +662,9 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
     // one kernel: W -> U_m (full monitor) -> four on-chip transforms -> H (cqpass.cuh)
     CQArgs c{};
     c.in = in; c.out = out; c.ufull = p->ufull; c.wrap_new = wnew; c.upd = p->upd;
-    c.tw0 = p->cq_twi; c.tw1 = p->cq_twz; c.tw2 = p->cq_twx; c.dpr = p->cq_dpr; c.dh = p->dh; c.chat = p->cqhat; c.src = p->src;
+    c.tw = p->cq_twi; c.th = p->cq_th; c.dpr = p->cq_dpr; c.dh = p->dh; c.chat = p->cqhat; c.src = p->src;
     c.igs = p->igs;
+    for (int t = 0; t < 32; ++t) c.gt[t] = t < (p->N == 1024 ? 32 : 16) ? p->cq_gt[t] : 0.0;
     c.S = p->S; c.k = p->k; c.ntiles = p->ntiles;
     CUDA_TRY(launch_tpass_cq_fused((int)p->N, c, p->stream));
   } else if (split) {
@@ -744,7 +760,7 @@ static FinishArgs finargs(pint_plan p, const double2* wold, double2* wnew, doubl
   FinishArgs a{};
   a.P = p->Pp; a.wrap_old = wold; a.wrap_new = wnew; a.X = X;
   a.src = p->src; a.coef = p->coef; a.spar = p->srclist; a.nsparse = p->nsparse;
-  a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->upd;
+  a.igs = p->igs; a.gsf = p->gsf; a.wk = p->wk; a.upd = p->pmon ? p->upd_sink : p->upd;
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.pstride = p->nch;
   a.skip = p->cap_skip;
@@ -818,12 +834,14 @@ static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
 // problem setup
 // ------------------------------------------------------------------------------------------
 static pint_status nl_reset(pint_plan p);
+static pint_status modal_window_phys(pint_plan p, const double2* wmodal, double2* out);
 
 static pint_status bootstrap(pint_plan p) {
   // U_0^n = v (default) or 0 (PINT_FLAG_U0_ZERO): A = H_1, wrap = last-k of U_0
   const bool zero = (p->flags & PINT_FLAG_U0_ZERO) != 0;
   if (p->fused) {   // window of U_0 and X_1 only
     TRY(finish_pass(p, zero ? FIN_ZERO : FIN_FROM_V, nullptr, p->wrap[p->wcur], p->X[p->xcur]));
+    if (p->pmon) TRY(modal_window_phys(p, p->wrap[p->wcur], p->pwin[p->wcur]));
   } else {
     TRY(tpass(p, zero ? IN_TIME_ZERO : IN_TIME_V, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur], false));
   }
@@ -1093,6 +1111,7 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
     TRY(tpass(p, IN_TIME_BUF, OUT_H, p->A, p->A, nullptr, p->wrap[p->wcur], false));
   }
   if (p->fused) TRY(finish_pass(p, FIN_FROM_WRAP, p->wrap[p->wcur], nullptr, p->X[p->xcur]));
+  if (p->pmon) TRY(modal_window_phys(p, p->wrap[p->wcur], p->pwin[p->wcur]));
   p->stateA = 0;
   p->m = 0;
   p->last_upd = -1.0;
@@ -1105,9 +1124,31 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // iteration
 // ------------------------------------------------------------------------------------------
 // one fused iteration: update monitor reset, Steps 1-3 (fused kernel), window / X / monitor (finish)
+// fused modal plans: the window levels of U (modal) -> physical [k][M] (DST-y, then DST-x in 2D)
+static pint_status modal_window_phys(pint_plan p, const double2* wmodal, double2* out) {
+  TRY(dst_y(p, wmodal, p->wtmp, p->k, p->Qb));
+  if (p->dim == 2) {
+    DstArgs a = dargs(p);
+    a.in = p->wtmp; a.out = out; a.rows = (long)p->k * p->my; a.N = p->k; a.n0 = 0;
+    CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
+  } else {
+    RemapArgs r{};
+    r.in = p->wtmp; r.out = out; r.count = (long)p->k * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
+    r.N = p->k; r.n0 = 0; r.M = p->M; r.Qb = 1;
+    CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
+  }
+  ++p->launches;
+  return PINT_OK;
+}
+
 static pint_status fused_kernels(pint_plan p) {
   TRY(fused_pass(p, p->X[p->xcur], false, true));   // Steps 1-3 (block 0 zeroes the update monitor)
   TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
+  if (p->pmon) {   // max |U_m - U_{m-1}| on the physical window levels
+    TRY(modal_window_phys(p, p->wrap[1 - p->wcur], p->pwin[1 - p->wcur]));
+    CUDA_TRY(launch_nl_diffmax(p->pwin[1 - p->wcur], p->pwin[p->wcur], (long)p->k * p->M, p->upd, p->stream));
+    ++p->launches;
+  }
   return PINT_OK;
 }
 
@@ -1171,6 +1212,7 @@ static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool g
     p->cap_skip = nullptr;
     p->wcur = w0;
     p->xcur = x0;
+    p->llaunch[key] = (p->launches - l0) / 2 + 1;   // + the ctl kernel (not counted by launch_loop_ctl)
     p->launches = l0;
     cudaGraph_t body = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(p->stream, &body);
@@ -1191,7 +1233,7 @@ static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool g
   const int it = hs->it;
   if (it & 1) { p->wcur ^= 1; p->xcur ^= 1; }
   p->m += it;
-  p->launches += 3 * (int64_t)it;          // fused + finish + ctl per iteration
+  p->launches += p->llaunch[key] * (int64_t)it;   // fused + finish [+ modal monitor] + ctl per iteration
   p->stateA = 0;
   p->upd_queued = false;
   if (guard) { p->last_upd = hs->last; p->increases = hs->inc; }
@@ -1367,7 +1409,14 @@ extern "C" pint_status pint_wr_run(pint_plan p, int32_t iters, double* update_in
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (iters < 1) return fail(PINT_ERR_ARG, "need iters >= 1");
   CUDA_TRY(cudaSetDevice(p->device));
-  // enqueue all iterations (fused path: one graph replay each), read (and all-reduce) the last update only
+  if (p->fused && p->graphs && p->nranks == 1 && !p->timing) {   // the device-side loop, no stopping rule
+    int it = 0, status = 1;
+    double u = INFINITY;
+    TRY(fused_loop(p, 0.0, iters, false, &it, &u, &status));
+    if (update_inf) *update_inf = u;
+    return PINT_OK;
+  }
+  // enqueue all iterations, read (and all-reduce) the last update only
   for (int32_t i = 0; i < iters - 1; ++i) {
     const pint_status st = iterate_async(p);
     if (st != PINT_OK) {

@@ -1,0 +1,11 @@
+python -c "
+import os; from paper_2007_13125_b200 import build as b
+assert os.path.getmtime(b.LIB) >= b._newest_dep(), 'stale libpint.so'" || exit 3
+python -m pytest tests -x -q -m "gpu and not slow" -k "cq or c5 or C5 or full or random_complex or residual or slabs or two_processes" > gpurun_out/t9.log 2>&1
+tail -2 gpurun_out/t9.log
+for r in 1 2; do
+python bench.py --config C5 --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/b9_$r.json 2>/dev/null
+python -c "import json;d=json.load(open('gpurun_out/b9_$r.json'));print('C5', d['ms_per_step'], d['roofline']['passes']['tpass_ms'])"
+done
+timeout 600 ncu --set full --import-source on -k regex:tpass_cq_fused -c 1 -o gpurun_out/prof_cqf_v9 python bench.py --config C5 --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_cqf_v9.log 2>&1
+tail -1 gpurun_out/ncu_cqf_v9.log

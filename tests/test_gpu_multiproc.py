@@ -87,7 +87,7 @@ def test_two_processes_match_single_plan(variant):
     assert [r[4] for r in res] == [0, prob.mx // 2] and res[-1][5] == prob.mx
     assert all(r[1] == it1 and r[3] == pint.PINT_OK for r in res)       # same stop (all-reduced update)
     assert all(r[2] == res[0][2] for r in res)
-    assert abs(res[0][2] - u1) <= 1e-6 * u1 + 1e-15
+    assert abs(res[0][2] - u1) <= 1e-6 * u1 + 1e-13    # (modal: the single plan monitors physically)
     U = res[0][6]
     err = float(np.linalg.norm(U - ref) / np.linalg.norm(ref))
     print(f"{variant}: gathered two-process solution vs single plan: rel L2 {err:.2e}")
