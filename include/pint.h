@@ -68,7 +68,17 @@ typedef enum {
  * both K and M: lambda_j = K_j / M_j; heat: fused modal kernel, CQ: streaming path with the
  * shifted solves as divisions), so it needs 2(mx+1) a power of two (UNSUPPORTED otherwise);
  * PINT_FLAG_MODAL is implied. */
-enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2, PINT_OP_FEM1D_DIRICHLET = 3 };
+/* PINT_OP_FEM2D_DIRICHLET: P1 finite elements on the uniform triangulation of the unit square
+ * (Example 3), each cell split by its '/' diagonal (DESIGN.md reading
+ * R-FEM2D), mx = my interior nodes per axis, h = 1/(mx+1); nodal coefficient vectors as in 1D.  The
+ * stiffness is h^2 times the 5-point Laplacian and the mass matrix M = h^2 (M_sym + E) couples the
+ * '/' diagonal neighbours, so M is not diagonalised by the DSTs: Step 2, (s_p M + K) W = M H, is
+ * solved by a fixed-point iteration preconditioned by the DST-diagonal s_p M_sym + K (fem2d.cuh),
+ * iterated to round-off.  Runs on the fully modal streaming path (PINT_FLAG_MODAL | PINT_FLAG_STREAM
+ * implied); needs 2(mx+1) a power of two, one rank (UNSUPPORTED otherwise); pint_residual is
+ * UNSUPPORTED (A = M^{-1} K is not diagonal in the modes). */
+enum { PINT_OP_FD1D_DIRICHLET = 1, PINT_OP_FD2D_DIRICHLET = 2, PINT_OP_FEM1D_DIRICHLET = 3,
+       PINT_OP_FEM2D_DIRICHLET = 4 };
 enum { PINT_HOST = 0, PINT_DEVICE = 1 };
 enum {
   PINT_FLAG_U0_ZERO = 1,       /* WR initial guess U_0 = 0 instead of U_0^n = v */
@@ -102,7 +112,8 @@ enum {
 };
 
 typedef struct {
-  int32_t kind;                /* PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET or PINT_OP_FEM1D_DIRICHLET */
+  int32_t kind;                /* PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET, PINT_OP_FEM1D_DIRICHLET or
+                                  PINT_OP_FEM2D_DIRICHLET */
   int64_t mx, my;              /* grid points per axis (1D: my = 1); M = mx*my */
 } pint_operator;
 

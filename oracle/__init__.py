@@ -16,7 +16,8 @@ listed in DESIGN.md §"Readings of the paper" and in SURVEY.md §8(c).
 Modules
   bdf        BDFk weights (exact), Table 1 corrections (exact), CQ weights, eigenvalues d_p
   spatial    FD Laplacian, DST-I, shifted spatial solves (DST eigen-solve / banded LU);
-             space="fem": 1D P1 finite elements, A = M^-1 K
+             space="fem": P1 finite elements, A = M^-1 K (1D mesh, 2D uniform triangulation;
+             PAPER.md:1374-1376)
   problem    static right-hand side  f̄_n + tau^-a (sum_{j<n} w_j) v
   sequential O1: corrected sequential BDFk / CQ-BDFk stepping (the WR fixed point)
   wr         O2: Algorithm 1/2 literally (explicit wrap loops, naive DFT matrices)

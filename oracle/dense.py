@@ -25,8 +25,9 @@ def iteration_system(prob, U_prev: np.ndarray):
     CQ:   j = 0..infinity, J_wrap = N-1, tail sum_{j>=N} omega_j = -sum_{j<N} omega_j.
     """
     N, M, tau, kap, a = prob.N, prob.M, prob.tau, prob.kappa, prob.alpha
-    if getattr(prob, "space", "fd") == "fem":        # A = M^{-1} K (P1 FEM, 1D)
-        K_, M_ = (x.toarray() for x in spatial.fem_matrices(prob.mx))
+    if getattr(prob, "space", "fd") == "fem":        # A = M^{-1} K (P1 FEM, 1D / 2D)
+        K_, M_ = (x.toarray() for x in (spatial.fem_matrices(prob.mx) if prob.my == 1
+                                        else spatial.fem2d_matrices(prob.mx, prob.my)))
         A = np.linalg.solve(M_, K_)
     else:
         A = spatial.laplacian_sparse(prob.mx, prob.my).toarray()

@@ -6,11 +6,14 @@ The paper discretizes with P1 FEM; BASELINE fixes the FD an
 (READING R-FD): A = -Delta_h, mass = I.
 2D arrays are flattened [iy][ix] (x fastest).
 
-space="fem" (1D only): piecewise-linear Galerkin on the uniform mesh
-(PAPER.md:1374-1375), stiffness K = (1/h) tridiag(-1, 2, -1), mass M = (h/6) tridiag(1, 4, 1).
+space="fem": piecewise-linear Galerkin.
+  1D: the uniform mesh of (0,1): stiffness K = (1/h) tridiag(-1, 2, -1), mass M = (h/6) tridiag(1, 4, 1).
+  2D: the uniform triangulation of (0,1)^2 (Example 3 PAPER.md:1567-1575): every cell
+      [x_a, x_a+1] x [y_b, y_b+1] split by the diagonal from (x_a, y_b) to (x_a+1, y_b+1) (reading
+      R-FEM2D); K and M assembled triangle by triangle from the P1 element matrices.
 The semi-discrete problem M U' + K U = M f~ is U' + A U = f~ with A = M^{-1} K (the discrete
 Laplacian -Delta_h of PAPER.md:196-203 in its FEM form); the shifted solves of Step 2 are
-(s M + K) x = M b.  Vectors are nodal coefficients.
+(s M + K) x = M b.  Vectors are nodal coefficients of the interior nodes (homogeneous Dirichlet).
 """
 from __future__ import annotations
 
@@ -34,6 +37,51 @@ def fem_matrices(m: int) -> tuple[sp.csc_matrix, sp.csc_matrix]:
     return sp.csc_matrix(K), sp.csc_matrix(Mm)
 
 
+def fem2d_matrices(mx: int, my: int) -> tuple[sp.csc_matrix, sp.csc_matrix]:
+    """(K, M) of P1 FEM on the uniform triangulation of (0,1)^2 with mx x my interior nodes
+    (h_x = 1/(mx+1), h_y = 1/(my+1)), interior node (ix, iy) -> index iy*mx + ix.  Assembled element
+    by element: for a triangle with vertices p_1..p_3 and area A, K_e[i,j] = (b_i b_j + c_i c_j)/(4A)
+    (b_i = y_{i+1} - y_{i+2}, c_i = x_{i+2} - x_{i+1}, indices cyclic) and M_e[i,j] = (A/12)(1 + [i = j]);
+    entries of boundary vertices are dropped (their coefficients are zero)."""
+    hx, hy = 1.0 / (mx + 1), 1.0 / (my + 1)
+    rows, cols, kv, mv = [], [], [], []
+
+    def idx(a, b):                    # grid vertex (a, b), a = 0..mx+1 -> interior index or -1
+        return (b - 1) * mx + (a - 1) if (1 <= a <= mx and 1 <= b <= my) else -1
+
+    for a in range(mx + 1):
+        for b in range(my + 1):
+            for tri in (((a, b), (a + 1, b), (a + 1, b + 1)), ((a, b), (a + 1, b + 1), (a, b + 1))):
+                xs = [v[0] * hx for v in tri]
+                ys = [v[1] * hy for v in tri]
+                area = 0.5 * abs((xs[1] - xs[0]) * (ys[2] - ys[0]) - (xs[2] - xs[0]) * (ys[1] - ys[0]))
+                bb = [ys[(i + 1) % 3] - ys[(i + 2) % 3] for i in range(3)]
+                cc = [xs[(i + 2) % 3] - xs[(i + 1) % 3] for i in range(3)]
+                ids = [idx(*v) for v in tri]
+                for i in range(3):
+                    for j in range(3):
+                        if ids[i] < 0 or ids[j] < 0:
+                            continue
+                        rows.append(ids[i])
+                        cols.append(ids[j])
+                        kv.append((bb[i] * bb[j] + cc[i] * cc[j]) / (4.0 * area))
+                        mv.append(area / 12.0 * (2.0 if i == j else 1.0))
+    n = mx * my
+    K = sp.csc_matrix((kv, (rows, cols)), shape=(n, n))
+    M = sp.csc_matrix((mv, (rows, cols)), shape=(n, n))
+    return K, M
+
+
+def solve_shifted_fem2d(shift: np.ndarray, b: np.ndarray, mx: int, my: int) -> np.ndarray:
+    """x_p = (shift_p M + K)^{-1} M b_p for each row p (2D P1 FEM; sparse LU, SuperLU)."""
+    K, Mm = fem2d_matrices(mx, my)
+    out = np.empty(b.shape, np.complex128)
+    for p in range(b.shape[0]):
+        lu = spla.splu(sp.csc_matrix(shift[p] * Mm.astype(np.complex128) + K))
+        out[p] = lu.solve((Mm @ b[p]).astype(np.complex128))
+    return out
+
+
 def _banded3(lo, d, up, b: np.ndarray) -> np.ndarray:
     """Tridiagonal solve (LAPACK banded LU), right-hand sides along the last axis."""
     m = len(d)
@@ -47,10 +95,13 @@ def _banded3(lo, d, up, b: np.ndarray) -> np.ndarray:
 
 def apply_A(u: np.ndarray, mx: int, my: int, space: str = "fd") -> np.ndarray:
     """A u with the 3-point (1D, my == 1) or 5-point (2D) stencil, zero Dirichlet values.
-    space="fem": A u = M^{-1} K u (1D).  Works on [..., M] arrays."""
+    space="fem": A u = M^{-1} K u (1D banded, 2D sparse LU).  Works on [..., M] arrays."""
+    if space == "fem" and my != 1:
+        K, Mm = fem2d_matrices(mx, my)
+        lu = spla.splu(sp.csc_matrix(Mm.astype(np.complex128)))
+        U = u.reshape(-1, mx * my)
+        return np.stack([lu.solve(K @ r) for r in U.astype(np.complex128)]).reshape(u.shape)
     if space == "fem":
-        if my != 1:
-            raise ValueError("P1 FEM is 1D only")
         K, _ = fem_matrices(mx)
         h = hstep(mx)
         Ku = (K @ u.reshape(-1, mx).T).T
@@ -122,6 +173,8 @@ def solve_shifted_dst(shift: np.ndarray, b: np.ndarray, mx: int, my: int, space:
     (exact in the shift: the shift is added to each eigenvalue, never rounded into 2/h^2;
     SURVEY §8(c) item 15).  shift: [P] complex.  space="fem": A = M^{-1} K (1D)."""
     shift = np.asarray(shift)
+    if space == "fem" and my != 1:        # 2D FEM: M is not diagonalised by the DST (R-FEM2D)
+        return solve_shifted_fem2d(shift, b, mx, my)
     if my == 1:
         lam = eigenvalues(mx, space)
         bh = dst1(b, axis=-1)

@@ -160,6 +160,22 @@ cudaError_t launch_spass(int C, const SPassArgs& a, long Qb, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_fem2d(const Fem2dArgs& a, bool init, cudaStream_t st) {
+  const long blocks = std::min<long>((a.total + 255) / 256, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  if (init) fem2d_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else fem2d_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fem2d_mixed(const double2* Y, double2* Z, long levels, int mx, int my, int NB, int WB, long total,
+                               cudaStream_t st) {
+  const long blocks = std::min<long>((total + 255) / 256, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  fem2d_mixed_kernel<<<(unsigned)blocks, 256, 0, st>>>(Y, Z, levels, mx, my, NB, WB, total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st) {
   if (a.count <= 0) return cudaSuccess;
   const long blocks = (a.count + 255) / 256;

@@ -119,44 +119,10 @@ cudaError_t launch_finish(const FinishArgs& a0, int mode, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// one thread: the host loop's stopping rule (pint.cu, pint_wr_solve), then the while-node condition
+// one thread: the stopping rule after the monitor (fully modal plans; otherwise the finish kernel's
+// last block does it, finish_loop_tail)
 __global__ void wr_loop_ctl_kernel(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h) {
-  if (s->done) {
-    cudaGraphSetConditional(h, 0);
-    return;
-  }
-  const double u = __longlong_as_double((long long)*upd);
-  s->u = u;
-  s->it += 1;
-  int stop = 0;
-  if (s->guard) {
-    if (!(u <= 1.7976931348623157e308)) {
-      s->status = 2;
-      stop = 1;
-    } else {
-      if (s->last >= 0.0 && u > s->last) {
-        if (++s->inc >= 3) {
-          s->status = 3;
-          stop = 1;
-        }
-      } else {
-        s->inc = 0;
-      }
-      s->last = u;
-      if (!stop && u < s->tol) {
-        s->status = 0;
-        stop = 1;
-      }
-    }
-  }
-  if (!stop && s->it >= s->max_it) {
-    s->status = 1;
-    stop = 1;
-  }
-  if (stop) {
-    s->done = 1;
-    cudaGraphSetConditional(h, 0);
-  }
+  loop_ctl_step(s, __longlong_as_double((long long)*upd), h);
 }
 
 cudaError_t launch_loop_ctl(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h, cudaStream_t st) {

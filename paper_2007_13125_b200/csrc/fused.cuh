@@ -559,16 +559,73 @@ struct FinishArgs {
   int L, Lf, Lpad, WB, NB, k, nk, nsparse, nch;
   int pstride;             // chunks per x-mode in the memory layout of P; nch = how many are summed
   const int* skip;         // device-side WR loop: return at once when *skip != 0 (see FusedArgs)
+  struct LoopCtl* ctl;     // device-side WR loop: the LAST block to finish applies the stopping rule
+  unsigned int* arrive;    //   (block arrival counter, reset by that block)
+  unsigned long long hnd;  //   while-node condition handle (cudaGraphConditionalHandle)
 };
-static_assert(sizeof(FinishArgs) == 152, "FinishArgs must stay padding-free");
+static_assert(sizeof(FinishArgs) == 176, "FinishArgs must stay padding-free");
 
 // Device-side WR loop (pint_wr_solve without a host round trip per iteration): the state of the
 // stopping rule of pint_wr_solve (update < tol, max_iters, 3 consecutive increases or a non-finite
-// update: PAPER.md:1747-1748), advanced by wr_loop_ctl_kernel after every iteration.
+// update: PAPER.md:1747-1748), advanced after every iteration by the last block of the finish
+// kernel (or by wr_loop_ctl_kernel when the monitor comes later: fully modal plans).
 struct LoopCtl {
   int it, max_it, status, done, inc, guard;   // status: 0 OK, 1 max_iters, 2 non-finite, 3 three increases
   double tol, last, u;                        // last < 0: no previous update
 };
+
+// the host loop's stopping rule (pint.cu, pint_wr_solve) for update u; clears the while condition
+__device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphConditionalHandle h) {
+  if (s->done) {
+    cudaGraphSetConditional(h, 0);
+    return;
+  }
+  s->u = u;
+  s->it += 1;
+  int stop = 0;
+  if (s->guard) {
+    if (!(u <= 1.7976931348623157e308)) {
+      s->status = 2;
+      stop = 1;
+    } else {
+      if (s->last >= 0.0 && u > s->last) {
+        if (++s->inc >= 3) {
+          s->status = 3;
+          stop = 1;
+        }
+      } else {
+        s->inc = 0;
+      }
+      s->last = u;
+      if (!stop && u < s->tol) {
+        s->status = 0;
+        stop = 1;
+      }
+    }
+  }
+  if (!stop && s->it >= s->max_it) {
+    s->status = 1;
+    stop = 1;
+  }
+  if (stop) {
+    s->done = 1;
+    cudaGraphSetConditional(h, 0);
+  }
+}
+
+// after this block's atomicMax into *upd: the last block to arrive reads the final update and
+// advances the loop (device-scope fence + arrival counter: every block's maximum is in before)
+__device__ __forceinline__ void finish_loop_tail(LoopCtl* ctl, unsigned int* arrive, unsigned long long hnd,
+                                                 const unsigned long long* upd) {
+  if (!ctl || threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(arrive, 1u) == gridDim.x - 1) {
+    *arrive = 0u;
+    __threadfence();
+    const double u = __longlong_as_double((long long)*(volatile const unsigned long long*)upd);
+    loop_ctl_step(ctl, u, (cudaGraphConditionalHandle)hnd);
+  }
+}
 
 #ifdef PINT_DEFINE_FUSED_KERNELS
 
@@ -881,6 +938,7 @@ __global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs 
   }
   if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
   block_max_atomic(updl, a.upd);
+  finish_loop_tail(a.ctl, a.arrive, a.hnd, a.upd);
 }
 
 
@@ -936,6 +994,7 @@ __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int 
   if (mode == FIN_PARTIALS) {
     if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
     block_max_atomic(updl, a.upd);
+    finish_loop_tail(a.ctl, a.arrive, a.hnd, a.upd);
   }
 }
 

@@ -7,6 +7,7 @@
 #include "fused.cuh"
 #include "newton.cuh"
 #include "cqpass.cuh"
+#include "fem2d.cuh"
 #include <algorithm>
 
 namespace pint {
@@ -24,6 +25,10 @@ cudaError_t launch_tpass_pruned(int N, const TPassArgs& a, long ntiles, cudaStre
 cudaError_t launch_tpass_cq_split(int N, int half, const TPassArgs& a, long ntiles, cudaStream_t st);
 // CQ FREQ -> H as one kernel (cqpass.cuh), N in {256, 1024}; UNSUPPORTED lengths return cudaErrorInvalidValue
 cudaError_t launch_tpass_cq_fused(int N, const CQArgs& a, cudaStream_t st);
+// 2D P1-FEM Step 2 (fem2d.cuh, dispatch.cu): fixed-point init / step, the mixed stencil Dx Dy / 24
+cudaError_t launch_fem2d(const Fem2dArgs& a, bool init, cudaStream_t st);
+cudaError_t launch_fem2d_mixed(const double2* Y, double2* Z, long levels, int mx, int my, int NB, int WB, long total,
+                               cudaStream_t st);
 // layout remaps and the FD stencil (dispatch.cu)
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);

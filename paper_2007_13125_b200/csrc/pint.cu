@@ -145,6 +145,11 @@ struct pint_plan_s {
   bool half = false;          // PINT_FLAG_REAL_DATA: half-spectrum fused iteration
   bool modal = false;         // PINT_FLAG_MODAL: DST along y too, one warp per (q, j) mode
   bool fem = false;           // PINT_OP_FEM1D_DIRICHLET (modal, mu_j = h^2 K_j / M_j)
+  bool fem2d = false;         // PINT_OP_FEM2D_DIRICHLET (modal + streaming, Step 2 by fem2d_solve)
+  double *fcx = nullptr, *fcy = nullptr;       // [Qb] cos(q pi h), [L] cos(j pi h)
+  double2 *fb = nullptr, *fe = nullptr, *ft = nullptr;   // fem2d_solve: right-hand side, E X, scratch
+  unsigned long long* fupd = nullptr;          // [2] fem2d_solve monitors
+  int fem_iters = 0;                           // inner iterations of the last fem2d_solve (introspection)
   int NEy = 0;
   double2* twEy = nullptr;    // [NEy] DST-y twiddles
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
@@ -200,6 +205,9 @@ struct pint_plan_s {
   // device-side WR loop (pint_wr_solve on the fused path): a graph with a while-conditional node whose
   // body runs two iterations (both ping-pong parities) each followed by the stopping-rule kernel
   const int* cap_skip = nullptr;   // during its capture: the kernels' early-exit flag (LoopCtl::done)
+  LoopCtl* cap_ctl = nullptr;      // during its capture (fused, non-modal-monitor plans): the finish
+  unsigned long long cap_hnd = 0;  //   kernel's last block applies the stopping rule
+  unsigned int* larrive = nullptr; // its block arrival counter
   LoopCtl* lctl = nullptr;         // device state of the loop
   LoopCtl* lctl_h = nullptr;       // pinned host copy
   cudaGraphExec_t lexec[4] = {};   // per (wcur, xcur) at loop entry
@@ -330,29 +338,38 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (N < k + 1) return fail(PINT_ERR_ARG, "N must be >= k+1 (DESIGN.md reading R-Nk)");
   const double alpha = opt ? opt->alpha : 1.0;
   if (!(alpha > 0.0 && alpha <= 1.0)) return fail(PINT_ERR_ARG, "alpha must be in (0,1]");
-  if (op->kind != PINT_OP_FD1D_DIRICHLET && op->kind != PINT_OP_FD2D_DIRICHLET && op->kind != PINT_OP_FEM1D_DIRICHLET)
-    return fail(PINT_ERR_ARG, "op->kind must be PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET or PINT_OP_FEM1D_DIRICHLET");
+  if (op->kind != PINT_OP_FD1D_DIRICHLET && op->kind != PINT_OP_FD2D_DIRICHLET && op->kind != PINT_OP_FEM1D_DIRICHLET &&
+      op->kind != PINT_OP_FEM2D_DIRICHLET)
+    return fail(PINT_ERR_ARG, "op->kind must be PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET, PINT_OP_FEM1D_DIRICHLET "
+                              "or PINT_OP_FEM2D_DIRICHLET");
   if (op->mx < 1 || op->my < 1) return fail(PINT_ERR_ARG, "op->mx, op->my must be >= 1");
   const bool fem = op->kind == PINT_OP_FEM1D_DIRICHLET;
+  const bool fem2d = op->kind == PINT_OP_FEM2D_DIRICHLET;
+  const bool two_d = op->kind == PINT_OP_FD2D_DIRICHLET || fem2d;
+  if (fem2d && op->mx != op->my) return fail(PINT_ERR_UNSUPPORTED, "PINT_OP_FEM2D_DIRICHLET needs mx == my (uniform triangulation, h_x = h_y)");
   if ((op->kind == PINT_OP_FD1D_DIRICHLET || fem) && op->my != 1) return fail(PINT_ERR_ARG, "1D operator needs my == 1");
   if (op->mx * op->my != M) return fail(PINT_ERR_ARG, "M must equal mx*my");
   const int rank = opt ? opt->rank : 0, nranks = opt ? opt->nranks : 1;
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PINT_ERR_ARG, "need 0 <= rank < nranks");
   if (nranks > 1 && op->kind != PINT_OP_FD2D_DIRICHLET)
-    return fail(PINT_ERR_ARG, "1D operators do not shard (replicas only): nranks must be 1");
+    return fail(fem2d ? PINT_ERR_UNSUPPORTED : PINT_ERR_ARG,
+                fem2d ? "2D P1-FEM couples the x-modes (mass matrix): one rank only"
+                      : "1D operators do not shard (replicas only): nranks must be 1");
   if (nranks > op->mx) return fail(PINT_ERR_ARG, "nranks must be <= mx");
   if (opt && (opt->flags & PINT_FLAG_DST_PER_ITER) && (op->kind != PINT_OP_FD2D_DIRICHLET || nranks != 1))
     return fail(PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator on one rank");
-  const int32_t flags = (opt ? opt->flags : 0) | (fem ? PINT_FLAG_MODAL : 0);   // P1-FEM runs modal
+  // P1-FEM runs modal (1D: diagonal; 2D: the mass matrix's M_sym part is, fem2d.cuh), 2D FEM on the
+  // streaming path (its Step 2 is the fem2d fixed-point solve)
+  const int32_t flags = (opt ? opt->flags : 0) | ((fem || fem2d) ? PINT_FLAG_MODAL : 0) | (fem2d ? PINT_FLAG_STREAM : 0);
   if (flags & PINT_FLAG_MODAL) {
-    const int64_t Lm = op->kind == PINT_OP_FD2D_DIRICHLET ? op->my : op->mx;
+    const int64_t Lm = two_d ? op->my : op->mx;
     if (flags & PINT_FLAG_DST_PER_ITER) return fail(PINT_ERR_ARG, "PINT_FLAG_MODAL excludes PINT_FLAG_DST_PER_ITER");
     if (!is_pow2(2 * (Lm + 1)) || 2 * (Lm + 1) < 16 || 2 * (Lm + 1) > 4096)
       return fail(PINT_ERR_UNSUPPORTED, "PINT_FLAG_MODAL needs 2(L+1) a power of two in [16, 4096] (L = my in 2D, mx in 1D)");
   }
   if (nranks > 1 && !(opt && opt->allreduce_max)) return fail(PINT_ERR_ARG, "nranks > 1 needs allreduce_max");
   if (!is_pow2(N) || N < 16 || N > 4096) return fail(PINT_ERR_UNSUPPORTED, "N must be a power of two in [16, 4096]");
-  const int dim = op->kind == PINT_OP_FD2D_DIRICHLET ? 2 : 1;
+  const int dim = two_d ? 2 : 1;
   const int64_t L = dim == 1 ? op->mx : op->my;
   if (L > 1024) return fail(PINT_ERR_UNSUPPORTED, "line length (1D: mx, 2D: my) must be <= 1024");
   int NE = 0;
@@ -363,7 +380,7 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
 
   pint_plan p = new pint_plan_s();
   p->M = M; p->N = N; p->mx = op->mx; p->my = op->my; p->k = k; p->dim = dim;
-  p->flags = flags; p->rank = rank; p->nranks = nranks; p->fem = fem;
+  p->flags = flags; p->rank = rank; p->nranks = nranks; p->fem = fem; p->fem2d = fem2d;
   p->kappa = kappa; p->tau = tau; p->alpha = alpha;
   p->allreduce = opt ? opt->allreduce_max : nullptr; p->actx = opt ? opt->allreduce_ctx : nullptr;
   p->L = L; p->h = 1.0 / (double)(L + 1); p->NE = NE;
@@ -445,6 +462,19 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
   if (p->modal) {   // DST along the line axis (fused modal kernel, or division pass of the streaming path)
     if ((st = dalloc(p, &p->twEy, p->NEy)) != PINT_OK) return bail(st);
     if ((st = dalloc(p, &p->mu, (size_t)L)) != PINT_OK) return bail(st);
+  }
+  if (fem2d) {      // 2D P1-FEM Step 2 (fem2d.cuh): mode cosines, fixed-point buffers
+    std::vector<double> cx(p->Qb), cy(L);
+    for (int64_t q = 0; q < p->Qb; ++q) cx[q] = (double)cosl((ld)(p->q0 + q + 1) * PI_L / (ld)(op->mx + 1));
+    for (int64_t j = 0; j < L; ++j) cy[j] = (double)cosl((ld)(j + 1) * PI_L / (ld)(L + 1));
+    if ((st = dalloc(p, &p->fcx, p->Qb)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->fcy, (size_t)L)) != PINT_OK) return bail(st);
+    if ((st = h2d(p, p->fcx, cx)) != PINT_OK) return bail(st);
+    if ((st = h2d(p, p->fcy, cy)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->fb, arr)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->fe, arr)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->ft, arr)) != PINT_OK) return bail(st);
+    if ((st = dalloc(p, &p->fupd, 2)) != PINT_OK) return bail(st);
   }
   if (p->fused_ok && p->modal) {
     // physical-space window monitor (one rank: the DST-x back needs every x-mode): the orthonormal
@@ -679,7 +709,19 @@ static pint_status tpass(pint_plan p, int mode_in, int mode_out, const double2* 
   return PINT_OK;
 }
 
+static pint_status fem2d_solve(pint_plan p, const double2* H, double2* X, long levels, bool av);
+
 static pint_status spass(pint_plan p, const double2* in, double2* out) {
+  if (p->fem2d) {   // 2D P1-FEM: (s_p M + K) W = M H by the DST-preconditioned fixed point (fem2d.cuh)
+    cudaEvent_t m0 = nullptr, m1 = nullptr;
+    if (p->timing) {
+      CUDA_TRY(cudaEventCreate(&m0)); CUDA_TRY(cudaEventCreate(&m1));
+      CUDA_TRY(cudaEventRecord(m0, p->stream));
+    }
+    TRY(fem2d_solve(p, in, out, p->N, false));
+    if (m0) { CUDA_TRY(cudaEventRecord(m1, p->stream)); p->sev.push_back({m0, m1}); }
+    return PINT_OK;
+  }
   SPassArgs a{};
   a.in = in; a.out = out; a.sig_p = p->sig_p; a.sig_q = p->sig_q;
   a.N = p->N; a.NB = p->NB; a.WB = p->WB; a.L = (int)p->L; a.lc = p->slc;
@@ -764,6 +806,7 @@ static FinishArgs finargs(pint_plan p, const double2* wold, double2* wnew, doubl
   a.N = p->N; a.Qb = p->Qb; a.L = (int)p->L; a.Lf = p->Lf; a.Lpad = (int)(p->NB * p->WB); a.WB = p->WB;
   a.NB = (int)p->NB; a.k = p->k; a.nk = p->nk; a.nch = p->nch; a.pstride = p->nch;
   a.skip = p->cap_skip;
+  a.ctl = p->cap_ctl; a.arrive = p->cap_ctl ? p->larrive : nullptr; a.hnd = p->cap_hnd;
   return a;
 }
 
@@ -828,6 +871,57 @@ static pint_status to_source(pint_plan p, const double2* phys_vec, int s) {
   CUDA_TRY(launch_dst(p->NE, a, DST_PHYS_TO_SRC, p->stream));
   ++p->launches;
   return PINT_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// 2D P1-FEM Step 2 (fem2d.cuh): E = Dx Dy / 24 applied in physical space, fixed point in the modes
+// ------------------------------------------------------------------------------------------
+static pint_status fem2d_applyE(pint_plan p, const double2* Y, double2* Z, long levels) {
+  TRY(dst_y(p, Y, p->ft, levels, p->Qb));                           // (q, j) -> (q, y)
+  DstArgs d = dargs(p);
+  d.rows = levels * p->my; d.N = levels; d.n0 = 0;
+  d.in = p->ft; d.out = Z;
+  CUDA_TRY(launch_dst(p->NE, d, DST_INT_TO_INT, p->stream));        // (q, y) -> (x, y)
+  const long total = p->Qb * p->NB * levels * p->WB;
+  CUDA_TRY(launch_fem2d_mixed(Z, p->ft, levels, (int)p->mx, (int)p->my, (int)p->NB, p->WB, total, p->stream));
+  d.in = p->ft; d.out = Z;
+  CUDA_TRY(launch_dst(p->NE, d, DST_INT_TO_INT, p->stream));        // (x, y) -> (q, y)
+  TRY(dst_y(p, Z, Z, levels, p->Qb));                               // (q, y) -> (q, j)
+  p->launches += 3;
+  return PINT_OK;
+}
+
+// X = (s_p M + K)^{-1} M H per level (av: X = M^{-1} K H), modal tile layout with `levels` levels.
+// Fixed point X <- P^{-1} (b - s E X), P = s M_sym + K, until max |dX| <= 2^-50 max |X| (at most 300
+// steps); one synchronisation per step (the stopping test).
+static pint_status fem2d_solve(pint_plan p, const double2* H, double2* X, long levels, bool av) {
+  Fem2dArgs f{};
+  f.b = p->fb; f.H = H; f.X = X; f.sig_p = p->sig_p; f.sig_q = p->sig_q; f.mu = p->mu; f.cx = p->fcx; f.cy = p->fcy;
+  f.levels = levels; f.total = p->Qb * p->NB * levels * p->WB; f.L = (int)p->L; f.NB = (int)p->NB; f.WB = p->WB;
+  f.av = av ? 1 : 0; f.kscale = 1.0 / (p->h * p->h); f.upd = p->fupd;
+  CUDA_TRY(cudaMemsetAsync(p->fupd, 0, 2 * sizeof(unsigned long long), p->stream));
+  if (!av) TRY(fem2d_applyE(p, H, p->fe, levels));
+  f.EH = p->fe;
+  CUDA_TRY(launch_fem2d(f, true, p->stream));
+  ++p->launches;
+  unsigned long long bits[2];
+  CUDA_TRY(cudaMemcpyAsync(bits, p->fupd, sizeof(bits), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  double xmax;
+  std::memcpy(&xmax, &bits[1], sizeof(double));
+  for (int it = 1; it <= 300; ++it) {
+    TRY(fem2d_applyE(p, X, p->fe, levels));
+    CUDA_TRY(cudaMemsetAsync(p->fupd, 0, sizeof(unsigned long long), p->stream));
+    CUDA_TRY(launch_fem2d(f, false, p->stream));
+    ++p->launches;
+    CUDA_TRY(cudaMemcpyAsync(bits, p->fupd, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    double d;
+    std::memcpy(&d, &bits[0], sizeof(double));
+    if (!std::isfinite(d)) return fail(PINT_ERR_DIVERGED, "2D FEM inner fixed point: non-finite update");
+    if (d <= 0x1p-50 * xmax) { p->fem_iters = it; return PINT_OK; }
+  }
+  return fail(PINT_ERR_NOT_CONVERGED, "2D FEM inner fixed point: no convergence in 300 steps");
 }
 
 // ------------------------------------------------------------------------------------------
@@ -910,6 +1004,7 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
     CUDA_TRY(launch_mode_scale(p->src + (size_t)p->ntiles * p->WB, p->src, p->mu, 1.0 / (p->h * p->h), (int)p->L, p->stream));
     ++p->launches;
   }
+  if (p->fem2d) TRY(fem2d_solve(p, p->src, p->src + (size_t)p->ntiles * p->WB, 1, true));   // A v = M^{-1} K v
   if (chk_real) {
     double im = 0.0;
     unsigned long long bits = 0;
@@ -1167,6 +1262,8 @@ static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool g
                               int* status) {
   if (!p->lctl) {
     TRY(dalloc(p, &p->lctl, 1));
+    TRY(dalloc(p, &p->larrive, 1));
+    CUDA_TRY(cudaMemsetAsync(p->larrive, 0, sizeof(unsigned int), p->stream));
     CUDA_TRY(cudaHostAlloc((void**)&p->lctl_h, sizeof(LoopCtl), cudaHostAllocDefault));
   }
   const int key = p->wcur * 2 + p->xcur;
@@ -1199,20 +1296,23 @@ static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool g
     const int64_t l0 = p->launches;
     const int w0 = p->wcur, x0 = p->xcur;
     p->cap_skip = &p->lctl->done;
+    if (!p->pmon) { p->cap_ctl = p->lctl; p->cap_hnd = (unsigned long long)hnd; }   // ctl in the finish kernel
     pint_status st = PINT_OK;
     for (int h = 0; h < 2 && st == PINT_OK; ++h) {
       p->wcur = w0 ^ h;
       p->xcur = x0 ^ h;
       st = fused_kernels(p);
-      if (st == PINT_OK) {
+      if (st == PINT_OK && p->pmon) {
         const cudaError_t ec = launch_loop_ctl(p->lctl, p->upd, hnd, p->stream);
         if (ec != cudaSuccess) st = fail(PINT_ERR_CUDA, std::string("loop ctl: ") + cudaGetErrorString(ec));
       }
     }
     p->cap_skip = nullptr;
+    p->cap_ctl = nullptr;
+    p->cap_hnd = 0;
     p->wcur = w0;
     p->xcur = x0;
-    p->llaunch[key] = (p->launches - l0) / 2 + 1;   // + the ctl kernel (not counted by launch_loop_ctl)
+    p->llaunch[key] = (p->launches - l0) / 2 + (p->pmon ? 1 : 0);   // + the ctl kernel (modal monitor)
     p->launches = l0;
     cudaGraph_t body = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(p->stream, &body);
@@ -1815,8 +1915,8 @@ extern "C" pint_status pint_residual(pint_plan p, double* residual_inf, double* 
 static pint_status residual_local(pint_plan p, double* r_out, double* f_out) {
   if (!p->problem_set) return fail(PINT_ERR_STATE, "call pint_set_problem_separable first");
   if (p->m == 0) return fail(PINT_ERR_STATE, "no WR iterate computed yet (m = 0)");
-  if (p->nl || p->dst_iter || p->has_fd || (p->alpha != 1.0 && p->modal))
-    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: separable data; CQ on the line-solve path");
+  if (p->nl || p->dst_iter || p->has_fd || (p->alpha != 1.0 && p->modal) || p->fem2d)
+    return fail(PINT_ERR_UNSUPPORTED, "pint_residual: separable data; CQ on the line-solve path; not 2D P1-FEM");
   CUDA_TRY(cudaSetDevice(p->device));
   TRY(materialize(p));                     // U_m, x in DST modes, y physical (tile layout)
   const double2* U = ucur(p);

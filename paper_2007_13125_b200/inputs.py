@@ -41,7 +41,8 @@ class Problem:
     dphi: np.ndarray   # float64 [R][max(k-2,0)]
     u0: str = "v"      # WR initial guess: "v" or "zero" (tables)
     tol: float = 1e-12
-    space: str = "fd"  # "fd": 3/5-point stencil (BASELINE); "fem": 1D P1 Galerkin,
+    space: str = "fd"  # "fd": 3/5-point stencil (BASELINE); "fem": P1 Galerkin (1D mesh / 2D uniform
+                       # triangulation),
                        # v and g_r are then nodal coefficient vectors
 
     @property
@@ -184,6 +185,23 @@ def example1_fem(k: int, M: int = 999, N: int = 100, kappa: float = 0.5) -> Prob
     """The paper's Example 1 in its own discretisation (P1 FEM):
     v_h and f~ = the nodal interpolants of chi_(0,1/2) and e^t cos x (READING R-FEMdata), U_0 = 0."""
     return example1_fd(k, M, N, kappa).with_(name=f"E1fem_k{k}", space="fem")
+
+
+def example3_fem(k: int = 3, m: int = 63, N: int = 128, T: float = 0.1, kappa: float = 0.05,
+                 alpha: float = 0.5) -> Problem:
+    """The paper's Example 3 in its own discretisation on a reduced grid: 2D
+    subdiffusion on the uniform triangulation of the unit square (P1 FEM, space="fem", m x m interior
+    nodes), v = chi_{(0,1/2)^2}, f = cos(t) chi_{(1/2,1)^2}, as nodal interpolants of the OPEN sets
+    (READING R-FEMdata); the paper uses h = 1e-2, tau = 1e-3 (Figure 3)."""
+    x = grid1d(m)
+    X, Y = np.meshgrid(x, x)                       # [iy][ix]
+    v = ((X < 0.5) & (Y < 0.5)).astype(np.complex128).reshape(-1)
+    g = ((X > 0.5) & (Y > 0.5)).astype(np.complex128).reshape(1, -1)
+    t = np.arange(N + 1) * (T / N)
+    phi = np.cos(t)[None, :]
+    nd = max(k - 2, 0)
+    dphi = np.array([[[1.0, 0.0, -1.0, 0.0][l % 4] for l in range(1, nd + 1)]]).reshape(1, nd)   # cos^(l)(0)
+    return Problem(f"E3fem_k{k}_a{alpha}", m, m, T, N, k, kappa, alpha, v, g, phi, dphi, space="fem")
 
 
 def example2_fd(k: int, M: int = 999, N: int = 100, kappa: float = 0.1,

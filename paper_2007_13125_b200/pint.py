@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("PINT_LIB", os.path.join(HERE, "libpint.so"))
 
 PINT_OK, PINT_ERR_ARG, PINT_ERR_ALLOC, PINT_ERR_CUDA, PINT_ERR_COMM, PINT_ERR_STATE, \
     PINT_ERR_NOT_CONVERGED, PINT_ERR_DIVERGED, PINT_ERR_UNSUPPORTED = range(9)
-PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET, PINT_OP_FEM1D_DIRICHLET = 1, 2, 3
+PINT_OP_FD1D_DIRICHLET, PINT_OP_FD2D_DIRICHLET, PINT_OP_FEM1D_DIRICHLET, PINT_OP_FEM2D_DIRICHLET = 1, 2, 3, 4
 PINT_HOST, PINT_DEVICE = 0, 1
 PINT_FLAG_U0_ZERO = 1
 PINT_FLAG_FULL_FFT = 2
@@ -149,11 +149,15 @@ class Plan:
                  rank: int = 0, nranks: int = 1, allreduce_max=None, full_fft: bool = False,
                  stream_path: bool = False, dst_per_iter: bool = False, real_data: bool = False,
                  modal: bool = False, fem: bool = False, full_update_norm: bool = False):
-        """fem=True: 1D P1 finite elements (PINT_OP_FEM1D_DIRICHLET; nodal coefficient vectors)."""
+        """fem=True: P1 finite elements (1D mesh: PINT_OP_FEM1D_DIRICHLET; 2D uniform triangulation:
+        PINT_OP_FEM2D_DIRICHLET; nodal coefficient vectors)."""
         L = lib()
         self.mx, self.my, self.N, self.k = int(mx), int(my), int(N), int(k)
         self.M = self.mx * self.my
-        kind = PINT_OP_FEM1D_DIRICHLET if fem else (PINT_OP_FD1D_DIRICHLET if my == 1 else PINT_OP_FD2D_DIRICHLET)
+        if fem:
+            kind = PINT_OP_FEM1D_DIRICHLET if my == 1 else PINT_OP_FEM2D_DIRICHLET
+        else:
+            kind = PINT_OP_FD1D_DIRICHLET if my == 1 else PINT_OP_FD2D_DIRICHLET
         op = pint_operator(kind, mx, my)
         self._cb = ALLREDUCE_FN(0)
         if allreduce_max is not None:

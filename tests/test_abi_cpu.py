@@ -47,7 +47,9 @@ def test_status_strings_and_kappa_rule():
     (dict(mx=100, my=10), P.PINT_ERR_UNSUPPORTED, "2(mx+1)"),
     (dict(nranks=2, rank=0), P.PINT_ERR_ARG, "1D operators do not shard"),
     (dict(dst_per_iter=True), P.PINT_ERR_ARG, "PINT_FLAG_DST_PER_ITER needs a 2D operator"),
-    (dict(fem=True, mx=63, my=3), P.PINT_ERR_ARG, "1D operator needs my == 1"),
+    (dict(fem=True, mx=63, my=3), P.PINT_ERR_UNSUPPORTED, "needs mx == my"),          # 2D P1-FEM: square grid
+    (dict(fem=True, mx=63, my=63, nranks=2, rank=0), P.PINT_ERR_UNSUPPORTED, "one rank only"),
+    (dict(fem=True, mx=62, my=62), P.PINT_ERR_UNSUPPORTED, "2(L+1) a power of two"),
     (dict(fem=True, mx=62), P.PINT_ERR_UNSUPPORTED, "2(L+1) a power of two"),
     (dict(modal=True, mx=62), P.PINT_ERR_UNSUPPORTED, "2(L+1) a power of two"),
     (dict(modal=True, mx=63, my=63, dst_per_iter=True), P.PINT_ERR_ARG, "PINT_FLAG_MODAL excludes"),

@@ -292,3 +292,83 @@ def test_table2_example1_fem(k):
     e = [float(np.sqrt(np.real(np.vdot(U[-1] - Us[-1], Mm @ (U[-1] - Us[-1]))))) for U in wr.wr_naive(p, 3)]
     for m in range(4):
         assert abs(e[m] - g[m][k - 1]) <= 0.011 * g[m][k - 1] + 1e-13, (k, m, e[m], g[m][k - 1])
+
+
+# --- 2D P1 FEM on the uniform triangulation -------
+
+def _shift(m):
+    return sp_diags([np.ones(m - 1)], [1]).toarray()     # (S u)_i = u_{i+1}, zero Dirichlet padding
+
+
+def sp_diags(d, o):
+    import scipy.sparse as sps
+    return sps.diags(d, o, shape=(len(d[0]) + abs(o[0]), len(d[0]) + abs(o[0])))
+
+
+@pytest.mark.parametrize("mx,my", [(5, 4), (7, 7)])
+def test_fem2d_assembly(mx, my):
+    """Element-by-element P1 assembly on the right-triangle mesh, pinned to closed forms:
+    K = h_x h_y (-Delta_h) (the 5-point stencil: right triangles give no diagonal couplings);
+    M = M_sym + (h_x h_y / 24) Dx (x) Dy with M_sym = (h_x h_y / 12)(6 + Tx + Ty + Tx Ty / 2),
+    T = S + S^T, D = S - S^T (the '/'-diagonal neighbours carry h_x h_y / 12, the '\\' ones 0);
+    interior row sums of M are the patch areas h_x h_y; M reproduces linear functions there."""
+    K, Mm = (x.toarray() for x in spatial.fem2d_matrices(mx, my))
+    hx, hy = 1.0 / (mx + 1), 1.0 / (my + 1)
+    assert np.abs(K - hx * hy * spatial.laplacian_sparse(mx, my).toarray()).max() < 1e-13
+    Sx, Sy = _shift(mx), _shift(my)
+    Tx, Ty, Dx, Dy = Sx + Sx.T, Sy + Sy.T, Sx - Sx.T, Sy - Sy.T
+    Ix, Iy = np.eye(mx), np.eye(my)
+    Msym = hx * hy / 12 * (6 * np.kron(Iy, Ix) + np.kron(Iy, Tx) + np.kron(Ty, Ix) + 0.5 * np.kron(Ty, Tx))
+    E = hx * hy / 24 * np.kron(Dy, Dx)
+    assert np.abs(Mm - (Msym + E)).max() < 1e-15
+    assert np.abs(Mm - Mm.T).max() == 0.0 and np.linalg.eigvalsh(Mm).min() > 0
+    X, Y = np.meshgrid(np.arange(1, mx + 1) * hx, np.arange(1, my + 1) * hy)
+    g = (1 + 2 * X - 3 * Y).reshape(-1)
+    inner = np.zeros((my, mx), bool)
+    inner[1:-1, 1:-1] = True
+    inner = inner.reshape(-1)
+    assert np.allclose(Mm.sum(axis=1)[inner], hx * hy, rtol=1e-13, atol=0)
+    assert np.allclose((Mm @ g)[inner], hx * hy * g[inner], rtol=1e-13, atol=0)
+
+
+def test_fem2d_solves_and_apply():
+    """The shifted solves satisfy (s M + K) x = M b; apply_A = M^{-1} K (dense)."""
+    mx, my, rng = 6, 5, np.random.default_rng(7)
+    K, Mm = (x.toarray() for x in spatial.fem2d_matrices(mx, my))
+    shifts = np.array([3.0 + 40j, 1e-3 - 2e-3j, 250.0])
+    b = rng.standard_normal((3, mx * my)) + 1j * rng.standard_normal((3, mx * my))
+    x = spatial.solve_shifted_dst(shifts, b, mx, my, "fem")
+    for i, s in enumerate(shifts):
+        assert np.abs((s * Mm + K) @ x[i] - Mm @ b[i]).max() <= 1e-12 * np.abs(Mm @ b[i]).max()
+    u = b[0]
+    assert np.allclose(spatial.apply_A(u, mx, my, "fem"), np.linalg.solve(Mm, K @ u), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_fem2d_observed_order(k):
+    """BDFk with the 2D FEM operator converges at order k to the exact semi-discrete solution
+    e^{-A t} v (A = M^{-1} K from LAPACK's generalised eigensolver on the assembled K, M)."""
+    mx = my = 7
+    K, Mm = (x.toarray() for x in spatial.fem2d_matrices(mx, my))
+    lam, Q = scipy.linalg.eigh(K, Mm)
+    v = (np.random.default_rng(3).standard_normal(mx * my)).astype(complex)
+    exact = Q @ (np.exp(-lam * 0.1) * (Q.T @ (Mm @ v)))          # Q^T M Q = I
+    errs = []
+    for N in (64, 128):
+        p = inputs.random_complex_problem(mx, my, N, k, 0.05, 1.0, R=0, seed=1, T=0.1).with_(
+            space="fem", v=v)
+        errs.append(np.abs(sequential.sequential(p)[-1] - exact).max())
+    rate = np.log2(errs[0] / errs[1])
+    assert abs(rate - k) < 0.35, (k, rate, errs)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_fem2d_fixed_point_and_dense(alpha):
+    """2D FEM: the WR iteration converges to sequential FEM stepping, and one iteration equals the
+    dense all-at-once kappa-periodic solve with A = M^{-1} K."""
+    p = inputs.random_complex_problem(5, 4, 16, 3, 0.05, alpha, R=1, seed=5).with_(space="fem")
+    Us = sequential.sequential(p)
+    U = wr.wr_naive(p, 12)[-1]
+    assert np.linalg.norm(U - Us) <= 1e-11 * np.linalg.norm(Us)
+    U0 = wr.initial_guess(p)
+    assert rel(wr.wr_naive(p, 1, U0=U0)[1], dense.dense_iteration(p, U0)) < 1e-12
