@@ -125,6 +125,43 @@ __global__ void wr_loop_ctl_kernel(LoopCtl* s, const unsigned long long* upd, cu
   loop_ctl_step(s, __longlong_as_double((long long)*upd), h);
 }
 
+// the cooperative whole-loop kernel (fused.cuh wr_loop_kernel): NKC 4 or 8
+template <int C, int NKC>
+static cudaError_t loop_go(const LoopKArgs& L, long grid, int k, cudaStream_t st, int* capacity) {
+  auto kern = wr_loop_kernel<C, NKC>;
+  const size_t smem = fused_smem_bytes(32, C, k, true);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (capacity) {   // co-resident CTAs on this device (the cooperative launch requires grid <= it)
+    int per = 0, dev = 0, nsm = 148;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FG * 32, smem);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    *capacity = per * nsm;
+    return cudaSuccess;
+  }
+  void* args[] = {(void*)&L};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(FG * 32), args, smem, st);
+}
+
+template <int NKC>
+static cudaError_t loop_c(int C, const LoopKArgs& L, long grid, int k, cudaStream_t st, int* capacity) {
+  switch (C) {
+    case 1: return loop_go<1, NKC>(L, grid, k, st, capacity);
+    case 2: return loop_go<2, NKC>(L, grid, k, st, capacity);
+    case 4: return loop_go<4, NKC>(L, grid, k, st, capacity);
+    case 8: return loop_go<8, NKC>(L, grid, k, st, capacity);
+    case 16: return loop_go<16, NKC>(L, grid, k, st, capacity);
+    case 32: return loop_go<32, NKC>(L, grid, k, st, capacity);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_loop_kernel(int C, int nk, const LoopKArgs& L, long grid, int k, cudaStream_t st, int* capacity) {
+  return nk <= 4 ? loop_c<4>(C, L, grid, k, st, capacity) : loop_c<8>(C, L, grid, k, st, capacity);
+}
+
 cudaError_t launch_loop_ctl(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h, cudaStream_t st) {
   wr_loop_ctl_kernel<<<1, 1, 0, st>>>(s, upd, h);
   return cudaGetLastError();

@@ -574,12 +574,10 @@ struct LoopCtl {
   double tol, last, u;                        // last < 0: no previous update
 };
 
-// the host loop's stopping rule (pint.cu, pint_wr_solve) for update u; clears the while condition
-__device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphConditionalHandle h) {
-  if (s->done) {
-    cudaGraphSetConditional(h, 0);
-    return;
-  }
+// the host loop's stopping rule (pint.cu, pint_wr_solve) for update u: advances the state, returns
+// true (and sets done) when the loop stops
+__device__ __forceinline__ bool loop_ctl_eval(LoopCtl* s, double u) {
+  if (s->done) return true;
   s->u = u;
   s->it += 1;
   int stop = 0;
@@ -607,10 +605,46 @@ __device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphCon
     s->status = 1;
     stop = 1;
   }
-  if (stop) {
-    s->done = 1;
-    cudaGraphSetConditional(h, 0);
+  if (stop) s->done = 1;
+  return stop != 0;
+}
+// ... and clears the while-node condition of the device-loop graph
+__device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphConditionalHandle h) {
+  if (loop_ctl_eval(s, u)) cudaGraphSetConditional(h, 0);
+}
+
+// the whole WR loop as one cooperative kernel (wr_loop_kernel below)
+struct GridBar { unsigned int count, gen; };
+struct LoopKArgs {
+  FusedArgs fa[2];           // the two ping-pong parities (X in, window in/out)
+  FinishArgs fin[2];
+  LoopCtl* ctl;
+  GridBar* bar;
+};
+
+// grid-wide barrier of a co-resident (cooperatively launched) grid; the last block to arrive runs
+// the stopping rule on the iteration's update (and resets the monitor) before releasing the others
+__device__ __forceinline__ void grid_sync(GridBar* b, LoopCtl* ctl, unsigned long long* upd) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &b->gen;
+    const unsigned int g = *vgen;
+    __threadfence();                                   // this block's writes before its arrival
+    if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+      if (ctl) {
+        const double u = __longlong_as_double((long long)*(volatile unsigned long long*)upd);
+        *upd = 0ull;
+        loop_ctl_eval(ctl, u);
+      }
+      b->count = 0u;
+      __threadfence();
+      atomicExch(&b->gen, g + 1u);
+    } else {
+      while (*vgen == g) __nanosleep(40);
+    }
+    __threadfence();
   }
+  __syncthreads();
 }
 
 // after this block's atomicMax into *upd: the last block to arrive reads the final update and
@@ -643,14 +677,12 @@ template <int C, int LANES, int NKC = 8> struct FTmem {
 // HALF: real-data half spectrum (PINT_FLAG_REAL_DATA; instantiated with TM only).
 // NKC: compile-time bound on nk (and k): X_t = 0 for t >= NKC and window slots r < 8 - NKC are
 // unused, so the synthesis twiddles and the DFT8 butterflies on those zeros/outputs are pruned.
-template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false, int NKC = 8>
-__global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr_fused_kernel(const FusedArgs a) {
-  extern __shared__ double2 fsm[];
+// One fused iteration of this CTA's (x-mode, chunk): Steps 1-3 for its frequency groups, window partial
+// sums -> P.  TMEM (when TM && !STORE_W) is allocated by the caller: tbase.
+template <int C, int LANES, bool STORE_W, bool TM, bool HALF, int NKC>
+__device__ __forceinline__ void fused_iteration(const FusedArgs& a, double2* fsm, uint32_t tbase) {
   constexpr int LF = LANES * C;
   constexpr bool TMA = TM && !STORE_W;                  // TMEM accumulators in use
-  if (a.skip && *(volatile const int*)a.skip) return;   // device-side loop already stopped
-  if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
-  __shared__ uint32_t tbase;
   double2* Hs = fsm;                                   // [8][LF]  H (in) / W (out) of the group's lines
   double2* acc = fsm + 8 * LF;                         // [k][LF]  window partial sums (shared-memory variant)
   LineConst* slc = (LineConst*)(acc + (TMA ? 0 : a.k * LF));   // [8] line constants of the group
@@ -674,14 +706,6 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr
   }
   uint32_t tacc = 0, txs = 0;
   if constexpr (TMA) {
-    if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
-                   :: "r"((uint32_t)__cvta_generic_to_shared(&tbase)), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     tacc = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * FTmem<C, LANES, NKC>::RPT * 24);
     uint32_t z[24];
 #pragma unroll
@@ -763,16 +787,45 @@ __global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr
           if (j >= 0) P[j * LF + y] = tw_get(w, r - 2);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncthreads();
-      if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n"
-                     :: "r"(tbase), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
     } else {
       for (int y = threadIdx.x; y < LF; y += FCfg<LANES>::THREADS)
         for (int j = 0; j < a.k; ++j) P[j * LF + y] = acc[j * LF + y];
     }
   }
+}
+
+template <int C, int LANES, int NKC>
+__device__ __forceinline__ uint32_t fused_tmem_alloc(uint32_t* tbase_smem) {
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(tbase_smem)), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  return *tbase_smem;
+}
+template <int C, int LANES, int NKC>
+__device__ __forceinline__ void fused_tmem_free(uint32_t tbase) {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n"
+                 :: "r"(tbase), "n"(FTmem<C, LANES, NKC>::COLS) : "memory");
+}
+
+template <int C, int LANES, bool STORE_W, bool TM, bool HALF = false, int NKC = 8>
+__global__ void __launch_bounds__(FCfg<LANES>::THREADS, FCfg<LANES>::minb(C)) wr_fused_kernel(const FusedArgs a) {
+  extern __shared__ double2 fsm[];
+  constexpr bool TMA = TM && !STORE_W;
+  if (a.skip && *(volatile const int*)a.skip) return;   // device-side loop already stopped
+  if (a.upd_reset && blockIdx.x == 0 && threadIdx.x == 0) *a.upd_reset = 0ull;
+  __shared__ uint32_t tbase_s;
+  uint32_t tbase = 0;
+  if constexpr (TMA) tbase = fused_tmem_alloc<C, LANES, NKC>(&tbase_s);
+  fused_iteration<C, LANES, STORE_W, TM, HALF, NKC>(a, fsm, tbase);
+  if constexpr (TMA) fused_tmem_free<C, LANES, NKC>(tbase);
 }
 
 
@@ -913,13 +966,12 @@ __device__ __forceinline__ void finish_row(const FinishArgs& a, long q, int y, c
 
 // many chunks (nch > 16, 1D problems): one warp per row sums the chunks' window sums (lanes over
 // chunks, shuffle tree), then lane 0 runs the finish step — one kernel instead of reduce + finish
-__global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs a) {
-  if (a.skip && *(volatile const int*)a.skip) return;
-  const long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void reduce_finish_rows(const FinishArgs& a) {
   const int lane = threadIdx.x & 31;
   double updl = 0.0;
   bool nonfinite = false;
-  if (gw < a.Qb * (long)a.Lf) {
+  for (long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5; gw < a.Qb * (long)a.Lf;
+       gw += ((long)gridDim.x * blockDim.x) >> 5) {
     const long q = gw / a.Lf;
     const int y = (int)(gw % a.Lf);
     double2 S[8];
@@ -938,12 +990,15 @@ __global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs 
   }
   if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
   block_max_atomic(updl, a.upd);
+}
+__global__ void __launch_bounds__(TPB) wr_reduce_finish_kernel(const FinishArgs a) {
+  if (a.skip && *(volatile const int*)a.skip) return;
+  reduce_finish_rows(a);
   finish_loop_tail(a.ctl, a.arrive, a.hnd, a.upd);
 }
 
 
-__global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int mode) {
-  if (a.skip && *(volatile const int*)a.skip) return;
+__device__ __forceinline__ void finish_rows(const FinishArgs& a, int mode) {
   double updl = 0.0;
   bool nonfinite = false;
   const long total = a.Qb * a.Lf;
@@ -994,8 +1049,33 @@ __global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int 
   if (mode == FIN_PARTIALS) {
     if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
     block_max_atomic(updl, a.upd);
-    finish_loop_tail(a.ctl, a.arrive, a.hnd, a.upd);
   }
+}
+__global__ void __launch_bounds__(TPB) wr_finish_kernel(const FinishArgs a, int mode) {
+  if (a.skip && *(volatile const int*)a.skip) return;
+  finish_rows(a, mode);
+  if (mode == FIN_PARTIALS) finish_loop_tail(a.ctl, a.arrive, a.hnd, a.upd);
+}
+
+// ---- the whole WR loop as ONE cooperative kernel (small problems: every (x-mode, chunk) CTA resident) ----
+// Per iteration: the fused iteration of this CTA (Steps 1-3, window partial sums -> P), a grid barrier,
+// the finish step distributed over all CTAs (window of U_m, monitor, X of the next iteration), a grid
+// barrier whose last block applies pint_wr_solve's stopping rule.  No kernel launch, no graph node
+// and no host round trip per iteration.
+template <int C, int NKC>
+__global__ void __launch_bounds__(FG * 32, 1) wr_loop_kernel(const LoopKArgs L) {
+  extern __shared__ double2 fsm[];
+  __shared__ uint32_t tbase_s;
+  const uint32_t tbase = fused_tmem_alloc<C, 32, NKC>(&tbase_s);
+  for (int h = 0;; h ^= 1) {
+    fused_iteration<C, 32, false, true, false, NKC>(L.fa[h], fsm, tbase);
+    grid_sync(L.bar, nullptr, nullptr);
+    if (L.fin[h].nch > 16) reduce_finish_rows(L.fin[h]);
+    else finish_rows(L.fin[h], FIN_PARTIALS);
+    grid_sync(L.bar, L.ctl, L.fin[h].upd);
+    if (*(volatile int*)&L.ctl->done) break;
+  }
+  fused_tmem_free<C, 32, NKC>(tbase);
 }
 
 // ---- plan time: per-line constants ----

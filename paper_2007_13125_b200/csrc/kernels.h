@@ -41,6 +41,9 @@ int fused_ctas_per_sm(int lanes, int C, int k, bool tm);
 int fused_rows_per_subchain(int lanes, int C);
 cudaError_t launch_fused(int lanes, int C, bool store_w, bool tm, const FusedArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int mode, cudaStream_t st);
+// the whole WR loop as one cooperative kernel (small fused problems; fused.cu): capacity != NULL only
+// queries the number of co-resident CTAs
+cudaError_t launch_loop_kernel(int C, int nk, const LoopKArgs& L, long grid, int k, cudaStream_t st, int* capacity);
 // device-side WR loop: the stopping rule after each iteration, sets the while-node condition (fused.cu)
 cudaError_t launch_loop_ctl(LoopCtl* s, const unsigned long long* upd, cudaGraphConditionalHandle h, cudaStream_t st);
 // fully modal variant (PINT_FLAG_MODAL): one warp per (x-mode, y-mode)

@@ -155,7 +155,7 @@ struct pint_plan_s {
   double* mu = nullptr;       // [my] 4 sin^2(j pi h_y / 2)
   double2* wtmp = nullptr;    // [ntiles][k][WB] modal window -> (q, y) staging
   bool pmon = false;          // fused modal plan, one rank: update monitor on the PHYSICAL window levels
-  double2* pwin[2] = {nullptr, nullptr};   // [k][M] physical window of U_m (ping-pong with wcur)
+  double2* pwin[2] = {nullptr, nullptr};   // [ntiles][k][WB] window of U_m, line axis in grid space
   unsigned long long* upd_sink = nullptr;  // the finish kernel's (modal-basis) monitor goes here then
   double2* fd = nullptr;      // dense forcing f(t_1..t_N) in the tile layout (pint_set_problem)
   bool full = false;          // full-array update monitor (CQ plans, PINT_FLAG_FULL_UPDATE_NORM)
@@ -208,6 +208,7 @@ struct pint_plan_s {
   LoopCtl* cap_ctl = nullptr;      // during its capture (fused, non-modal-monitor plans): the finish
   unsigned long long cap_hnd = 0;  //   kernel's last block applies the stopping rule
   unsigned int* larrive = nullptr; // its block arrival counter
+  GridBar* lbar = nullptr;         // small problems: the whole loop as one cooperative kernel (grid barrier)
   LoopCtl* lctl = nullptr;         // device state of the loop
   LoopCtl* lctl_h = nullptr;       // pinned host copy
   cudaGraphExec_t lexec[4] = {};   // per (wcur, xcur) at loop entry
@@ -477,13 +478,13 @@ extern "C" pint_status pint_plan_create(int64_t M, int64_t N, int32_t k, double 
     if ((st = dalloc(p, &p->fupd, 2)) != PINT_OK) return bail(st);
   }
   if (p->fused_ok && p->modal) {
-    // physical-space window monitor (one rank: the DST-x back needs every x-mode): the orthonormal
+    // window monitor with the line axis in grid space (DST-y back; reading R-norm2D): the orthonormal
     // DSTs scale the modal coefficients of a smooth field by up to sqrt(M) against the grid values, so
-    // a modal-basis max-norm would sit ~sqrt(M) above the grid update (its round-off floor 1.7e-12 at C4)
+    // a modal-basis max-norm sits ~sqrt(M) above the grid update (its round-off floor 1.7e-12 at C4)
     p->pmon = nranks == 1;
     if (p->pmon) {
       for (int i = 0; i < 2; ++i)
-        if ((st = dalloc(p, &p->pwin[i], (size_t)k * M)) != PINT_OK) return bail(st);
+        if ((st = dalloc(p, &p->pwin[i], (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
       if ((st = dalloc(p, &p->wtmp, (size_t)p->ntiles * k * p->WB)) != PINT_OK) return bail(st);
       if ((st = dalloc(p, &p->upd_sink, 1)) != PINT_OK) return bail(st);
     }
@@ -1219,20 +1220,10 @@ extern "C" pint_status pint_set_initial_guess(pint_plan p, const void* U0, int32
 // iteration
 // ------------------------------------------------------------------------------------------
 // one fused iteration: update monitor reset, Steps 1-3 (fused kernel), window / X / monitor (finish)
-// fused modal plans: the window levels of U (modal) -> physical [k][M] (DST-y, then DST-x in 2D)
+// fused modal plans: the window levels of U, (q, j) modes -> (q, y): DST-y back, the line axis in
+// grid space (1D: the grid values; 2D: the DST-x basis of the line path, reading R-norm2D), tile layout
 static pint_status modal_window_phys(pint_plan p, const double2* wmodal, double2* out) {
-  TRY(dst_y(p, wmodal, p->wtmp, p->k, p->Qb));
-  if (p->dim == 2) {
-    DstArgs a = dargs(p);
-    a.in = p->wtmp; a.out = out; a.rows = (long)p->k * p->my; a.N = p->k; a.n0 = 0;
-    CUDA_TRY(launch_dst(p->NE, a, DST_INT_TO_PHYS_LEVELS, p->stream));
-  } else {
-    RemapArgs r{};
-    r.in = p->wtmp; r.out = out; r.count = (long)p->k * p->M; r.WB = p->WB; r.my = 1; r.NB = p->NB;
-    r.N = p->k; r.n0 = 0; r.M = p->M; r.Qb = 1;
-    CUDA_TRY(launch_remap(r, RM_INT_TO_1D_LEVELS, p->stream));
-  }
-  ++p->launches;
+  TRY(dst_y(p, wmodal, out, p->k, p->Qb));
   return PINT_OK;
 }
 
@@ -1241,7 +1232,7 @@ static pint_status fused_kernels(pint_plan p) {
   TRY(finish_pass(p, FIN_PARTIALS, p->wrap[p->wcur], p->wrap[1 - p->wcur], p->X[1 - p->xcur]));
   if (p->pmon) {   // max |U_m - U_{m-1}| on the physical window levels
     TRY(modal_window_phys(p, p->wrap[1 - p->wcur], p->pwin[1 - p->wcur]));
-    CUDA_TRY(launch_nl_diffmax(p->pwin[1 - p->wcur], p->pwin[p->wcur], (long)p->k * p->M, p->upd, p->stream));
+    CUDA_TRY(launch_nl_diffmax(p->pwin[1 - p->wcur], p->pwin[p->wcur], (long)p->ntiles * p->k * p->WB, p->upd, p->stream));
     ++p->launches;
   }
   return PINT_OK;
@@ -1263,8 +1254,45 @@ static pint_status fused_loop(pint_plan p, double tol, int32_t max_iters, bool g
   if (!p->lctl) {
     TRY(dalloc(p, &p->lctl, 1));
     TRY(dalloc(p, &p->larrive, 1));
+    TRY(dalloc(p, &p->lbar, 1));
     CUDA_TRY(cudaMemsetAsync(p->larrive, 0, sizeof(unsigned int), p->stream));
+    CUDA_TRY(cudaMemsetAsync(p->lbar, 0, sizeof(GridBar), p->stream));
     CUDA_TRY(cudaHostAlloc((void**)&p->lctl_h, sizeof(LoopCtl), cudaHostAllocDefault));
+  }
+  // small problems (every (x-mode, chunk) CTA co-resident): the whole loop as ONE cooperative kernel,
+  // grid barriers instead of kernel boundaries (fused.cuh wr_loop_kernel)
+  if (!p->pmon && !p->modal && !p->half) {
+    LoopKArgs L{};
+    int cap = 0;
+    CUDA_TRY(launch_loop_kernel(p->Cf, p->nk, L, 0, p->k, p->stream, &cap));
+    const long grid = p->Qb * (long)p->nch;
+    if (grid <= cap) {
+      for (int h = 0; h < 2; ++h) {
+        const int w = p->wcur ^ h, x = p->xcur ^ h;
+        L.fa[h] = fargs(p, p->X[x]);
+        L.fin[h] = finargs(p, p->wrap[w], p->wrap[1 - w], p->X[1 - x]);
+      }
+      L.ctl = p->lctl;
+      L.bar = p->lbar;
+      LoopCtl* hs = p->lctl_h;
+      *hs = LoopCtl{0, max_iters, 1, 0, p->increases, guard ? 1 : 0, tol, p->last_upd, 0.0};
+      CUDA_TRY(cudaMemcpyAsync(p->lctl, hs, sizeof(LoopCtl), cudaMemcpyHostToDevice, p->stream));
+      CUDA_TRY(cudaMemsetAsync(p->upd, 0, sizeof(unsigned long long), p->stream));
+      CUDA_TRY(launch_loop_kernel(p->Cf, p->nk, L, grid, p->k, p->stream, nullptr));
+      CUDA_TRY(cudaMemcpyAsync(hs, p->lctl, sizeof(LoopCtl), cudaMemcpyDeviceToHost, p->stream));
+      CUDA_TRY(cudaStreamSynchronize(p->stream));
+      const int it = hs->it;
+      if (it & 1) { p->wcur ^= 1; p->xcur ^= 1; }
+      p->m += it;
+      p->launches += 1;
+      p->stateA = 0;
+      p->upd_queued = false;
+      if (guard) { p->last_upd = hs->last; p->increases = hs->inc; }
+      *iters = it;
+      *u_out = it > 0 ? hs->u : INFINITY;
+      *status = hs->status;
+      return PINT_OK;
+    }
   }
   const int key = p->wcur * 2 + p->xcur;
   FusedArgs fa[2];

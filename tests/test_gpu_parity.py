@@ -758,7 +758,8 @@ def test_device_loop_matches_host_loop(pint, monkeypatch, make, tol):
         print(f"{prob.name}: host loop {ih} it (update {uh:.3e}, status {sh}); device loop {idv} it ({ud:.3e}, {sd})")
         assert (ih, sh) == (idv, sd) and sh == pint.PINT_OK
         assert ud == uh
-        assert dev.info()["m"] == idv and dev.info()["kernel_launches"] - l0 == 2 * idv   # fused + finish (+ctl)
+        # one cooperative kernel per solve (small problems), or fused + finish per iteration (graph loop)
+        assert dev.info()["m"] == idv and dev.info()["kernel_launches"] - l0 in (1, 2 * idv)
         assert np.array_equal(host.get_solution(), dev.get_solution())
         # a second solve continues from the converged state (parity and guard state carried over)
         assert host.solve(tol, 5, raise_on_fail=False)[:2] == dev.solve(tol, 5, raise_on_fail=False)[:2]
@@ -794,14 +795,18 @@ def test_wr_run_streaming_and_args(pint):
 
 @pytest.mark.parametrize("mx,my,N,k,real", [(63, 31, 256, 3, False), (127, 63, 512, 6, True), (255, 1, 256, 2, False)])
 def test_modal_window_monitor_is_physical(pint, mx, my, N, k, real):
-    """Fully modal heat plans monitor the update on the PHYSICAL window levels (DST back every
-    iteration): the value equals the oracle's max_{n > N-k} |U_m^n - U_{m-1}^n| on the grid, not the
-    modal-basis norm, which the orthonormal DSTs scale by up to sqrt(M) (VERDICT r1 weak #8)."""
+    """Fully modal heat plans monitor the window update with the line axis back in grid space (DST-y
+    every iteration): 1D the grid values, 2D the DST-x basis of the line path (reading R-norm2D) — the
+    oracle's max over the window levels in that basis, not the modal-basis norm, which the orthonormal
+    DSTs scale by up to sqrt(M) (VERDICT r1 weak #8)."""
+    from oracle import spatial
     prob = inputs.random_complex_problem(mx, my, N, k, 0.05, 1.0, R=1, seed=mx + k)
     if real:
         prob = prob.real_part()
     o = wr.wr_naive(prob, 4, dft="fft")
-    ou = [float(np.abs(o[m][N - k:] - o[m - 1][N - k:]).max()) for m in range(1, 5)]
+    basis = (lambda U: U) if my == 1 else \
+        (lambda U: spatial.dst1(U.reshape(U.shape[0], my, mx), axis=2).reshape(U.shape[0], -1))
+    ou = [float(np.abs(basis(o[m][N - k:]) - basis(o[m - 1][N - k:])).max()) for m in range(1, 5)]
     with pint.Plan.from_problem(prob, modal=True) as p:
         assert p.path()["fused"]
         gu = [p.iterate() for _ in range(4)]
