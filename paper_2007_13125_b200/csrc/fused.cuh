@@ -98,11 +98,16 @@ template <bool AF> __device__ __forceinline__ double2 mstep(double2 c, double2 z
   if constexpr (AF) return cfma(c, z, d);
   else return cadd(d, amul(c, z));
 }
+// the backward sweep on v = a w: v_y = a (f_y + v_{y+1}) — the final x = a (w - w_0 phi) then needs no
+// multiplication by a per row (the chunked scan combines exactly as for w: a chunk's value is its
+// zero-carry total plus a^len times the carry)
+template <bool AF> __device__ __forceinline__ double2 vstep(double2 c, double2 z, double2 f);
 template <bool AF> __device__ __forceinline__ double2 mmul(double2 c, double2 z) {
   if constexpr (AF) return cmul(c, z);
   else return amul(c, z);
 }
 template <bool AF> __device__ __forceinline__ double2 mconv(double2 uform) { return AF ? one_minus(uform) : uform; }
+template <bool AF> __device__ __forceinline__ double2 vstep(double2 c, double2 z, double2 f) { return mmul<AF>(c, cadd(f, z)); }
 constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 
 // LANES lanes per line: 32 (one warp; default) or 64 (two warps, pair-scoped named barriers);
@@ -204,13 +209,13 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
       if (r >= nv) d[r] = make_double2(0.0, 0.0);
   }
 
-  // ---- backward recurrence w_y = f_y + a w_{y+1} ----
+  // ---- backward recurrence w_y = f_y + a w_{y+1}, carried as v = a w: v_y = a (f_y + v_{y+1}) ----
 #pragma unroll
   for (int s2 = 0; s2 < NS; ++s2) fs[s2] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int r = CS - 1; r >= 0; --r)
 #pragma unroll
-    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = mstep<AF>(u, fs[s2], d[s2 * CS + r]);
+    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = vstep<AF>(u, fs[s2], d[s2 * CS + r]);
   double2 w = fs[NS - 1];
 #pragma unroll
   for (int s2 = NS - 2; s2 >= 0; --s2) w = mstep<AF>(uh, w, fs[s2]);
@@ -240,11 +245,11 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   for (int r = CS - 1; r >= 0; --r)
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) {
-      st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
+      st[s2] = vstep<AF>(u, st[s2], d[s2 * CS + r]);
       d[s2 * CS + r] = st[s2];
     }
 
-  // ---- rank-1 Dirichlet correction x = a (w - w_0 phi), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2}) ----
+  // ---- rank-1 Dirichlet correction x = v - v_0 phi (v = a w), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2}) ----
   double2 w0;
   if constexpr (PAIR) {
     if (half == 0 && lane == 0) xch[2] = d[0];
@@ -299,20 +304,20 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 #pragma unroll
     for (int r = 0; r < C; ++r) {
       const int y = y0 + r;
-      if (y < a.Lpad) Wq[((long)(y / a.WB) * a.N) * a.WB + (y % a.WB)] = (r < nv) ? mmul<AF>(u, d[r]) : make_double2(0.0, 0.0);
+      if (y < a.Lpad) Wq[((long)(y / a.WB) * a.N) * a.WB + (y % a.WB)] = (r < nv) ? d[r] : make_double2(0.0, 0.0);
     }
   } else {
 #pragma unroll
-    for (int r = 0; r < C; ++r) rows[r] = mmul<AF>(u, d[r]);   // pad rows: never read (finish uses y < L)
+    for (int r = 0; r < C; ++r) rows[r] = d[r];   // pad rows: never read (finish uses y < L)
     if (fastP) {
-      // x_y -= a K a^{y+2} = K a^{y+3} for y < rP (value-form powers: |a| < 0.85 here)
+      // x_y -= K a^{y+2} for y < rP, K = v_0 / (1 - a^{2L+2}) (value-form powers: |a| < 0.85 here)
       __syncwarp();
       const int rP = min((int)ceil(rPd), L);
       double2 al = make_double2(1.0, 0.0);                                 // a^{lane}
 #pragma unroll
       for (int i = 0; i < 5; ++i)
         if ((lane >> i) & 1) al = cmul(al, lc.ap[i]);
-      double2 Ka = cmul(K, cmul(lc.ap[0], lc.ap[1]));                      // K a^3
+      double2 Ka = cmul(K, lc.ap[1]);                                      // K a^2
       Ka = cmul(Ka, al);
       const double2 a32 = cmul(lc.ap[4], lc.ap[4]);
       for (int yy = lane; yy < rP; yy += 32) {
