@@ -54,7 +54,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False,
     """defines/lib: experimental variants (e.g. ["-DPINT_TPASS_MINB=3"], "libpint_minb3.so")."""
     defines = defines or []
     LIB = os.path.join(HERE, lib) if lib else globals()["LIB"]
-    build_dir = BUILD + ("_" + os.path.splitext(lib)[0] if lib else "")
+    # variant objects outside the repo (the repo snapshot shipped to the GPU box stays small)
+    build_dir = os.path.join("/tmp", "pint_build_" + os.path.splitext(lib)[0]) if lib else BUILD
     extra = os.environ.get("PINT_NVCC_EXTRA", "").split()
     if extra and not lib:
         raise RuntimeError("PINT_NVCC_EXTRA is for variant builds only: pass lib=<variant name>")

@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   if (tid == 0 && tile < ntiles) tile_bulk_load(sbuf, a.in + tile * (long)TILE, TILE * 16, sbar);
   double upd2 = 0.0;                   // max |U_m - U_{m-1}|^2 (one square root at the end)
   bool nonfinite = false;
+  PINT_ASSERT(blockDim.x == G::THREADS && i < N1 && c < WB);
+  PINT_ASSERT(N1 * G::ROW <= G::BUF && TILE <= G::BUF);
   for (; tile < ntiles; tile += gridDim.x) {
     const long base = tile * (long)TILE, nt = tile + gridDim.x;
     if (tid < 4) {
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < N1; ++t) v[t] = buf[i * G::ROW + t * G::WB + c];
+      PINT_ASSERT((N1 - 1) * G::ROW + i * G::WB + c < G::BUF && i * G::ROW + (N1 - 1) * G::WB + c < G::BUF);
       if (x == 0) {                          // U_{m-1} of this tile lands during the pass-B DFT
         __syncthreads();
         if (tid == 0) {
@@ -317,7 +320,11 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
           if (!(d2 <= 1.7976931348623157e308)) nonfinite = true;
           upd2 = fmax(upd2, d2);
           a.ufull[base + (long)n * WB + c] = U;
-          if (t == N1 - 1 && i >= N1 - a.k) a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
+          PINT_ASSERT(n * WB + c < TILE);
+          if (t == N1 - 1 && i >= N1 - a.k) {
+            PINT_ASSERT(n - (N - a.k) >= 0 && n - (N - a.k) < a.k);
+            a.wrap_new[(tile * a.k + (n - (N - a.k))) * WB + c] = U;
+          }
         }
       } else if (x == 1) {
 #pragma unroll

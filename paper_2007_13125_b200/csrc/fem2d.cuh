@@ -55,6 +55,7 @@ __global__ void fem2d_kernel(const Fem2dArgs a) {
     long q, n;
     int j;
     fem2d_decode(a, e, q, j, n);
+    PINT_ASSERT(n < a.levels && j < a.NB * a.WB);
     if (j >= a.L) continue;                               // pad modes stay zero
     const double cq = __ldg(&a.cx[q]), cj = __ldg(&a.cy[j]);
     const double m = (2.0 + (1.0 + cq) * (1.0 + cj)) / 6.0;

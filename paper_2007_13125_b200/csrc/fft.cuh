@@ -16,6 +16,15 @@
 
 namespace pint {
 
+// Checked builds (-DPINT_CHECK, `build.py -D PINT_CHECK --lib libpint_check.so`): device-side bounds and
+// protocol assertions on the shared-memory, tensor-memory, bulk-copy and grid-barrier indexing (a
+// failed check traps: the launch fails loudly).  compute-sanitizer is closed on this GPU pool.
+#ifdef PINT_CHECK
+#define PINT_ASSERT(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define PINT_ASSERT(c) do { } while (0)
+#endif
+
 constexpr int TPB = 256;
 constexpr int TILE = 4096;
 

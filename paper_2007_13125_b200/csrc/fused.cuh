@@ -635,7 +635,9 @@ __device__ __forceinline__ void grid_sync(GridBar* b, LoopCtl* ctl, unsigned lon
     volatile unsigned int* vgen = &b->gen;
     const unsigned int g = *vgen;
     __threadfence();                                   // this block's writes before its arrival
-    if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+    const unsigned int arrived = atomicAdd(&b->count, 1u);
+    PINT_ASSERT(arrived < gridDim.x);                  // a barrier generation never overflows
+    if (arrived == gridDim.x - 1) {
       if (ctl) {
         const double u = __longlong_as_double((long long)*(volatile unsigned long long*)upd);
         *upd = 0ull;
@@ -695,6 +697,8 @@ __device__ __forceinline__ void fused_iteration(const FusedArgs& a, double2* fsm
   double2* Xs = xch + (LANES == 64 ? 32 : 0);          // [nk][LF] X of this x-mode (a.xs)
   const long q = blockIdx.x / a.nch;
   const int ch = blockIdx.x % a.nch;
+  PINT_ASSERT(q < a.Qb && a.L <= LF && a.k <= 8 && a.nk <= NKC && blockDim.x == FCfg<LANES>::THREADS);
+  static_assert(!TMA || FTmem<C, LANES, NKC>::NEED <= FTmem<C, LANES, NKC>::COLS, "TMEM columns");
   const int NG = (int)(a.N / FG);                      // line stride of a group
   const int NGL = HALF ? NG / 2 + 1 : NG;               // groups solved (half spectrum: i <= N/16)
   const int g0 = ch * a.gpc, g1 = min(g0 + a.gpc, NGL);
