@@ -365,4 +365,36 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(G::TCOLS) : "memory");
 }
 
+// CQ bootstrap (pint.cu bootstrap): U_0^n = v (or 0) at every level, H_1 = sum_s chat_s[p] src_s +
+// cwhat[p] v elementwise over the tile layout [tile][N][WB] (p = level slot of the H layout)
+struct CqBootArgs {
+  double2* H;                 // H_1 (tile layout)
+  double2* ufull;             // U_0 for the full monitor (may be NULL)
+  double2* wrap;              // [ntiles][k][WB] window of U_0
+  const double2* src;         // [S][ntiles][WB]
+  const double2* cqhat;       // [S][N]
+  const double2* cwhat;       // [N]
+  int S, zero, k;
+  long N, ntiles;
+  int WB;
+};
+#ifdef PINT_DEFINE_PLAIN_KERNELS
+__global__ void cq_boot_kernel(const CqBootArgs b) {
+  const long total = b.ntiles * (long)TILE;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long tile = e / TILE;
+    const int r = (int)(e % TILE), n = r / b.WB, c = r % b.WB;
+    const long sstr = b.ntiles * b.WB, so = tile * b.WB + c;
+    const double2 v = b.zero ? make_double2(0.0, 0.0) : __ldg(&b.src[so]);
+    double2 h = cmul(__ldg(&b.cwhat[n]), v);
+    for (int s = 0; s < b.S; ++s) h = cfma(__ldg(&b.cqhat[(long)s * b.N + n]), __ldg(&b.src[s * sstr + so]), h);
+    b.H[e] = h;
+    if (b.ufull) b.ufull[e] = v;
+    if (n >= b.N - b.k) b.wrap[(tile * b.k + (n - (b.N - b.k))) * b.WB + c] = v;
+  }
+}
+#else
+__global__ void cq_boot_kernel(const CqBootArgs b);
+#endif
+
 }  // namespace pint

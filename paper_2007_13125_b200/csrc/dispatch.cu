@@ -176,6 +176,14 @@ cudaError_t launch_fem2d_mixed(const double2* Y, double2* Z, long levels, int mx
   return cudaGetLastError();
 }
 
+cudaError_t launch_cq_boot(const CqBootArgs& b, cudaStream_t st) {
+  const long total = b.ntiles * (long)TILE;
+  const long blocks = std::min<long>((total + 255) / 256, 148L * 16);
+  if (blocks <= 0) return cudaSuccess;
+  cq_boot_kernel<<<(unsigned)blocks, 256, 0, st>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st) {
   if (a.count <= 0) return cudaSuccess;
   const long blocks = (a.count + 255) / 256;

@@ -29,6 +29,8 @@ cudaError_t launch_tpass_cq_fused(int N, const CQArgs& a, cudaStream_t st);
 cudaError_t launch_fem2d(const Fem2dArgs& a, bool init, cudaStream_t st);
 cudaError_t launch_fem2d_mixed(const double2* Y, double2* Z, long levels, int mx, int my, int NB, int WB, long total,
                                cudaStream_t st);
+// CQ bootstrap: U_0 and H_1 elementwise from the separable sources (cqpass.cuh, dispatch.cu)
+cudaError_t launch_cq_boot(const CqBootArgs& b, cudaStream_t st);
 // layout remaps and the FD stencil (dispatch.cu)
 cudaError_t launch_remap(const RemapArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_stencil(const double2* v, double2* Av, int mx, int my, double ihx2, double ihy2, cudaStream_t st);

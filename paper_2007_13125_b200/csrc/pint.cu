@@ -124,6 +124,7 @@ struct pint_plan_s {
   int* srclist = nullptr;     // [S]: sparse sources, then dense sources
   double2* chat = nullptr;    // [S][N] DFTs of dense coefficient sequences
   double2* cqhat = nullptr;   // [S][N] CQ split T-pass: DFTs of Gamma h^2/N c_s(n) for every source
+  double2* cqwhat = nullptr;  // [N] CQ bootstrap: DFT of Gamma h^2/N times the wrap coefficient of U_0 = v
   double2 *tw = nullptr, *twE = nullptr;
   double *gsf = nullptr, *igs = nullptr, *gsN = nullptr, *wk = nullptr;
   double* cqw = nullptr;      // [N] tau^-a omega_j (CQ plans)
@@ -937,6 +938,14 @@ static pint_status bootstrap(pint_plan p) {
   if (p->fused) {   // window of U_0 and X_1 only
     TRY(finish_pass(p, zero ? FIN_ZERO : FIN_FROM_V, nullptr, p->wrap[p->wcur], p->X[p->xcur]));
     if (p->pmon) TRY(modal_window_phys(p, p->wrap[p->wcur], p->pwin[p->wcur]));
+  } else if (p->alpha != 1.0 && p->cqwhat && !p->has_fd && !p->nl) {
+    // CQ: H_1 and the full monitor's U_0 elementwise from the separable sources (no transforms)
+    CqBootArgs b{};
+    b.H = p->A; b.ufull = p->full ? p->ufull : nullptr; b.wrap = p->wrap[p->wcur]; b.src = p->src;
+    b.cqhat = p->cqhat; b.cwhat = p->cqwhat; b.S = p->S; b.zero = zero ? 1 : 0; b.k = p->k;
+    b.N = p->N; b.ntiles = p->ntiles; b.WB = p->WB;
+    CUDA_TRY(launch_cq_boot(b, p->stream));
+    ++p->launches;
   } else {
     TRY(tpass(p, zero ? IN_TIME_ZERO : IN_TIME_V, OUT_H, nullptr, p->A, nullptr, p->wrap[p->wcur], false));
   }
@@ -1092,6 +1101,26 @@ static pint_status set_problem_impl(pint_plan p, const void* v, int32_t R, const
       for (int64_t pp = 0; pp < N; ++pp) ch[(size_t)s * N + pp] = d2(x[pp]);
     }
     TRY(h2d_async(p, p->cqhat, ch));
+    // the bootstrap iterate U_0^n = v is constant in time, so its kappa-wrap (kappa/tau^a) sum_{j=n}^{N-1}
+    // omega_j U_0^{N+n-j} = c_w(n) v is separable too: H_1 = H_static + cwhat[p] v, cwhat = DFT of
+    // kappa^{n/N} h^2/N c_w(n) (eq:BDF-subdiff-F): no transform at bootstrap
+    {
+      std::vector<ld> wq = cq_weights(k, (ld)p->alpha, N + 1);
+      const ld ta = powl((ld)p->tau, -(ld)p->alpha);
+      ld tail = 0.0L;                                   // sum_{j=n}^{N-1} omega_j, n = N..1
+      std::vector<ld> cw(N);
+      for (int64_t n = N; n >= 1; --n) {
+        cw[n - 1] = (ld)p->kappa * ta * tail;           // n = N: empty sum
+        tail += wq[n - 1];
+      }
+      // cw[n-1] = kappa tau^-a sum_{j=n}^{N-1} omega_j  (tail before adding omega_{n-1})
+      for (int64_t n = 0; n < N; ++n) x[n] = cw[n] * powl((ld)p->kappa, (ld)n / Nl) * hl * hl / Nl;
+      fft_ld(x, -1);
+      std::vector<double2> cwv(N);
+      for (int64_t pp = 0; pp < N; ++pp) cwv[pp] = d2(x[pp]);
+      if (!p->cqwhat) TRY(dalloc(p, &p->cqwhat, N));
+      TRY(h2d_async(p, p->cqwhat, cwv));
+    }
   }
   TRY(h2d_async(p, p->coef, coef));
   TRY(h2d_async(p, p->nhi, nhi));

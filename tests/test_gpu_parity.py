@@ -154,6 +154,7 @@ def test_c5_full_size_modal_sampled(pint):
 def test_u0_zero_and_initial_guess(pint):
     prob = inputs.example1_fd(3, M=99, N=64)            # U_0 = 0 (table setting)
     check(pint, prob, 3)
+    check(pint, inputs.example2_fd(2, M=255, N=256), 3)  # CQ, U_0 = 0 (separable CQ bootstrap)
     prob = inputs.config_c1()
     Us = sequential.sequential(prob)
     with pint.Plan.from_problem(prob) as p:
