@@ -114,9 +114,9 @@ static cudaError_t spass_pair_go(const SPassArgs& a, long Qb, cudaStream_t st) {
   int lwb = 0;
   while ((1 << lwb) < a.WB) ++lwb;
   b.lwb = lwb;
-  b.nwork = Qb * a.N;                        // lines, 2 per CTA
-  const long grid = (b.nwork + 1) / 2;
-  spass_pair_kernel<C><<<(unsigned)grid, 128, 0, st>>>(b);
+  b.nwork = Qb * a.N;                        // lines, PINT_PAIR_LPC per CTA
+  const long grid = (b.nwork + PINT_PAIR_LPC - 1) / PINT_PAIR_LPC;
+  spass_pair_kernel<C><<<(unsigned)grid, 64 * PINT_PAIR_LPC, 0, st>>>(b);
   return cudaGetLastError();
 }
 

@@ -392,6 +392,9 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 #ifndef PINT_PAIR_MINB
 #define PINT_PAIR_MINB 4
 #endif
+#ifndef PINT_PAIR_LPC
+#define PINT_PAIR_LPC 2   // lines (consecutive frequencies of one x-mode) per CTA, two warps each
+#endif
 
 // The pair solve: lane gl = 32 half + lane of the pair owns rows [gl C, gl C + C) in d (rows >= L
 // zero on entry); on exit d holds the solution rows (zero beyond L).  xch: the pair's exchange slots.
@@ -531,11 +534,11 @@ static __global__ void spass_const_kernel(SPassConst* out, const double2* sig_p,
 
 
 template <int C>
-__global__ void __launch_bounds__(128, PINT_PAIR_MINB) spass_pair_kernel(const SPassArgs a) {
-  __shared__ double2 xch[2][4];                      // per pair: fwd total, bwd total, w0, spare
+__global__ void __launch_bounds__(64 * PINT_PAIR_LPC, PINT_PAIR_MINB * 2 / PINT_PAIR_LPC) spass_pair_kernel(const SPassArgs a) {
+  __shared__ double2 xch[PINT_PAIR_LPC][4];          // per pair: fwd total, bwd total, w0, spare
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const int pair = warp >> 1, half = warp & 1;
-  const long line = (long)blockIdx.x * 2 + pair;
+  const long line = (long)blockIdx.x * PINT_PAIR_LPC + pair;
   const long N = a.N, NB = a.NB;
   const bool live = line < a.nwork;
   const long q = live ? line / N : 0, p = live ? line - q * N : 0;
