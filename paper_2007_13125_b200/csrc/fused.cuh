@@ -618,6 +618,9 @@ __device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphCon
   if (loop_ctl_eval(s, u)) cudaGraphSetConditional(h, 0);
 }
 
+#ifndef PINT_BAR_SLEEP
+#define PINT_BAR_SLEEP 0    // ns between polls of the grid barrier's generation word (0: spin; 40 measured no better)
+#endif
 // the whole WR loop as one cooperative kernel (wr_loop_kernel below)
 struct GridBar { unsigned int count, gen; };
 struct LoopKArgs {
@@ -647,7 +650,11 @@ __device__ __forceinline__ void grid_sync(GridBar* b, LoopCtl* ctl, unsigned lon
       __threadfence();
       atomicExch(&b->gen, g + 1u);
     } else {
-      while (*vgen == g) __nanosleep(40);
+      while (*vgen == g) {
+#if PINT_BAR_SLEEP > 0
+        __nanosleep(PINT_BAR_SLEEP);
+#endif
+      }
     }
     __threadfence();
   }
