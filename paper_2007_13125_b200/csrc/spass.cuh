@@ -392,17 +392,33 @@ __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64
 #ifndef PINT_PAIR_MINB
 #define PINT_PAIR_MINB 4
 #endif
+// recurrence step d + m z with the multiplier in u-form (c = 1 - m; shift-accurate: z - c z) or, AF, in
+// value form (c = m; one complex FMA) — the value form for lines with |u| >= 1e-3, where rounding
+// a = 1 - u perturbs u (hence the shift) by at most 2e-13 relatively (as the fused solve, fused.cuh)
+template <bool AF> __device__ __forceinline__ double2 pstep(double2 c, double2 z, double2 d) {
+  if constexpr (AF) return cfma(c, z, d);
+  else return cadd(d, amul(c, z));
+}
+template <bool AF> __device__ __forceinline__ double2 pconv(double2 uform) {
+  return AF ? make_double2(1.0 - uform.x, -uform.y) : uform;
+}
+#ifndef PINT_PAIR_AF
+#define PINT_PAIR_AF 1
+#endif
+constexpr double PAIR_AF_U2 = 1e-6;
+
 #ifndef PINT_PAIR_LPC
 #define PINT_PAIR_LPC 2   // lines (consecutive frequencies of one x-mode) per CTA, two warps each
 #endif
 
 // The pair solve: lane gl = 32 half + lane of the pair owns rows [gl C, gl C + C) in d (rows >= L
 // zero on entry); on exit d holds the solution rows (zero beyond L).  xch: the pair's exchange slots.
-template <int C>
+template <int C, bool AF = false>
 __device__ __forceinline__ void pair_solve(double2 (&d)[C], const SPassConst& lc, int L, int lane, int half, int gl,
                                            int nv, double2* xch, int pair) {
   // ---- line constants (plan-time table) ----
   const double2 u = lc.u, rr = lc.rr;
+  const double2 um = pconv<AF>(u);                   // the step multiplier (u- or value form)
   // the lane holding row L-1 zeroes its rows >= L (2^n - 1 lines: one pad row, a single register)
   const bool pad1 = L >= 64 * C - 1;
   auto zero_tail = [&](double2 (&v)[C]) {
@@ -425,22 +441,26 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], const SPassConst& lc
     if ((lane + 1) & (1 << i)) ufw = uprod(ufw, uc[i]);
     if ((32 - lane) & (1 << i)) ubw = uprod(ubw, uc[i]);
   }
+  double2 ucm[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) ucm[i] = pconv<AF>(uc[i]);
+  const double2 ufm = pconv<AF>(ufw), ubm = pconv<AF>(ubw);
 
   // ---- forward recurrence ----
   double2 f = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int r = 0; r < C; ++r) f = cadd(d[r], amul(u, f));
+  for (int r = 0; r < C; ++r) f = pstep<AF>(um, f, d[r]);
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_up_sync(0xffffffffu, f.x, o);
     x.y = __shfl_up_sync(0xffffffffu, f.y, o);
-    if (lane >= o) f = cadd(f, amul(uc[i], x));
+    if (lane >= o) f = pstep<AF>(ucm[i], x, f);
   }
   if (half == 0 && lane == 31) xch[0] = f;     // warp-0 total (inclusive at its last row)
   pair_bar(1 + pair);
-  if (half == 1) f = cadd(f, amul(ufw, xch[0]));
+  if (half == 1) f = pstep<AF>(ufm, xch[0], f);
   double2 carry;
   carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
   carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
@@ -448,32 +468,32 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], const SPassConst& lc
   f = carry;
 #pragma unroll
   for (int r = 0; r < C; ++r) {
-    f = cadd(d[r], amul(u, f));
+    f = pstep<AF>(um, f, d[r]);
     d[r] = f;
   }
   zero_tail(d);
   // ---- backward recurrence ----
   double2 w = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int r = C - 1; r >= 0; --r) w = cadd(d[r], amul(u, w));
+  for (int r = C - 1; r >= 0; --r) w = pstep<AF>(um, w, d[r]);
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_down_sync(0xffffffffu, w.x, o);
     x.y = __shfl_down_sync(0xffffffffu, w.y, o);
-    if (lane + o < 32) w = cadd(w, amul(uc[i], x));
+    if (lane + o < 32) w = pstep<AF>(ucm[i], x, w);
   }
   if (half == 1 && lane == 0) xch[1] = w;      // warp-1 total (suffix from its first row)
   pair_bar(1 + pair);
-  if (half == 0) w = cadd(w, amul(ubw, xch[1]));
+  if (half == 0) w = pstep<AF>(ubm, xch[1], w);
   carry.x = __shfl_down_sync(0xffffffffu, w.x, 1);
   carry.y = __shfl_down_sync(0xffffffffu, w.y, 1);
   if (lane == 31) carry = half ? make_double2(0.0, 0.0) : xch[1];
   w = carry;
 #pragma unroll
   for (int r = C - 1; r >= 0; --r) {
-    w = cadd(d[r], amul(u, w));
+    w = pstep<AF>(um, w, d[r]);
     d[r] = w;
   }
   // ---- rank-1 Dirichlet correction ----
@@ -500,7 +520,7 @@ __device__ __forceinline__ void pair_solve(double2 (&d)[C], const SPassConst& lc
     }
   }
 #pragma unroll
-  for (int r = 0; r < C; ++r) d[r] = amul(u, d[r]);
+  for (int r = 0; r < C; ++r) d[r] = AF ? cmul(um, d[r]) : amul(u, d[r]);
   zero_tail(d);
 }
 
@@ -556,7 +576,9 @@ __global__ void __launch_bounds__(64 * PINT_PAIR_LPC, PINT_PAIR_MINB * 2 / PINT_
   const int nv = min(max(L - gl * C, 0), C);
   // input rows y >= L are exact zeros (pad rows of H), so no masking after the loads
   SPassConst lc = live ? a.lc[q * N + p] : a.lc[0];
-  pair_solve<C>(d, lc, L, lane, half, gl, nv, xch[pair], pair);
+  // (C = 16, N = 2048: the second instance of the solve no longer fits the 128-register budget)
+  if (PINT_PAIR_AF && C <= 8 && cabs2(lc.u) >= PAIR_AF_U2) pair_solve<C, (C <= 8)>(d, lc, L, lane, half, gl, nv, xch[pair], pair);
+  else pair_solve<C, false>(d, lc, L, lane, half, gl, nv, xch[pair], pair);
   double2* out = a.out + (q * NB * N + p) * WB;
 #pragma unroll
   for (int r = 0; r < C; r += 2) {
