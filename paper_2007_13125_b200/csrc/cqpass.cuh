@@ -12,12 +12,12 @@
 // transform as three radix-16 passes with two shared-memory exchanges):
 //  * N = N1 * N1 (N1 = 32: N = 1024, the C5 configuration; N1 = 16: N = 256) as a 4-step transform:
 //    thread (i, c) owns the N1 values i + N1 t of column c; pass A = DFT_N1 over t in registers, twiddle
-//    w^{i k2}, ONE shared-memory exchange (row-padded: conflict-free 16-byte accesses), pass B = DFT_N1.
+//    w^{i k2}, ONE shared-memory exchange (rows XOR-swizzled: conflict-free 16-byte accesses), pass B = DFT_N1.
 //    Input and output mappings are the same (thread i holds index i + N1 t), so the four transforms
 //    chain without further exchanges: 4 exchanges per tile instead of 8 (+2 for the split halves).
-//  * The diagonal Theta/N and C Theta^{-1} factors are folded into the forward transforms: the
-//    per-thread part theta^i into the pass-A twiddle table, the per-register part e^{+-i pi t/N1} into
-//    compile-time rotations (no table loads for them).
+//  * The diagonal Theta factors of the forward transforms: theta^n = theta^i e^{i pi t / N1}, the
+//    per-thread theta^i in a register, the per-register part a compile-time rotation (no table); the
+//    1/N and c_x are moved onto D'.  d_p and chat_0 (the stash factors) live in shared memory.
 //  * The tile arrives by a 1D TMA bulk copy (cp.async.bulk, completion on an mbarrier) into the same
 //    shared buffer the exchanges use; the next tile's copy is issued as soon as the last exchange of
 //    the current tile has been read, and lands while the current tile finishes its last DFT, the
@@ -102,10 +102,15 @@ template <int N1> struct CQCfg {
   static constexpr int N = N1 * N1;
   static constexpr int WB = TILE / N;                       // columns per tile
   static constexpr int THREADS = N1 * WB;                   // thread (i, c) = (tid / WB, tid % WB)
-  static constexpr int ROW = N1 * WB + (WB == 4 ? 4 : 0);   // exchange row stride (complex), padded
-  static constexpr int BUF = (N1 * ROW > TILE ? N1 * ROW : TILE);
-  static constexpr int TWROW = N1 + 1;                      // twiddle rows in shared memory, padded
-  static constexpr int SMEM = (BUF + N1 * TWROW + N) * 16;   // exchange / tile buffer + twiddles + Theta
+  static constexpr int ROW = N1 * WB;                       // exchange row stride (complex; see xidx)
+  static constexpr int BUF = TILE;                          // tile landing zone = exchange buffer
+  static constexpr int TWC = N1 - 1;                        // twiddle row: k2 = 1..N1-1 (odd stride:
+                                                            // conflict-free rows without padding)
+  // tile / exchange buffer + pass-A twiddles + d_p + chat_0: 111.5 KB at N1 = 32, two CTAs per SM
+  static constexpr int SMEM = (BUF + N1 * TWC + 2 * N) * 16;
+  // exchange slot of (row r, column j): WB = 4 rows XOR-swizzled by the row parity (the 8 threads of a
+  // 16-byte wavefront read rows i, i+1 at the same column: the swizzle puts them on disjoint banks)
+  static __device__ __forceinline__ int xidx(int r, int j) { return r * ROW + (WB == 4 ? (j ^ ((r & 1) << 2)) : j); }
   // two CTAs per SM: 255 registers (no spills of the 32 values per thread), 2 x 256 TMEM columns
   static constexpr int MINB = 2;
   static constexpr int TCOLS = 256;                         // TMEM columns per CTA: the stash of D W + H_static
@@ -120,7 +125,8 @@ struct CQArgs {
   unsigned long long* upd;    // max |U_m - U_{m-1}| as ordered bits
   const double2* tw;          // [N] pass-A twiddles w^{+i k2} at [i N1 + k2] (every transform runs as an
                               //     inverse 4-step transform; a forward one as conj . inverse . conj)
-  const double2* th;          // [N] theta^n = e^{i pi n / N} (the skew-circulant rotation Theta)
+  const double2* th;          // [N] theta^n = e^{i pi n / N} (the skew-circulant rotation Theta; the kernel
+                              //     reads theta^i, i < N1, and rotates by theta^{N1 t} = e^{i pi t / N1})
   const double2* dpr;         // [N] (c_x / N) d'_p: d'_p the eigenvalues of C(-kappa), c_x = -h^2/(2 tau^a N)
                               //     (the 1/N of V^{-1} and c_x of the Theta^{-1} factor, moved onto D')
   const double2* dh;          // [N] (h^2/(2 tau^a)) d_p
@@ -201,13 +207,17 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // the pass-A twiddles and Theta, staged once per CTA (persistent kernel): conflict-free shared loads
-  double2* stw = buf + G::BUF;                 // [N1][N1 + 1]
-  double2* sth = stw + N1 * G::TWROW;          // [N]
+  // the pass-A twiddles, d_p and chat_0, staged once per CTA (persistent kernel): conflict-free shared
+  // loads (per-tile L2 loads of d_p and chat_0 stalled the stash on their latency, ncu v9)
+  double2* stw = buf + G::BUF;                 // [N1][N1 - 1]
+  double2* sdh = stw + N1 * G::TWC;            // [N]
+  double2* sch = sdh + N;                      // [N] chat_0 (S > 0)
   for (int e = tid; e < N; e += G::THREADS) {
-    stw[(e / N1) * G::TWROW + e % N1] = __ldg(&a.tw[e]);
-    sth[e] = __ldg(&a.th[e]);
+    if (e % N1) stw[(e / N1) * G::TWC + e % N1 - 1] = __ldg(&a.tw[e]);
+    sdh[e] = __ldg(&a.dh[e]);
+    if (a.S > 0) sch[e] = __ldg(&a.chat[e]);
   }
+  const double2 thi = __ldg(&a.th[i]);         // theta^i
   __syncthreads();
   // this thread's stash columns: lane 32 (warp % 4) + lane, N1 * 4 columns (N1 complex doubles)
   const uint32_t tst = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * N1 * 4);
@@ -227,7 +237,7 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   double upd2 = 0.0;                   // max |U_m - U_{m-1}|^2 (one square root at the end)
   bool nonfinite = false;
   PINT_ASSERT(blockDim.x == G::THREADS && i < N1 && c < WB);
-  PINT_ASSERT(N1 * G::ROW <= G::BUF && TILE <= G::BUF);
+  static_assert(N1 * CQCfg<N1>::ROW <= CQCfg<N1>::BUF && TILE <= CQCfg<N1>::BUF, "exchange buffer");
   for (; tile < ntiles; tile += gridDim.x) {
     const long base = tile * (long)TILE, nt = tile + gridDim.x;
     if (tid < 4) {
@@ -252,8 +262,8 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int p = i + N1 * (4 * q + j);
-          double2 h = cmul(v[4 * q + j], __ldg(&a.dh[p]));
-          if (a.S > 0) h = cfma(__ldg(&a.chat[p]), g0, h);
+          double2 h = cmul(v[4 * q + j], sdh[p]);
+          if (a.S > 0) h = cfma(sch[p], g0, h);
           if (a.S > 1) h = cfma(__ldg(&a.chat[N + p]), g1, h);
           for (int s = 2; s < a.S; ++s) h = cfma(__ldg(&a.chat[(long)s * N + p]), __ldg(&srcp[s * sstr]), h);
           x[j] = h;
@@ -271,28 +281,25 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
 #pragma unroll 1
     for (int x = 0; x < 4; ++x) {
       const bool fwd = (x & 1) != 0;
-      if (fwd) {   // conj(Theta^{+-1} y) = Theta^{-+1} conj(y): x = 1 multiplies by theta^{-n}, x = 3 by theta^{+n}
-        conj_all<N1>(v);
-        const double sg = x == 1 ? -1.0 : 1.0;
+      if (fwd) {   // x = 1: conj(y) theta^{-n} = conj(y theta^n); x = 3: conj(y) theta^{+n}
+        if (x == 3) conj_all<N1>(v);
 #pragma unroll
-        for (int t = 0; t < N1; ++t) {
-          const double2 r = sth[i + N1 * t];
-          v[t] = cmul(v[t], make_double2(r.x, sg * r.y));
-        }
+        for (int t = 0; t < N1; ++t) v[t] = crot32(cmul(v[t], thi), t * (32 / N1));   // theta^{i + N1 t}
+        if (x == 1) conj_all<N1>(v);
       }
       dft_n1<N1, +1>(v);
       {
-        const double2* tr = stw + i * G::TWROW;
+        const double2* tr = stw + i * G::TWC - 1;
 #pragma unroll
         for (int k2 = 1; k2 < N1; ++k2) v[k2] = cmul(v[k2], tr[k2]);
       }
       __syncthreads();                       // the buffer is free (previous exchange / tile input read)
 #pragma unroll
-      for (int k2 = 0; k2 < N1; ++k2) buf[k2 * G::ROW + i * G::WB + c] = v[k2];
+      for (int k2 = 0; k2 < N1; ++k2) buf[G::xidx(k2, i * WB + c)] = v[k2];
       __syncthreads();
 #pragma unroll
-      for (int t = 0; t < N1; ++t) v[t] = buf[i * G::ROW + t * G::WB + c];
-      PINT_ASSERT((N1 - 1) * G::ROW + i * G::WB + c < G::BUF && i * G::ROW + (N1 - 1) * G::WB + c < G::BUF);
+      for (int t = 0; t < N1; ++t) v[t] = buf[G::xidx(i, t * WB + c)];
+      PINT_ASSERT(G::xidx(N1 - 1, i * WB + c) < G::BUF && G::xidx(i, (N1 - 1) * WB + c) < G::BUF);
       if (x == 0) {                          // U_{m-1} of this tile lands during the pass-B DFT
         __syncthreads();
         if (tid == 0) {
