@@ -101,20 +101,22 @@ template <int N1, int DIR> __device__ __forceinline__ void dft_n1(double2* a) {
 template <int N1> struct CQCfg {
   static constexpr int N = N1 * N1;
   static constexpr int WB = TILE / N;                       // columns per tile
-  static constexpr int THREADS = N1 * WB;                   // thread (i, c) = (tid / WB, tid % WB)
+  static constexpr int GT = N1 * WB;                        // threads per tile group: (i, c) = (t / WB, t % WB)
+  static constexpr int GROUPS = 2;                          // tile groups per CTA (one CTA per SM)
+  static constexpr int THREADS = GROUPS * GT;
   static constexpr int ROW = N1 * WB;                       // exchange row stride (complex; see xidx)
-  static constexpr int BUF = TILE;                          // tile landing zone = exchange buffer
+  static constexpr int BUF = TILE;                          // per group: tile landing zone = exchange buffer
   static constexpr int TWC = N1 - 1;                        // twiddle row: k2 = 1..N1-1 (odd stride:
                                                             // conflict-free rows without padding)
-  // tile / exchange buffer + pass-A twiddles + d_p + chat_0: 111.5 KB at N1 = 32, two CTAs per SM
-  static constexpr int SMEM = (BUF + N1 * TWC + 2 * N) * 16;
+  static constexpr int SCH = 2;                             // chat_s staged in shared memory, s < SCH
+  // two tile buffers + the tables both groups share (pass-A twiddles, d_p, chat_0, chat_1):
+  // 191.5 KB at N1 = 32 (the tables would not fit twice beside two buffers in two CTAs)
+  static constexpr int SMEM = (GROUPS * BUF + N1 * TWC + (1 + SCH) * N) * 16;
+  static constexpr int TCOLS = 512;                         // all TMEM columns of the SM: per thread N1 complex
+                                                            // of stash (D W + H_static) and N1 of (c_x/N) D'
   // exchange slot of (row r, column j): WB = 4 rows XOR-swizzled by the row parity (the 8 threads of a
   // 16-byte wavefront read rows i, i+1 at the same column: the swizzle puts them on disjoint banks)
   static __device__ __forceinline__ int xidx(int r, int j) { return r * ROW + (WB == 4 ? (j ^ ((r & 1) << 2)) : j); }
-  // two CTAs per SM: 255 registers (no spills of the 32 values per thread), 2 x 256 TMEM columns
-  static constexpr int MINB = 2;
-  static constexpr int TCOLS = 256;                         // TMEM columns per CTA: the stash of D W + H_static
-                                                            // (128) and this thread's (c_x/N) D' values (128)
 };
 
 struct CQArgs {
@@ -184,21 +186,25 @@ template <int N1> __device__ __forceinline__ void conj_all(double2 (&v)[N1]) {
   for (int t = 0; t < N1; ++t) v[t].y = __longlong_as_double(__double_as_longlong(v[t].y) ^ (long long)0x8000000000000000ULL);
 }
 
+// the tile group's barrier (named barrier 1 + g over its GT threads; 0 is __syncthreads)
+template <int GT> __device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "n"(GT) : "memory");
+}
+
 template <int N1>
-__global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_fused_kernel(const CQArgs a) {
+__global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(const CQArgs a) {
   using G = CQCfg<N1>;
   constexpr int N = G::N, WB = G::WB, NW = G::THREADS / 32;
-  extern __shared__ __align__(128) double2 buf[];
-  __shared__ __align__(8) unsigned long long bar, ubar;   // W tile landed / U_{m-1} tile landed
+  extern __shared__ __align__(128) double2 smem_cq[];
+  __shared__ __align__(8) unsigned long long bars[2 * G::GROUPS];   // per group: W tile landed, U_{m-1} landed
   __shared__ uint32_t tbase;
   __shared__ double red[NW];
-  const int tid = threadIdx.x, i = tid / WB, c = tid % WB, warp = tid / 32;
-  const uint32_t sbuf = smem_u32(buf), sbar = smem_u32(&bar), subar = smem_u32(&ubar);
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sbar) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(subar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
+  const int tid = threadIdx.x, warp = tid / 32, g = tid / G::GT, gtid = tid % G::GT;
+  const int i = gtid / WB, c = gtid % WB;
+  double2* buf = smem_cq + g * G::BUF;                        // this group's tile / exchange buffer
+  const uint32_t sbuf = smem_u32(buf), sbar = smem_u32(&bars[2 * g]), subar = smem_u32(&bars[2 * g + 1]);
+  if (tid < 2 * G::GROUPS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[tid])) : "memory");
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                  ::"r"(smem_u32(&tbase)), "n"(G::TCOLS) : "memory");
@@ -207,21 +213,24 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // the pass-A twiddles, d_p and chat_0, staged once per CTA (persistent kernel): conflict-free shared
-  // loads (per-tile L2 loads of d_p and chat_0 stalled the stash on their latency, ncu v9)
-  double2* stw = buf + G::BUF;                 // [N1][N1 - 1]
+  // the pass-A twiddles, d_p, chat_0 and chat_1, staged once per CTA (persistent kernel) and shared by
+  // both groups: conflict-free shared loads (per-tile L2 loads of them stalled the stash, ncu v9/v10)
+  double2* stw = smem_cq + G::GROUPS * G::BUF; // [N1][N1 - 1]
   double2* sdh = stw + N1 * G::TWC;            // [N]
-  double2* sch = sdh + N;                      // [N] chat_0 (S > 0)
+  double2* sch = sdh + N;                      // [SCH][N] chat_s, s < min(S, SCH)
   for (int e = tid; e < N; e += G::THREADS) {
     if (e % N1) stw[(e / N1) * G::TWC + e % N1 - 1] = __ldg(&a.tw[e]);
     sdh[e] = __ldg(&a.dh[e]);
-    if (a.S > 0) sch[e] = __ldg(&a.chat[e]);
+#pragma unroll
+    for (int s = 0; s < G::SCH; ++s)
+      if (s < a.S) sch[s * N + e] = __ldg(&a.chat[(long)s * N + e]);
   }
   const double2 thi = __ldg(&a.th[i]);         // theta^i
   __syncthreads();
-  // this thread's stash columns: lane 32 (warp % 4) + lane, N1 * 4 columns (N1 complex doubles)
-  const uint32_t tst = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * N1 * 4);
-  const uint32_t tdp = tst + 128;      // this thread's (c_x/N) d'_p, p = i + N1 t: fixed for the whole kernel
+  // this thread's columns: lane 32 (warp % 4) + lane; the warps sharing a lane quarter take 2 N1 * 4
+  // columns each: N1 complex of stash, then N1 complex of (c_x/N) d'_p, p = i + N1 t (whole kernel)
+  const uint32_t tst = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 2 * N1 * 4);
+  const uint32_t tdp = tst + N1 * 4;
 #pragma unroll
   for (int q = 0; q < N1 / 4; ++q) {
     double2 x[4];
@@ -231,20 +240,27 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
   }
   const double gi0 = __ldg(&a.igs[i]);
   const long ntiles = a.ntiles;
-  long tile = blockIdx.x;
+  const long tstride = (long)gridDim.x * G::GROUPS;
+  long tile = (long)blockIdx.x * G::GROUPS + g;
   uint32_t phase = 0;
-  if (tid == 0 && tile < ntiles) tile_bulk_load(sbuf, a.in + tile * (long)TILE, TILE * 16, sbar);
+  if (gtid == 0 && tile < ntiles) tile_bulk_load(sbuf, a.in + tile * (long)TILE, TILE * 16, sbar);
   double upd2 = 0.0;                   // max |U_m - U_{m-1}|^2 (one square root at the end)
   bool nonfinite = false;
-  PINT_ASSERT(blockDim.x == G::THREADS && i < N1 && c < WB);
+  PINT_ASSERT(blockDim.x == G::THREADS && i < N1 && c < WB && g < G::GROUPS);
+  static_assert(G::TCOLS >= (G::THREADS / 128) * 2 * N1 * 4, "TMEM columns");
   static_assert(N1 * CQCfg<N1>::ROW <= CQCfg<N1>::BUF && TILE <= CQCfg<N1>::BUF, "exchange buffer");
-  for (; tile < ntiles; tile += gridDim.x) {
-    const long base = tile * (long)TILE, nt = tile + gridDim.x;
-    if (tid < 4) {
-      if (nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + tid * (TILE / 4), TILE / 4 * 16);
-    } else if (tid < 8) {                    // this tile's U_{m-1}: its bulk copy (after u = V W) hits L2
-      prefetch_l2_t(a.ufull + base + (tid - 4) * (TILE / 4), TILE / 4 * 16);
+  for (; tile < ntiles; tile += tstride) {
+    const long base = tile * (long)TILE, nt = tile + tstride;
+    if (gtid < 4) {
+      if (nt < ntiles) prefetch_l2_t(a.in + nt * (long)TILE + gtid * (TILE / 4), TILE / 4 * 16);
+    } else if (gtid < 8) {                   // this tile's U_{m-1}: its bulk copy (after u = V W) hits L2
+      prefetch_l2_t(a.ufull + base + (gtid - 4) * (TILE / 4), TILE / 4 * 16);
     }
+    // the tile's spatial sources (issued before the wait: their latency hides behind it)
+    const double2* srcp = a.src + tile * WB + c;
+    const long sstr = ntiles * WB;
+    const double2 g0 = a.S > 0 ? __ldg(&srcp[0]) : make_double2(0.0, 0.0);
+    const double2 g1 = a.S > 1 ? __ldg(&srcp[sstr]) : make_double2(0.0, 0.0);
     mbar_wait(sbar, phase);
     phase ^= 1;
     double2 v[N1];
@@ -252,10 +268,6 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
     for (int t = 0; t < N1; ++t) v[t] = buf[(i + N1 * t) * WB + c];
     // stash = D W + H_static (frequency p = i + N1 t) -> TMEM, 4 values per tcgen05.st
     {
-      const double2* srcp = a.src + tile * WB + c;
-      const long sstr = ntiles * WB;
-      const double2 g0 = a.S > 0 ? __ldg(&srcp[0]) : make_double2(0.0, 0.0);
-      const double2 g1 = a.S > 1 ? __ldg(&srcp[sstr]) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int q = 0; q < N1 / 4; ++q) {
         double2 x[4];
@@ -264,11 +276,22 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
           const int p = i + N1 * (4 * q + j);
           double2 h = cmul(v[4 * q + j], sdh[p]);
           if (a.S > 0) h = cfma(sch[p], g0, h);
-          if (a.S > 1) h = cfma(__ldg(&a.chat[N + p]), g1, h);
-          for (int s = 2; s < a.S; ++s) h = cfma(__ldg(&a.chat[(long)s * N + p]), __ldg(&srcp[s * sstr]), h);
+          if (a.S > 1) h = cfma(sch[N + p], g1, h);
           x[j] = h;
         }
         tmem_st4c(tst + 16 * q, x);
+      }
+      if (a.S > G::SCH) {                    // further sources (not staged): read-modify-write of the stash
+#pragma unroll 1
+        for (int q = 0; q < N1 / 4; ++q) {
+          double2 x[4];
+          tmem_ld4c(tst + 16 * q, x);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            for (int s = G::SCH; s < a.S; ++s)
+              x[j] = cfma(__ldg(&a.chat[(long)s * N + i + N1 * (4 * q + j)]), __ldg(&srcp[s * sstr]), x[j]);
+          tmem_st4c(tst + 16 * q, x);
+        }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     }
@@ -293,22 +316,22 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, CQCfg<N1>::MINB) tpass_cq_
 #pragma unroll
         for (int k2 = 1; k2 < N1; ++k2) v[k2] = cmul(v[k2], tr[k2]);
       }
-      __syncthreads();                       // the buffer is free (previous exchange / tile input read)
+      group_sync<G::GT>(g);                  // the buffer is free (previous exchange / tile input read)
 #pragma unroll
       for (int k2 = 0; k2 < N1; ++k2) buf[G::xidx(k2, i * WB + c)] = v[k2];
-      __syncthreads();
+      group_sync<G::GT>(g);
 #pragma unroll
       for (int t = 0; t < N1; ++t) v[t] = buf[G::xidx(i, t * WB + c)];
       PINT_ASSERT(G::xidx(N1 - 1, i * WB + c) < G::BUF && G::xidx(i, (N1 - 1) * WB + c) < G::BUF);
       if (x == 0) {                          // U_{m-1} of this tile lands during the pass-B DFT
-        __syncthreads();
-        if (tid == 0) {
+        group_sync<G::GT>(g);
+        if (gtid == 0) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           tile_bulk_load(sbuf, a.ufull + base, TILE * 16, subar);
         }
       } else if (x == 3) {
-        __syncthreads();
-        if (tid == 0 && nt < ntiles) {       // the next tile lands while this one finishes
+        group_sync<G::GT>(g);
+        if (gtid == 0 && nt < ntiles) {      // the next tile lands while this one finishes
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           tile_bulk_load(sbuf, a.in + nt * (long)TILE, TILE * 16, sbar);
         }

@@ -64,11 +64,10 @@ cudaError_t PINT_CAT(launch_tpass_cq_fused_, PINT_N)(const CQArgs& a, cudaStream
   constexpr int N1 = PINT_N == 1024 ? 32 : 16;
   using G = CQCfg<N1>;
   auto kern = tpass_cq_fused_kernel<N1>;
-  // persistent grid of MINB CTAs per SM (the kernel's launch bound; MINB 67 KB exchange buffers and
-  // MINB x 256 TMEM columns per SM) with a shared-memory carve-out of just what they need: the rest of
-  // the 256 KB stays L1 for the pass-A twiddle and eigenvalue tables
+  // persistent grid of one CTA per SM (two tile groups; 191.5 KB of shared memory and all 512 TMEM
+  // columns) with a shared-memory carve-out of just what it needs: the rest stays L1
   static const long resident = [&]() -> long {
-    const int need = G::MINB * (G::SMEM + 1024 + 256);
+    const int need = G::SMEM + 1024 + 256;
     const int pct = (int)((100LL * need + 233471) / 233472);
     if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct) != cudaSuccess)
       return 0;
@@ -76,11 +75,12 @@ cudaError_t PINT_CAT(launch_tpass_cq_fused_, PINT_N)(const CQArgs& a, cudaStream
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return (long)nsm * G::MINB;
+    return (long)nsm;
   }();
   if (resident <= 0) return cudaErrorInvalidValue;
   if (a.ntiles <= 0) return cudaSuccess;
-  const long grid = a.ntiles < resident ? a.ntiles : resident;
+  const long want = (a.ntiles + G::GROUPS - 1) / G::GROUPS;
+  const long grid = want < resident ? want : resident;
   kern<<<(unsigned)grid, G::THREADS, G::SMEM, st>>>(a);
   return cudaGetLastError();
 #else
