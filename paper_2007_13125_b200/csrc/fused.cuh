@@ -941,68 +941,77 @@ __global__ void __launch_bounds__(256, PINT_MODAL_MINB) wr_modal_kernel(const Fu
   }
 }
 
-// Chunk reduction for small problems (many frequency-group chunks per x-mode, e.g. 1D): one warp per
-// (q, y), lanes over the chunks; the sum replaces chunk 0 (P[q][0][j][y]), deterministic order.
-// The finish step for one row (q, y) from its window sums S_j = sum_p e^{2 pi i n_j p/N} W_p
-// (all chunks summed): U_m window, monitor, new wrap state and X for the next iteration
-// (wr_finish_kernel, mode FIN_PARTIALS)
-__device__ __forceinline__ void finish_row(const FinishArgs& a, long q, int y, const double2 (&S)[8], double& updl,
-                                           bool& nonfinite) {
-  const int k = a.k;
-  const bool live = y < a.L;
-  const long wb = (q * a.NB + y / a.WB) * k * a.WB + (y % a.WB);
-  double2 U[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    U[j] = make_double2(0.0, 0.0);
-    if (j < k && live) {
-      U[j] = cscale(S[j], __ldg(&a.igs[a.N - k + j]));
-      const double dd = sqrt(cabs2(csub(U[j], a.wrap_old[wb + j * a.WB])));
-      if (!(dd <= 1.7976931348623157e308)) nonfinite = true;
-      updl = fmax(updl, dd);
-      a.wrap_new[wb + j * a.WB] = U[j];
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    double2 F = make_double2(0.0, 0.0);
-    if (t < a.nk && live) {
-      for (int i = 0; i < a.nsparse; ++i) {
-        const int s = __ldg(&a.spar[i]);
-        F = cfmar(__ldg(&a.src[((long)s * a.Qb + q) * a.Lpad + y]), __ldg(&a.coef[(long)s * a.N + t]), F);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j >= t && j < k) F = cfmar(U[j], __ldg(&a.wk[k + t - j]), F);
-      F = cscale(F, __ldg(&a.gsf[t]));
-    }
-    a.X[(q * 8 + t) * a.Lf + y] = F;
-  }
-}
-
 // many chunks (nch > 16, 1D problems): one warp per row sums the chunks' window sums (lanes over
-// chunks, shuffle tree), then lane 0 runs the finish step — one kernel instead of reduce + finish
+// chunks, a shuffle tree per window level j < k), then the warp runs the finish step of the row with
+// lane j on window level j (U_j, its update, the new wrap state) and lane t on X_t (the U_j reach it
+// by shuffles): every load of the step is issued by some lane at once (lane 0 alone serialised ~8 L2
+// round trips per row: the finish phase of C2 took 12 us of a 30 us iteration)
 __device__ __forceinline__ void reduce_finish_rows(const FinishArgs& a) {
   const int lane = threadIdx.x & 31;
+  const int k = a.k;
   double updl = 0.0;
   bool nonfinite = false;
   for (long gw = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5; gw < a.Qb * (long)a.Lf;
        gw += ((long)gridDim.x * blockDim.x) >> 5) {
     const long q = gw / a.Lf;
     const int y = (int)(gw % a.Lf);
+    const bool live = y < a.L;
+    // ---- window sums S_j (all lanes hold all S_j after the xor trees) ----
     double2 S[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      double2 s = make_double2(0.0, 0.0);
-      if (j < a.k)
-        for (int c = lane; c < a.nch; c += 32) s = cadd(s, a.P[((q * a.pstride + c) * a.k + j) * a.Lf + y]);
-      for (int o = 16; o > 0; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      S[j] = make_double2(0.0, 0.0);
+      if (j < k) {                                           // warp-uniform
+        const double2* Pj = a.P + (q * a.pstride * k + j) * a.Lf + y;
+        const long cs = (long)k * a.Lf;                      // chunk stride
+        double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+        int c = lane;
+        for (; c + 32 < a.nch; c += 64) { s0 = cadd(s0, Pj[c * cs]); s1 = cadd(s1, Pj[(c + 32) * cs]); }
+        if (c < a.nch) s0 = cadd(s0, Pj[c * cs]);
+        double2 sv = cadd(s0, s1);
+        for (int o = 16; o > 0; o >>= 1) {
+          sv.x += __shfl_xor_sync(0xffffffffu, sv.x, o);
+          sv.y += __shfl_xor_sync(0xffffffffu, sv.y, o);
+        }
+        S[j] = sv;
       }
-      S[j] = s;
     }
-    if (lane == 0) finish_row(a, q, y, S, updl, nonfinite);
+    // ---- lane j < k: U_j = kappa^{-n/N} S_j (n = N - k + j), update, new wrap state ----
+    const long wb = (q * a.NB + y / a.WB) * k * a.WB + (y % a.WB);
+    double2 Uj = make_double2(0.0, 0.0);
+    if (lane < k && live) {
+      double2 Sj = S[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (lane == j) Sj = S[j];
+      Uj = cscale(Sj, __ldg(&a.igs[a.N - k + lane]));
+      const double dd = sqrt(cabs2(csub(Uj, a.wrap_old[wb + lane * a.WB])));
+      if (!(dd <= 1.7976931348623157e308)) nonfinite = true;
+      updl = fmax(updl, dd);
+      a.wrap_new[wb + lane * a.WB] = Uj;
+    }
+    double2 U[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      U[j].x = __shfl_sync(0xffffffffu, Uj.x, j);
+      U[j].y = __shfl_sync(0xffffffffu, Uj.y, j);
+    }
+    // ---- lane t < 8: X_t = Gamma_t h^2/N [ F_static(t) + (kappa/tau) sum_jw omega_jw U^{N+t-jw} ] ----
+    if (lane < 8) {
+      const int t = lane;
+      double2 F = make_double2(0.0, 0.0);
+      if (t < a.nk && live) {
+        for (int i = 0; i < a.nsparse; ++i) {
+          const int sidx = __ldg(&a.spar[i]);
+          F = cfmar(__ldg(&a.src[((long)sidx * a.Qb + q) * a.Lpad + y]), __ldg(&a.coef[(long)sidx * a.N + t]), F);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)                          // window entry j = level N-k+j, jw = k+t-j
+          if (j >= t && j < k) F = cfmar(U[j], __ldg(&a.wk[k + t - j]), F);
+        F = cscale(F, __ldg(&a.gsf[t]));
+      }
+      a.X[(q * 8 + t) * a.Lf + y] = F;
+    }
   }
   if (nonfinite) updl = __longlong_as_double(0x7ff0000000000000LL);
   block_max_atomic(updl, a.upd);
@@ -1083,12 +1092,29 @@ __global__ void __launch_bounds__(FG * 32, 1) wr_loop_kernel(const LoopKArgs L) 
   extern __shared__ double2 fsm[];
   __shared__ uint32_t tbase_s;
   const uint32_t tbase = fused_tmem_alloc<C, 32, NKC>(&tbase_s);
+#ifdef PINT_FUSED_PROF
+#define PINT_GT(v) unsigned long long v; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#else
+#define PINT_GT(v)
+#endif
   for (int h = 0;; h ^= 1) {
+    PINT_GT(g0);
     fused_iteration<C, 32, false, true, false, NKC>(L.fa[h], fsm, tbase);
+    PINT_GT(g1);
     grid_sync(L.bar, nullptr, nullptr);
+    PINT_GT(g2);
     if (L.fin[h].nch > 16) reduce_finish_rows(L.fin[h]);
     else finish_rows(L.fin[h], FIN_PARTIALS);
+    PINT_GT(g3);
     grid_sync(L.bar, L.ctl, L.fin[h].upd);
+    PINT_GT(g4);
+#ifdef PINT_FUSED_PROF
+    if (threadIdx.x == 0 && L.fa[h].prof) {   // ns per phase, summed over blocks and iterations
+      unsigned long long* pr = L.fa[h].prof + 40;
+      atomicAdd(&pr[0], g1 - g0); atomicAdd(&pr[1], g2 - g1); atomicAdd(&pr[2], g3 - g2);
+      atomicAdd(&pr[3], g4 - g3); atomicAdd(&pr[4], 1ull);
+    }
+#endif
     if (*(volatile int*)&L.ctl->done) break;
   }
   fused_tmem_free<C, 32, NKC>(tbase);

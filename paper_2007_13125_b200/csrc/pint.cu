@@ -302,8 +302,11 @@ static void free_plan(pint_plan p) {
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
   if (p->prof) {   // profiling builds: print the phase cycle split of the fused kernel
-    unsigned long long h[36];
+    unsigned long long h[48];
     cudaMemcpy(h, p->prof, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h[44])
+      fprintf(stderr, "[pint prof] loop kernel ns per block-iteration: fused %.0f sync1 %.0f finish %.0f sync2 %.0f\n",
+              (double)h[40] / h[44], (double)h[41] / h[44], (double)h[42] / h[44], (double)h[43] / h[44]);
     const double tot = (double)(h[0] + h[1] + h[2] + h[3]) + 1e-30;
     fprintf(stderr, "[pint prof] fused phases (warp-cycles share): solve %.3f wait1 %.3f rows %.3f wait2 %.3f\n",
             h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot);
