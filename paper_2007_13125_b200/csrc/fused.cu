@@ -107,7 +107,8 @@ cudaError_t launch_modal(bool store_w, const FusedArgs& a, cudaStream_t st) {
 
 cudaError_t launch_finish(const FinishArgs& a0, int mode, cudaStream_t st) {
   FinishArgs a = a0;
-  if (mode == FIN_PARTIALS && a.nch > 16) {   // many chunks: warp per row, reduce + finish
+  // many chunks, or several chunks of a small problem: warp per row (lanes over the chunks)
+  if (mode == FIN_PARTIALS && (a.nch > 16 || (a.nch >= 2 && a.Qb * (long)a.Lf <= 4096))) {
     const long blocks = (a.Qb * (long)a.Lf * 32 + TPB - 1) / TPB;
     wr_reduce_finish_kernel<<<(unsigned)blocks, TPB, 0, st>>>(a);
     return cudaGetLastError();

@@ -613,9 +613,17 @@ __device__ __forceinline__ bool loop_ctl_eval(LoopCtl* s, double u) {
   if (stop) s->done = 1;
   return stop != 0;
 }
+// the rule on a register copy of the state: one batch of loads and one of stores (field by field on
+// global memory it was ~10 dependent L2 round trips inside the grid barrier's critical section)
+__device__ __forceinline__ bool loop_ctl_apply(LoopCtl* s, double u) {
+  LoopCtl c = *s;
+  const bool stop = loop_ctl_eval(&c, u);
+  *s = c;
+  return stop;
+}
 // ... and clears the while-node condition of the device-loop graph
 __device__ __forceinline__ void loop_ctl_step(LoopCtl* s, double u, cudaGraphConditionalHandle h) {
-  if (loop_ctl_eval(s, u)) cudaGraphSetConditional(h, 0);
+  if (loop_ctl_apply(s, u)) cudaGraphSetConditional(h, 0);
 }
 
 #ifndef PINT_BAR_SLEEP
@@ -644,7 +652,7 @@ __device__ __forceinline__ void grid_sync(GridBar* b, LoopCtl* ctl, unsigned lon
       if (ctl) {
         const double u = __longlong_as_double((long long)*(volatile unsigned long long*)upd);
         *upd = 0ull;
-        loop_ctl_eval(ctl, u);
+        loop_ctl_apply(ctl, u);
       }
       b->count = 0u;
       __threadfence();
@@ -1103,8 +1111,12 @@ __global__ void __launch_bounds__(FG * 32, 1) wr_loop_kernel(const LoopKArgs L) 
     PINT_GT(g1);
     grid_sync(L.bar, nullptr, nullptr);
     PINT_GT(g2);
-    if (L.fin[h].nch > 16) reduce_finish_rows(L.fin[h]);
-    else finish_rows(L.fin[h], FIN_PARTIALS);
+    // warp per row when the chunks are many or every row gets its own warp (thread per row left the
+    // C1 finish to block 0 alone: 8 sequential partial loads per level while 7 blocks waited)
+    if (L.fin[h].nch > 16 || L.fin[h].Qb * (long)L.fin[h].Lf <= (long)gridDim.x * (blockDim.x / 32))
+      reduce_finish_rows(L.fin[h]);
+    else
+      finish_rows(L.fin[h], FIN_PARTIALS);
     PINT_GT(g3);
     grid_sync(L.bar, L.ctl, L.fin[h].upd);
     PINT_GT(g4);
