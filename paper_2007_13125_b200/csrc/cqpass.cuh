@@ -106,12 +106,11 @@ template <int N1> struct CQCfg {
   static constexpr int THREADS = GROUPS * GT;
   static constexpr int ROW = N1 * WB;                       // exchange row stride (complex; see xidx)
   static constexpr int BUF = TILE;                          // per group: tile landing zone = exchange buffer
-  static constexpr int TWC = N1 - 1;                        // twiddle row: k2 = 1..N1-1 (odd stride:
-                                                            // conflict-free rows without padding)
+  static constexpr int TWROW = N1 + 1;                      // twiddle row stride (padded: conflict-free)
   static constexpr int SCH = 2;                             // chat_s staged in shared memory, s < SCH
-  // two tile buffers + the tables both groups share (pass-A twiddles, d_p, chat_0, chat_1):
-  // 191.5 KB at N1 = 32 (the tables would not fit twice beside two buffers in two CTAs)
-  static constexpr int SMEM = (GROUPS * BUF + N1 * TWC + (1 + SCH) * N) * 16;
+  // two tile buffers + the tables both groups share (three pass-A twiddle tables: w^{i k2} and
+  // w^{i k2} theta^{-+i} for the two Theta transforms; d_p, chat_0, chat_1): 225.5 KB at N1 = 32
+  static constexpr int SMEM = (GROUPS * BUF + 3 * N1 * TWROW + (1 + SCH) * N) * 16;
   static constexpr int TCOLS = 512;                         // all TMEM columns of the SM: per thread N1 complex
                                                             // of stash (D W + H_static) and N1 of (c_x/N) D'
   // exchange slot of (row r, column j): WB = 4 rows XOR-swizzled by the row parity (the 8 threads of a
@@ -215,17 +214,22 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   // the pass-A twiddles, d_p, chat_0 and chat_1, staged once per CTA (persistent kernel) and shared by
   // both groups: conflict-free shared loads (per-tile L2 loads of them stalled the stash, ncu v9/v10)
-  double2* stw = smem_cq + G::GROUPS * G::BUF; // [N1][N1 - 1]
-  double2* sdh = stw + N1 * G::TWC;            // [N]
+  double2* stw = smem_cq + G::GROUPS * G::BUF; // [N1][TWROW] w^{i k2}
+  double2* stm = stw + N1 * G::TWROW;          // [N1][TWROW] w^{i k2} theta^{-i}  (x = 1)
+  double2* stp = stm + N1 * G::TWROW;          // [N1][TWROW] w^{i k2} theta^{+i}  (x = 3)
+  double2* sdh = stp + N1 * G::TWROW;          // [N]
   double2* sch = sdh + N;                      // [SCH][N] chat_s, s < min(S, SCH)
   for (int e = tid; e < N; e += G::THREADS) {
-    if (e % N1) stw[(e / N1) * G::TWC + e % N1 - 1] = __ldg(&a.tw[e]);
+    const int r = e / N1, k2 = e % N1;
+    const double2 w = __ldg(&a.tw[e]), th = __ldg(&a.th[r]);
+    stw[r * G::TWROW + k2] = w;
+    stm[r * G::TWROW + k2] = cmul(w, make_double2(th.x, -th.y));
+    stp[r * G::TWROW + k2] = cmul(w, th);
     sdh[e] = __ldg(&a.dh[e]);
 #pragma unroll
     for (int s = 0; s < G::SCH; ++s)
       if (s < a.S) sch[s * N + e] = __ldg(&a.chat[(long)s * N + e]);
   }
-  const double2 thi = __ldg(&a.th[i]);         // theta^i
   __syncthreads();
   // this thread's columns: lane 32 (warp % 4) + lane; the warps sharing a lane quarter take 2 N1 * 4
   // columns each: N1 complex of stash, then N1 complex of (c_x/N) d'_p, p = i + N1 t (whole kernel)
@@ -304,15 +308,19 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
 #pragma unroll 1
     for (int x = 0; x < 4; ++x) {
       const bool fwd = (x & 1) != 0;
-      if (fwd) {   // x = 1: conj(y) theta^{-n} = conj(y theta^n); x = 3: conj(y) theta^{+n}
+      // x = 1: conj(y) theta^{-n} = conj(y theta^{N1 t}) theta^{-i}; x = 3: conj(y) theta^{N1 t} theta^{+i}
+      // (theta^n = theta^i theta^{N1 t}): the rotation theta^{N1 t} = e^{i pi t / N1} is a compile-time
+      // constant per register, and theta^{-+i}, constant over the pass-A DFT (over t), rides on its twiddles
+      if (fwd) {
         if (x == 3) conj_all<N1>(v);
 #pragma unroll
-        for (int t = 0; t < N1; ++t) v[t] = crot32(cmul(v[t], thi), t * (32 / N1));   // theta^{i + N1 t}
+        for (int t = 1; t < N1; ++t) v[t] = crot32(v[t], t * (32 / N1));
         if (x == 1) conj_all<N1>(v);
       }
       dft_n1<N1, +1>(v);
       {
-        const double2* tr = stw + i * G::TWC - 1;
+        const double2* tr = (x == 1 ? stm : (x == 3 ? stp : stw)) + i * G::TWROW;
+        if (fwd) v[0] = cmul(v[0], tr[0]);
 #pragma unroll
         for (int k2 = 1; k2 < N1; ++k2) v[k2] = cmul(v[k2], tr[k2]);
       }
