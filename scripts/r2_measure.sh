@@ -15,6 +15,7 @@ timeout 600 python bench.py --real --no-cpu > $o/C4_real.json 2>> $o/err.log
 timeout 600 python bench.py --modal --real --no-cpu > $o/C4_modal_real.json 2>> $o/err.log
 timeout 600 python bench.py --config C5 --modal --no-cpu > $o/C5_modal.json 2>> $o/err.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $o/ref.json 2>> $o/err.log
+timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu > $o/C4_gpus2.json 2> $o/gpus2.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches_C4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $o/ncu_launch_C4.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches_C5.csv python bench.py --config C5 --steps 2 --warmup 3 --no-e2e --no-cpu > $o/ncu_launch_C5.log 2>&1
 timeout 900 ncu --set full --import-source on -k regex:wr_modal_kernel -c 1 -o $o/prof_modal python bench.py --modal --mx 127 --steps 1 --warmup 3 --no-e2e --no-cpu > $o/ncu_modal.log 2>&1
