@@ -78,6 +78,10 @@ CASES = [
     (7, 100, 512, 3, 0.1, 0.7, 1),
     (255, 17, 1024, 1, 0.1, 0.5, 0),
     (127, 1024, 16, 2, 0.3, 1.0, 1),     # longest line, shortest N
+    # one-kernel CQ T-pass (N = 256: 16 x 16, N = 1024: 32 x 32) with S = R + 1 = 4 sources: two
+    # staged in shared memory, the others added to the TMEM stash; ragged tile tails
+    (63, 5, 256, 2, 0.05, 0.4, 3),
+    (40, 3, 1024, 3, 0.1, 0.6, 3),
 ]
 
 
