@@ -113,7 +113,7 @@ constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 // LANES lanes per line: 32 (one warp; default) or 64 (two warps, pair-scoped named barriers);
 // threads per CTA = 8 LANES; LF = LANES C rows per line; NS interleaved sub-chains per lane chunk.
 #ifndef PINT_FUSED_NS
-#define PINT_FUSED_NS 4
+#define PINT_FUSED_NS 2   // A/B r2 (C4 10.17 -> 10.07 ms, C3 0.418 -> 0.402 ms; 8: 10.63 ms)
 #endif
 #ifndef PINT_TM_BATCH
 #define PINT_TM_BATCH 4   // rows per TMEM load batch in the window phase

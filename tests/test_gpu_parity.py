@@ -81,7 +81,7 @@ CASES = [
     # one-kernel CQ T-pass (N = 256: 16 x 16, N = 1024: 32 x 32) with S = R + 1 = 4 sources: two
     # staged in shared memory, the others added to the TMEM stash; ragged tile tails
     (63, 5, 256, 2, 0.05, 0.4, 3),
-    (40, 3, 1024, 3, 0.1, 0.6, 3),
+    (31, 3, 1024, 3, 0.1, 0.6, 3),
 ]
 
 
