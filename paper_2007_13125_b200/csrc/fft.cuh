@@ -79,6 +79,39 @@ template <int DIR> __device__ __forceinline__ void dft8(double2* a) {
   a[2] = cadd(e2, o2); a[6] = csub(e2, o2);
   a[3] = cadd(e3, o3); a[7] = csub(e3, o3);
 }
+// dft8 with a[t] = 0 for t >= NIN (compile time): the additions of known zeros are skipped (the
+// compiler may not drop x + 0.0 itself: it is not an identity for x = -0.0)
+template <int DIR, int NIN> __device__ __forceinline__ void dft4z(double2& a0, double2& a1, double2& a2, double2& a3) {
+  // inputs (a0, a1, a2, a3) are time indices (i, i+2, i+4, i+6) of the dft8 below: NIN counts those < NIN
+  if constexpr (NIN >= 4) {
+    dft4<DIR>(a0, a1, a2, a3);
+  } else if constexpr (NIN == 3) {                      // a3 = 0
+    const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t3 = mul_i<DIR>(a1);
+    a0 = cadd(t0, a1); a2 = csub(t0, a1); a1 = cadd(t1, t3); a3 = csub(t1, t3);
+  } else if constexpr (NIN == 2) {                      // a2 = a3 = 0
+    const double2 t3 = mul_i<DIR>(a1);
+    a2 = csub(a0, a1); const double2 b0 = cadd(a0, a1); a1 = cadd(a0, t3); a3 = csub(a0, t3); a0 = b0;
+  } else {                                              // a1 = a2 = a3 = 0
+    a1 = a0; a2 = a0; a3 = a0;
+  }
+}
+template <int DIR, int NIN> __device__ __forceinline__ void dft8z(double2* a) {
+  if constexpr (NIN >= 8) {
+    dft8<DIR>(a);
+  } else {
+    double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+    double2 o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
+    dft4z<DIR, (NIN + 1) / 2>(e0, e1, e2, e3);         // even times 0, 2, 4, 6
+    dft4z<DIR, NIN / 2>(o0, o1, o2, o3);               // odd times 1, 3, 5, 7
+    o1 = cmul_w<DIR>(o1, R2H, R2H);
+    o2 = mul_i<DIR>(o2);
+    o3 = cmul_w<DIR>(o3, -R2H, R2H);
+    a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
+    a[1] = cadd(e1, o1); a[5] = csub(e1, o1);
+    a[2] = cadd(e2, o2); a[6] = csub(e2, o2);
+    a[3] = cadd(e3, o3); a[7] = csub(e3, o3);
+  }
+}
 template <int DIR> __device__ __forceinline__ void dft16(double2* a) {
   // index t = t1 + 4 t2; inner DFT4 over t2, twiddle w16^{t1 s1}, outer DFT4 over t1.
 #pragma unroll

@@ -36,7 +36,8 @@ struct LineConst {
   double2 uc[8];    // u-forms of a^{C 2^i}
   double2 ap[5];    // a^{2^i} (value form), i < 5: per-lane powers of the boundary fix-up
   double tl;        // log(1e-18 |1 - a^{2L+2}|) / log|a|: |a^e / (1 - a^{2L+2})| > 1e-18 iff e < tl
-  double pad0;
+  int nlev;         // lane-scan levels i < nlev have |a^{C 2^i}| >= 2^-64 (the others add nothing: skipped)
+  int pad1;
 };                  // 320 bytes
 constexpr int LC_CHUNKS = 20;   // 16-byte cp.async chunks per LineConst
 static_assert(sizeof(LineConst) == 16 * LC_CHUNKS, "LineConst is staged in 16-byte chunks");
@@ -108,6 +109,25 @@ template <bool AF> __device__ __forceinline__ double2 mmul(double2 c, double2 z)
 }
 template <bool AF> __device__ __forceinline__ double2 mconv(double2 uform) { return AF ? one_minus(uform) : uform; }
 template <bool AF> __device__ __forceinline__ double2 vstep(double2 c, double2 z, double2 f) { return mmul<AF>(c, cadd(f, z)); }
+// value form: the forward carry sweep stores g_y = a f_y, so that the backward sweeps are v_y = g_y + a v_{y+1}
+// (one complex FMA, two dependent DFMAs per step instead of an add and a multiply: three); u-form: g = f
+#ifndef PINT_GFORM
+#define PINT_GFORM 1
+#endif
+#ifndef PINT_SCAN_SKIP
+#define PINT_SCAN_SKIP 1
+#endif
+#ifndef PINT_FAST_TAIL
+#define PINT_FAST_TAIL 1
+#endif
+template <bool AF> __device__ __forceinline__ double2 gform(double2 c, double2 f) {
+  if constexpr (AF && PINT_GFORM) return cmul(c, f);
+  else return f;
+}
+template <bool AF> __device__ __forceinline__ double2 bstep(double2 c, double2 z, double2 g) {
+  if constexpr (AF && PINT_GFORM) return cfma(c, z, g);
+  else return vstep<false>(c, z, g);
+}
 constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
 
 // LANES lanes per line: 32 (one warp; default) or 64 (two warps, pair-scoped named barriers);
@@ -137,8 +157,14 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 // as NS interleaved sub-chains of CS rows (independent dependency chains).
 template <int C, int LANES, bool STORE_W, bool AF>
 __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, const LineConst& lc, double2* xch,
-                                            long q, long p, int half, int bar) {
+                                            long q, long p, int half, int bar, unsigned long long* sp = nullptr) {
   constexpr bool PAIR = LANES == 64;
+#ifdef PINT_SOLVE_PROF
+  long long tp_ = clock64();
+#define PINT_SP(j) do { const long long t_ = clock64(); if (sp) sp[j] += t_ - tp_; tp_ = t_; } while (0)
+#else
+#define PINT_SP(j) do { } while (0)
+#endif
   constexpr int NS = fused_ns<C, LANES>();
   constexpr int CS = C / NS;
   const int lane = threadIdx.x & 31;
@@ -154,8 +180,12 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   double2 d[C];
   // pad rows y >= L of Hl hold exact zeros (X and the sources vanish there): no load masking
   const SwzRows<C> rows(Hl, gl);
+  // loads in the order the forward sweep consumes them (row r of every sub-chain, then r + 1): the sweep
+  // starts as soon as its first rows land instead of after the whole chunk (all warps load at once)
 #pragma unroll
-  for (int r = 0; r < C; ++r) d[r] = rows[r];
+  for (int r = 0; r < CS; ++r)
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) d[s2 * CS + r] = rows[s2 * CS + r];
 
   // ---- forward recurrence f_y = d_y + a f_{y-1} ----
   double2 fs[NS];
@@ -165,6 +195,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   for (int r = 0; r < CS; ++r)
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) fs[s2] = mstep<AF>(u, fs[s2], d[s2 * CS + r]);
+  PINT_SP(0);
   double2 f = fs[0];
 #pragma unroll
   for (int s2 = 1; s2 < NS; ++s2) f = mstep<AF>(uh, f, fs[s2]);          // chunk total (zero carry)
@@ -172,8 +203,10 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     pair_sync(bar);
     if (lane == 0) f = mstep<AF>(uc[0], xch[0], f);
   }
+  const int nlev = (PAIR || !PINT_SCAN_SKIP) ? 5 : lc.nlev;               // warp-uniform
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
+    if (i >= nlev) break;
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_up_sync(0xffffffffu, f.x, o);
@@ -188,6 +221,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   carry.x = __shfl_up_sync(0xffffffffu, f.x, 1);
   carry.y = __shfl_up_sync(0xffffffffu, f.y, 1);
   if (lane == 0) carry = (PAIR && half) ? xch[0] : make_double2(0.0, 0.0);
+  PINT_SP(1);
   double2 st[NS];
   st[0] = carry;
 #pragma unroll
@@ -197,8 +231,9 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) {
       st[s2] = mstep<AF>(u, st[s2], d[s2 * CS + r]);
-      d[s2 * CS + r] = st[s2];
+      d[s2 * CS + r] = gform<AF>(u, st[s2]);
     }
+  PINT_SP(2);
   // the lane holding row L-1: the backward sweep starts from zero at row L.  L = LF - 1 (the
   // 2^n - 1 grids) has one pad row: a warp-uniform branch avoids C predicated selects per lane.
   if (L >= LANES * C - 1) {
@@ -215,7 +250,8 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 #pragma unroll
   for (int r = CS - 1; r >= 0; --r)
 #pragma unroll
-    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = vstep<AF>(u, fs[s2], d[s2 * CS + r]);
+    for (int s2 = 0; s2 < NS; ++s2) fs[s2] = bstep<AF>(u, fs[s2], d[s2 * CS + r]);
+  PINT_SP(3);
   double2 w = fs[NS - 1];
 #pragma unroll
   for (int s2 = NS - 2; s2 >= 0; --s2) w = mstep<AF>(uh, w, fs[s2]);
@@ -225,6 +261,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   }
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
+    if (i >= nlev) break;
     const int o = 1 << i;
     double2 x;
     x.x = __shfl_down_sync(0xffffffffu, w.x, o);
@@ -241,14 +278,49 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   st[NS - 1] = carry;
 #pragma unroll
   for (int s2 = NS - 2; s2 >= 0; --s2) st[s2] = mstep<AF>(uh, st[s2 + 1], fs[s2 + 1]);
+  PINT_SP(4);
+  if constexpr (!STORE_W && !PAIR) {
+    // Large-shift lines (the P correction reaches < 256 rows, the Q correction none): the rows are
+    // stored as the carry sweep produces them, and the warp fixes rows y < rP up afterwards, one row
+    // per lane.  v_0 is lane 0's inclusive backward total (the scan above), known before the sweep.
+    if (PINT_FAST_TAIL && lc.tl <= 258.0 && (double)L + 3.0 >= lc.tl) {   // warp-uniform
+      double2 w0;
+      w0.x = __shfl_sync(0xffffffffu, w.x, 0);
+      w0.y = __shfl_sync(0xffffffffu, w.y, 0);
+      double2 al = lc.ap[1];                                               // a^{lane + 2}
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+        if ((lane >> i) & 1) al = cmul(al, lc.ap[i]);
+#pragma unroll
+      for (int r = CS - 1; r >= 0; --r)
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          st[s2] = bstep<AF>(u, st[s2], d[s2 * CS + r]);
+          rows[s2 * CS + r] = st[s2];
+        }
+      PINT_SP(5);
+      const int rP = min((int)ceil(lc.tl - 2.0), L);
+      double2 Ka = cmul(cmul(w0, lc.ru2L), al);                            // K a^{y+2}, y = lane
+      const double2 a32 = cmul(lc.ap[4], lc.ap[4]);
+      __syncwarp();
+      for (int yy = lane; yy < rP; yy += 32) {
+        double2& xr = Hl[swz<C>(yy)];
+        xr = csub(xr, Ka);
+        Ka = cmul(Ka, a32);
+      }
+      PINT_SP(8);
+      return;
+    }
+  }
 #pragma unroll
   for (int r = CS - 1; r >= 0; --r)
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) {
-      st[s2] = vstep<AF>(u, st[s2], d[s2 * CS + r]);
+      st[s2] = bstep<AF>(u, st[s2], d[s2 * CS + r]);
       d[s2 * CS + r] = st[s2];
     }
 
+  PINT_SP(5);
   // ---- rank-1 Dirichlet correction x = v - v_0 phi (v = a w), phi_y = (a^{y+2} - a^{2L+2-y}) / (1 - a^{2L+2}) ----
   double2 w0;
   if constexpr (PAIR) {
@@ -299,6 +371,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
         for (int s2 = 0; s2 < NS; ++s2) { d[s2 * CS + r] = cadd(d[s2 * CS + r], KQ[s2]); KQ[s2] = cmul(KQ[s2], rr); }
     }
   }
+  PINT_SP(6);
   if constexpr (STORE_W) {
     double2* Wq = a.W + (q * a.NB * a.N + p) * a.WB;
 #pragma unroll
@@ -309,6 +382,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   } else {
 #pragma unroll
     for (int r = 0; r < C; ++r) rows[r] = d[r];   // pad rows: never read (finish uses y < L)
+    PINT_SP(7);
     if (fastP) {
       // x_y -= K a^{y+2} for y < rP, K = v_0 / (1 - a^{2L+2}) (value-form powers: |a| < 0.85 here)
       __syncwarp();
@@ -326,6 +400,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
         Ka = cmul(Ka, a32);
       }
     }
+    PINT_SP(8);
   }
 }
 
@@ -518,7 +593,7 @@ __device__ __forceinline__ void fused_rows(const FusedArgs& a, double2* Hs, doub
       double2* z = xv[rr];
 #pragma unroll
       for (int t = 1; t < NKC; ++t) z[t] = cmul(z[t], tws[t]);                   // X_t w_N^{t (i+1)}
-      dft8<-1>(z);                                       // H_{i+1 + (N/8) s} = sum_t (.) e^{-2 pi i ts/8}
+      dft8z<-1, NKC>(z);                                 // H_{i+1 + (N/8) s} = sum_t (.) e^{-2 pi i ts/8}
       for (int dd = 0; dd < a.ndense; ++dd) {
         const double2 g = y < a.L ? __ldg(&a.src[((long)__ldg(&a.dsrc[dd]) * a.Qb + q) * a.Lpad + y])
                                   : make_double2(0.0, 0.0);
@@ -757,6 +832,7 @@ __device__ __forceinline__ void fused_iteration(const FusedArgs& a, double2* fsm
   fused_rows<C, LANES, false, false, false, NKC>(a, Hs, acc, Xq, q, g0 - 1, true);   // synthesise group g0
   cp_async_wait0();
   __syncthreads();
+  unsigned long long sp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};   // PINT_SOLVE_PROF: cycles per solve sub-phase
 #ifdef PINT_FUSED_PROF
   unsigned long long pt[4] = {0, 0, 0, 0};
 #define PINT_TS(v) long long v = clock64()
@@ -768,9 +844,9 @@ __device__ __forceinline__ void fused_iteration(const FusedArgs& a, double2* fsm
     {
       const LineConst& lcl = slc[line];
       if (cabs2(lcl.u) >= FUSED_AF_U2)
-        fused_solve<C, LANES, STORE_W, true>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
+        fused_solve<C, LANES, STORE_W, true>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line, sp);
       else
-        fused_solve<C, LANES, STORE_W, false>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line);
+        fused_solve<C, LANES, STORE_W, false>(a, Hs + line * LF, lcl, xch + 4 * line, q, i + (long)NG * line, half, 1 + line, sp);
     }
     PINT_TS(t1);
     __syncthreads();
@@ -794,8 +870,13 @@ __device__ __forceinline__ void fused_iteration(const FusedArgs& a, double2* fsm
       atomicAdd(&a.prof[j], pt[j]);
       atomicAdd(&a.prof[4 + 4 * w + j], pt[j]);
     }
+#ifdef PINT_SOLVE_PROF
+    for (int j = 0; j < 9; ++j) atomicAdd(&a.prof[48 + j], sp[j]);
+    atomicAdd(&a.prof[57], (unsigned long long)(g1 - g0));
+#endif
   }
 #endif
+  (void)sp;
   if (!STORE_W) {
     double2* P = a.P + ((q * a.nch + ch) * a.k) * LF;
     if constexpr (TMA) {
@@ -1162,7 +1243,9 @@ __global__ void line_const_kernel(LineConst* lc, const double2* sig_p, const dou
     const double la = 0.5 * log(cabs2(one_minus(c.u)));                // log|a| < 0
     const double thr = -41.44653167389282 + 0.5 * log(cabs2(u2L));      // log(1e-18 |1 - a^{2L+2}|)
     c.tl = la < 0.0 ? thr / la : INFINITY;
-    c.pad0 = 0.0;
+    c.nlev = 0;
+    while (c.nlev < 5 && cabs2(one_minus(c.uc[c.nlev])) >= 0x1p-128) ++c.nlev;
+    c.pad1 = 0;
     lc[e] = c;
   }
 }

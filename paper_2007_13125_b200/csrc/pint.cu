@@ -302,7 +302,7 @@ static void free_plan(pint_plan p) {
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
   if (p->prof) {   // profiling builds: print the phase cycle split of the fused kernel
-    unsigned long long h[48];
+    unsigned long long h[64];
     cudaMemcpy(h, p->prof, sizeof(h), cudaMemcpyDeviceToHost);
     if (h[44])
       fprintf(stderr, "[pint prof] loop kernel ns per block-iteration: fused %.0f sync1 %.0f finish %.0f sync2 %.0f\n",
@@ -310,6 +310,13 @@ static void free_plan(pint_plan p) {
     const double tot = (double)(h[0] + h[1] + h[2] + h[3]) + 1e-30;
     fprintf(stderr, "[pint prof] fused phases (warp-cycles share): solve %.3f wait1 %.3f rows %.3f wait2 %.3f\n",
             h[0] / tot, h[1] / tot, h[2] / tot, h[3] / tot);
+    if (h[48 + 8]) {
+      unsigned long long g[9];
+      cudaMemcpy(g, p->prof + 48, sizeof(g), cudaMemcpyDeviceToHost);
+      double t = 0; for (int j = 0; j < 9; ++j) t += (double)g[j];
+      fprintf(stderr, "[pint prof] solve sub-phases (share): fwd0 %.3f scan1 %.3f fwd1 %.3f bwd0 %.3f scan2 %.3f bwd1 %.3f corr %.3f store %.3f fastP %.3f; cycles per warp-solve %.0f\n",
+              g[0] / t, g[1] / t, g[2] / t, g[3] / t, g[4] / t, g[5] / t, g[6] / t, g[7] / t, g[8] / t, t / (double)h[57]);
+    }
     for (int w = 0; w < 8; ++w)
       fprintf(stderr, "[pint prof] warp %d: solve %.3e wait1 %.3e rows %.3e wait2 %.3e\n", w, (double)h[4 + 4 * w],
               (double)h[5 + 4 * w], (double)h[6 + 4 * w], (double)h[7 + 4 * w]);
