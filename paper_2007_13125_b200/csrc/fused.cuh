@@ -111,21 +111,12 @@ template <bool AF> __device__ __forceinline__ double2 mconv(double2 uform) { ret
 template <bool AF> __device__ __forceinline__ double2 vstep(double2 c, double2 z, double2 f) { return mmul<AF>(c, cadd(f, z)); }
 // value form: the forward carry sweep stores g_y = a f_y, so that the backward sweeps are v_y = g_y + a v_{y+1}
 // (one complex FMA, two dependent DFMAs per step instead of an add and a multiply: three); u-form: g = f
-#ifndef PINT_GFORM
-#define PINT_GFORM 1
-#endif
-#ifndef PINT_SCAN_SKIP
-#define PINT_SCAN_SKIP 1
-#endif
-#ifndef PINT_FAST_TAIL
-#define PINT_FAST_TAIL 1
-#endif
 template <bool AF> __device__ __forceinline__ double2 gform(double2 c, double2 f) {
-  if constexpr (AF && PINT_GFORM) return cmul(c, f);
+  if constexpr (AF) return cmul(c, f);
   else return f;
 }
 template <bool AF> __device__ __forceinline__ double2 bstep(double2 c, double2 z, double2 g) {
-  if constexpr (AF && PINT_GFORM) return cfma(c, z, g);
+  if constexpr (AF) return cfma(c, z, g);
   else return vstep<false>(c, z, g);
 }
 constexpr double FUSED_AF_U2 = 1e-6;   // |u|^2 threshold of the value form
@@ -180,8 +171,8 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   double2 d[C];
   // pad rows y >= L of Hl hold exact zeros (X and the sources vanish there): no load masking
   const SwzRows<C> rows(Hl, gl);
-  // loads in the order the forward sweep consumes them (row r of every sub-chain, then r + 1): the sweep
-  // starts as soon as its first rows land instead of after the whole chunk (all warps load at once)
+  // loads in the order the forward sweep consumes them (row r of every sub-chain, then r + 1; neutral in
+  // an A/B on C4 and C3, kept: the sweep may start before the whole chunk has landed)
 #pragma unroll
   for (int r = 0; r < CS; ++r)
 #pragma unroll
@@ -203,7 +194,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     pair_sync(bar);
     if (lane == 0) f = mstep<AF>(uc[0], xch[0], f);
   }
-  const int nlev = (PAIR || !PINT_SCAN_SKIP) ? 5 : lc.nlev;               // warp-uniform
+  const int nlev = PAIR ? 5 : lc.nlev;                                     // warp-uniform
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
     if (i >= nlev) break;
@@ -283,7 +274,7 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
     // Large-shift lines (the P correction reaches < 256 rows, the Q correction none): the rows are
     // stored as the carry sweep produces them, and the warp fixes rows y < rP up afterwards, one row
     // per lane.  v_0 is lane 0's inclusive backward total (the scan above), known before the sweep.
-    if (PINT_FAST_TAIL && lc.tl <= 258.0 && (double)L + 3.0 >= lc.tl) {   // warp-uniform
+    if (lc.tl <= 258.0 && (double)L + 3.0 >= lc.tl) {                     // warp-uniform
       double2 w0;
       w0.x = __shfl_sync(0xffffffffu, w.x, 0);
       w0.y = __shfl_sync(0xffffffffu, w.y, 0);
