@@ -180,10 +180,11 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
 
   // ---- forward recurrence f_y = d_y + a f_{y-1} ----
   double2 fs[NS];
+  // zero carry: the first step of each sub-chain is its first row (no multiplication of the zero state)
 #pragma unroll
-  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = make_double2(0.0, 0.0);
+  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = d[s2 * CS];
 #pragma unroll
-  for (int r = 0; r < CS; ++r)
+  for (int r = 1; r < CS; ++r)
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) fs[s2] = mstep<AF>(u, fs[s2], d[s2 * CS + r]);
   PINT_SP(0);
@@ -236,10 +237,11 @@ __device__ __forceinline__ void fused_solve(const FusedArgs& a, double2* Hl, con
   }
 
   // ---- backward recurrence w_y = f_y + a w_{y+1}, carried as v = a w: v_y = a (f_y + v_{y+1}) ----
+  // (value form: v_y = g_y + a v_{y+1}, so the zero-carry start is the last row's g itself)
 #pragma unroll
-  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = make_double2(0.0, 0.0);
+  for (int s2 = 0; s2 < NS; ++s2) fs[s2] = AF ? d[s2 * CS + CS - 1] : make_double2(0.0, 0.0);
 #pragma unroll
-  for (int r = CS - 1; r >= 0; --r)
+  for (int r = AF ? CS - 2 : CS - 1; r >= 0; --r)
 #pragma unroll
     for (int s2 = 0; s2 < NS; ++s2) fs[s2] = bstep<AF>(u, fs[s2], d[s2 * CS + r]);
   PINT_SP(3);
