@@ -234,6 +234,11 @@ static pint_status dalloc(pint_plan p, T** ptr, size_t count) {
   p->allocs.push_back(q);
   p->dev_bytes += (int64_t)bytes;
   *ptr = (T*)q;
+  // zero-filled: pad slots (rows y >= L of the window / monitor buffers, tile tails) are never written by
+  // the kernels but some are read (the fully modal plans' physical-window monitor took differences over
+  // them: an uninitialised allocation left a constant, run-dependent update floor, e.g. 2.7e-10)
+  e = cudaMemsetAsync(q, 0, bytes, p->stream);
+  if (e != cudaSuccess) return fail(PINT_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   return PINT_OK;
 }
 #define TRY(x)                        \

@@ -603,11 +603,33 @@ def test_fem_and_modal_1d(pint, name, make, iters):
             win = p.get_levels(N - k, k)          # window levels before materialisation
             errs.append(float(np.linalg.norm(win - o[m][N - k:]) / np.linalg.norm(o[m])))
             errs.append(rel(p.get_solution(), o[m]))
-        it, u, st = p.solve(1e-12, 40)
+        it, u, st = p.solve(1e-12, 40, raise_on_fail=False)
+        if st != 0:   # diagnostics: the update history of plain iterations from here
+            hist = [p.iterate() for _ in range(6)]
+            print(name, "solve status", st, "iterations", it, "last update", u, "then", hist)
         seq_err = rel(p.get_solution(), sequential.sequential(prob))
     print(name, errs, it, seq_err)
     assert max(errs) <= TOL, errs
     assert st == 0 and seq_err <= 1e-9, (st, seq_err)
+
+
+def test_plan_buffers_zero_filled_after_dirty_memory(pint):
+    """Device memory left dirty by earlier allocations must not reach the iteration: the fully modal
+    plans' physical-window monitor once read never-written pad slots of its window buffers, which gave a
+    constant, run-dependent update floor (2.7e-10 on fem_63_bdf2 after other tests) and a solve that
+    never reached 1e-12.  Plan allocations are zero-filled since."""
+    import torch
+    # large-pool and small-pool (2 MB segment) allocations, filled, then handed back to the driver
+    junk = [torch.full((1 << 24,), 1e3 * (i + 1), dtype=torch.float64, device="cuda:0") for i in range(8)]
+    junk += [torch.full((1 << 15,), 7e2 + i, dtype=torch.float64, device="cuda:0") for i in range(512)]
+    torch.cuda.synchronize()
+    del junk
+    torch.cuda.empty_cache()                      # give the dirty segments back to the driver
+    prob = inputs.random_complex_problem(63, 1, 64, 2, 0.1, 1.0, R=2, seed=12).with_(space="fem")
+    with pint.Plan.from_problem(prob) as p:
+        it, u, st = p.solve(1e-12, 40, raise_on_fail=False)
+        assert st == 0 and it <= 8, (st, it, u)
+        assert p.iterate() < 1e-14
 
 
 def test_fem_rejects_unsupported(pint):
