@@ -367,8 +367,8 @@ def main():
         peak = 2 * FP64_FMA_PER_CLK_SM * torch.cuda.get_device_properties(dev).multi_processor_count * smx * 1e6 / 1e12
         flops_launch = fl * local_unknowns
         achieved = flops_launch / (s_avg / 1e3) / 1e12
-        if os.path.exists(tf):
-            traffic = json.load(open(tf)).get(f"{args.config}:fused")
+        if os.path.exists(tf) and not args.real:   # per variant: the line path's or the modal kernel's capture
+            traffic = json.load(open(tf)).get(f"{args.config}:{'modal' if args.modal else 'fused'}")
         roofline = {"bound": "alu", "kernel": "wr_modal_kernel" if args.modal else "wr_fused_kernel",
                     "achieved": achieved, "peak": peak,
                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
