@@ -98,6 +98,9 @@ template <int N1, int DIR> __device__ __forceinline__ void dft_n1(double2* a) {
   else dft16<DIR>(a);
 }
 
+#ifndef PINT_CQ_STAGGER
+#define PINT_CQ_STAGGER 1   // A/B: C5 T-pass 4.19 -> 4.16 ms (scripts/r2_gpu_ab_stag.sh)
+#endif
 template <int N1> struct CQCfg {
   static constexpr int N = N1 * N1;
   static constexpr int WB = TILE / N;                       // columns per tile
@@ -253,6 +256,13 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
   PINT_ASSERT(blockDim.x == G::THREADS && i < N1 && c < WB && g < G::GROUPS);
   static_assert(G::TCOLS >= (G::THREADS / 128) * 2 * N1 * 4, "TMEM columns");
   static_assert(N1 * CQCfg<N1>::ROW <= CQCfg<N1>::BUF && TILE <= CQCfg<N1>::BUF, "exchange buffer");
+#if PINT_CQ_STAGGER
+  // the two tile groups run half a tile apart: group 1 starts when group 0 has finished the second
+  // transform of its first tile (one named-barrier hand-off), so that one group's shared-memory phases
+  // (tile loads, exchanges) meet the other's FP64 phases instead of their own copies
+  bool stag = g == 0;                  // group 0: arrive once
+  if (g == 1) asm volatile("bar.sync 3, %0;\n" ::"n"(G::THREADS) : "memory");
+#endif
   for (; tile < ntiles; tile += tstride) {
     const long base = tile * (long)TILE, nt = tile + tstride;
     if (gtid < 4) {
@@ -365,6 +375,12 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
           }
         }
       } else if (x == 1) {
+#if PINT_CQ_STAGGER
+        if (stag) {
+          asm volatile("bar.arrive 3, %0;\n" ::"n"(G::THREADS) : "memory");
+          stag = false;
+        }
+#endif
 #pragma unroll
         for (int q = 0; q < N1 / 4; ++q) {   // (c_x/N) D' from tensor memory
           double2 dq[4];
@@ -387,6 +403,9 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
       }
     }
   }
+#if PINT_CQ_STAGGER
+  if (stag) asm volatile("bar.arrive 3, %0;\n" ::"n"(G::THREADS) : "memory");   // group 0 had no tile
+#endif
   // ---- update monitor: block max, one atomic per CTA; TMEM release ----
   double upd = sqrt(upd2);
   if (nonfinite) upd = __longlong_as_double(0x7ff0000000000000LL);
