@@ -99,7 +99,7 @@ template <int N1, int DIR> __device__ __forceinline__ void dft_n1(double2* a) {
 }
 
 #ifndef PINT_CQ_STAGGER
-#define PINT_CQ_STAGGER 1   // A/B: C5 T-pass 4.19 -> 4.16 ms (scripts/r2_gpu_ab_stag.sh)
+#define PINT_CQ_STAGGER 1   // A/B: C5 T-pass 4.19 -> 4.16-4.18 ms (r2_gpu_ab_stag*.sh; after transform 0: 4.34, worse)
 #endif
 template <int N1> struct CQCfg {
   static constexpr int N = N1 * N1;
@@ -356,6 +356,12 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
       }
       dft_n1<N1, +1>(v);
       if (fwd) conj_all<N1>(v);
+#if PINT_CQ_STAGGER
+      if (stag && x == 1) {                 // after the second transform of the first tile
+        asm volatile("bar.arrive 3, %0;\n" ::"n"(G::THREADS) : "memory");
+        stag = false;
+      }
+#endif
       if (x == 0) {
         double gi;   // kappa^{-i/N}, through an opaque move per tile: its 32 products with gt[t] would
         asm volatile("mov.b64 %0, %1;" : "=d"(gi) : "d"(gi0));   // otherwise be hoisted and kept live
@@ -375,12 +381,6 @@ __global__ void __launch_bounds__(CQCfg<N1>::THREADS, 1) tpass_cq_fused_kernel(c
           }
         }
       } else if (x == 1) {
-#if PINT_CQ_STAGGER
-        if (stag) {
-          asm volatile("bar.arrive 3, %0;\n" ::"n"(G::THREADS) : "memory");
-          stag = false;
-        }
-#endif
 #pragma unroll
         for (int q = 0; q < N1 / 4; ++q) {   // (c_x/N) D' from tensor memory
           double2 dq[4];
