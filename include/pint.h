@@ -130,7 +130,9 @@ typedef struct {
   void* allreduce_ctx;
 } pint_options;
 
-/* Create a plan for N time steps of size tau with BDF order k and relaxation parameter kappa.
+/* Create a plan for N time steps of size tau with BDF order k and relaxation parameter kappa
+ * (the kappa-wrapped scheme eqn:BDF-iter; CQ: eqn:CQ-iter).
+ * Builds the Step-1..3 tables of Algorithm 1 / 2: Gamma, d_p, twiddles.
  * M must equal op->mx * op->my.  Errors (PINT_ERR_ARG): k not in 1..6; kappa not in (0,1);
  * tau <= 0; N < k+1; alpha not in (0,1]; M != mx*my; mx, my < 1; rank/nranks invalid or
  * nranks > mx; nranks > 1 with a 1D operator.  PINT_ERR_UNSUPPORTED: N not a power of two in
@@ -166,7 +168,8 @@ pint_status pint_set_problem_separable(pint_plan plan, const void* v, int32_t R,
 pint_status pint_set_problem(pint_plan plan, const void* v, const void* f, const void* f0, const void* fderiv,
                              int32_t mem);
 
-/* Replace the WR initial guess by a full space-time array U0 [N][M] (this is U_0^1..U_0^N;
+/* Replace the WR initial guess by a full space-time array U0 [N][M] (this is U_0^1..U_0^N, the
+ * m = 0 iterate of eqn:BDF-iter; the paper starts from U_0^n = v, PAPER.md:173;
  * requires a prior pint_set_problem_separable).  Resets m to 0. */
 pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
 
@@ -178,7 +181,8 @@ pint_status pint_set_initial_guess(pint_plan plan, const void* U0, int32_t mem);
  * re-captured when the problem changes; PINT_NO_GRAPH=1 in the environment: eager launches). */
 pint_status pint_wr_iterate(pint_plan plan, double* update_inf);
 
-/* Iterate until update < tol, or max_iters iterations (PINT_ERR_NOT_CONVERGED), or the update
+/* Iterate until update < tol (the paper's stopping rule), or max_iters
+ * iterations (PINT_ERR_NOT_CONVERGED), or the update
  * grows 3 consecutive times / is not finite (PINT_ERR_DIVERGED).  *iters, *update_inf may be NULL.
  * Fused heat path on one rank: the whole loop runs on the device (a CUDA graph with a while-conditional
  * node; the stopping rule is evaluated by a kernel after every iteration) — one host synchronisation
@@ -186,25 +190,29 @@ pint_status pint_wr_iterate(pint_plan plan, double* update_inf);
 pint_status pint_wr_solve(pint_plan plan, double tol, int32_t max_iters, int32_t* iters,
                           double* update_inf);
 
-/* Run exactly `iters` >= 1 WR iterations (no stopping rule, no divergence guard) with one host
+/* Run exactly `iters` >= 1 WR iterations (Algorithm 1 / 2 Steps 1-3 each, PAPER.md:468-477,
+ * 1053-1061; no stopping rule, no divergence guard) with one host
  * synchronisation at the end; *update_inf (may be NULL) receives the last iteration's update (max over
  * ranks: one all-reduce per call).  The throughput call of bench.py. */
 pint_status pint_wr_run(pint_plan plan, int32_t iters, double* update_inf);
 
-/* Copy the current iterate U_m, time levels n_begin+1 .. n_begin+n_count (0-based row
+/* Copy the current iterate U_m (Step 3's output; the fused heat path materialises
+ * it here from the window state), time levels n_begin+1 .. n_begin+n_count (0-based row
  * n_begin .. n_begin+n_count-1 of the [N][M] array), into U [n_count][M] complex in mem.
  * 2D with nranks > 1: returns PINT_ERR_UNSUPPORTED (use the modal-slab calls below). */
 pint_status pint_get_levels(pint_plan plan, int64_t n_begin, int64_t n_count, void* U, int32_t mem);
 /* = pint_get_levels(plan, 0, N, U, mem) */
 pint_status pint_get_solution(pint_plan plan, void* U, int32_t mem);
 
-/* Multi-GPU output path: this rank's slab of U_m in the DST-x basis, layout
+/* Multi-GPU output path (the p-processor split of PAPER.md:493-508, here over x-modes, which needs
+ * no exchange once DST-x is hoisted): this rank's slab of U_m in the DST-x basis, layout
  * [n_count][my][q_end-q_begin] (mode q global index q_begin+j), and the inverse DST-I that
  * maps a gathered full modal array [n_count][my][mx] to physical [n_count][my][mx]. */
 pint_status pint_get_modal_levels(pint_plan plan, int64_t n_begin, int64_t n_count, void* Uq, int32_t mem);
 pint_status pint_modal_to_physical(pint_plan plan, int64_t n_count, const void* Uq_full, void* U, int32_t mem);
 
-/* Host-only (no CUDA call): the contiguous, balanced x-mode slab of `rank` among `nranks`
+/* Host-only (no CUDA call; partition of the Step-2 systems over p ranks): the
+ * contiguous, balanced x-mode slab of `rank` among `nranks`
  * for mx modes: [floor(rank*mx/nranks), floor((rank+1)*mx/nranks)).  PINT_ERR_ARG if
  * nranks < 1, rank outside [0, nranks) or nranks > mx. */
 pint_status pint_partition(int64_t mx, int32_t rank, int32_t nranks, int64_t* q_begin, int64_t* q_end);
