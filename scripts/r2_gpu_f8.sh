@@ -1,5 +1,5 @@
 # verification on the restored container (session 4): full GPU suite, C4 / C5 / C3 bench lines, smoke
-T=f7
+T=f8
 python -c "
 import os; from paper_2007_13125_b200 import build as b
 assert os.path.getmtime(b.LIB) >= b._newest_dep(), 'stale libpint.so'" || exit 3
