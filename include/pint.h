@@ -240,13 +240,15 @@ pint_status pint_get_timing(pint_plan plan, double* tpass_ms, double* spass_ms,
  * are general tridiagonal systems: shift-accurate Thomas); always the streaming path. */
 enum { PINT_NL_ALLEN_CAHN = 1 };
 
-/* Make the plan semilinear with nonlinearity `kind` and width eps > 0.  The forcing f and v are
+/* Make the plan semilinear with nonlinearity `kind` (g of eqn:BDF-CQ-m-r, PAPER.md:1660-1668;
+ * Allen-Cahn) and width eps > 0.  The forcing f and v are
  * still given by pint_set_problem_separable (before or after this call); the Newton state is reset
  * to U_0 = v by either call.  Errors: ARG (kind, eps), UNSUPPORTED (2D or nranks > 1).
  * Afterwards pint_wr_iterate / pint_wr_solve return STATE and pint_get_levels returns U_l. */
 pint_status pint_set_nonlinearity(pint_plan plan, int32_t kind, double eps);
 
-/* Run up to max_outer Newton steps from the current U_l (inner WR: at most max_inner iterations,
+/* Algorithm 3: run up to max_outer Newton steps from the current U_l (inner WR:
+ * at most max_inner iterations, PAPER.md:1747-1748;
  * stop when the full-array max-norm update < inner_tol).  inner_counts[l] / outer_updates[l]
  * (arrays of max_outer entries, may be NULL) receive the inner iteration count and
  * max |U_l - U_{l-1}| of each step; *outer_done the number of steps run.  Returns OK when the

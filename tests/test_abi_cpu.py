@@ -25,6 +25,22 @@ def test_exports_every_declared_symbol():
     assert sorted(P.EXPORTED) == decl
 
 
+def test_compute_declarations_cite_the_paper():
+    """Every entry point that performs a step of the method cites the passage (PAPER.md line /
+    SURVEY section) that defines it, in the comment block directly above its declaration."""
+    src = open(os.path.join(ROOT, "include", "pint.h")).read()
+    plumbing = {"pint_plan_destroy", "pint_status_string", "pint_last_error", "pint_get_info", "pint_get_path",
+                "pint_set_timing", "pint_get_timing", "pint_get_partition", "pint_get_solution",
+                "pint_modal_to_physical"}   # accessors / aliases documented with the call they belong to
+    for m in re.finditer(r"^(?:pint_status|double|const char\*) (pint_[a-z_0-9]+)\(", src, re.M):
+        name = m.group(1)
+        if name in plumbing:
+            continue
+        start = src.rfind("/*", 0, m.start())
+        block = src[start:m.start()]
+        assert block.count("*/") == 1 and re.search(r"PAPER\.md:\d+|P:\d+|SURVEY §", block), name
+
+
 def test_status_strings_and_kappa_rule():
     L = P.lib()
     assert L.pint_status_string(0) == b"PINT_OK"
