@@ -248,8 +248,8 @@ enum { PINT_NL_ALLEN_CAHN = 1 };
 pint_status pint_set_nonlinearity(pint_plan plan, int32_t kind, double eps);
 
 /* Algorithm 3: run up to max_outer Newton steps from the current U_l (inner WR:
- * at most max_inner iterations, PAPER.md:1747-1748;
- * stop when the full-array max-norm update < inner_tol).  inner_counts[l] / outer_updates[l]
+ * at most max_inner iterations, stop when the full-array max-norm update < inner_tol, the rule of
+ * PAPER.md:1747-1748).  inner_counts[l] / outer_updates[l]
  * (arrays of max_outer entries, may be NULL) receive the inner iteration count and
  * max |U_l - U_{l-1}| of each step; *outer_done the number of steps run.  Returns OK when the
  * Newton update fell below outer_tol (or outer_tol == 0 and max_outer steps ran),
