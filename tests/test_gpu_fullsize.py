@@ -154,8 +154,8 @@ def test_c4_full_array_every_level(pint):
 def test_c4_window_levels_nondecaying(pint):
     """C4 grid, N, k, kappa with a time-constant forcing g in the 32 x 32 sine span (phi = 1): the
     solution tends to A^{-1} g instead of decaying, so the window levels n = N-k+1..N that the fused
-    kernel produces directly are O(1).  Per-level relative error <= 1e-10 on the window, and the
-    full array <= 1e-10, m = 1..3 (O4 stays exact: v and g in the span)."""
+    kernel produces directly are O(1).  Per-level relative error <= 1e-10 on the window for m = 1..3, and the
+    full array <= 1e-10 at m = 3 (O4 stays exact: v and g in the span)."""
     base = inputs.config_c4()
     basis = modal.ModalBasis(1023, 1023, np.arange(1, 33), np.arange(1, 33))
     C = inputs.c4_mode_coefficients()
@@ -168,15 +168,21 @@ def test_c4_window_levels_nondecaying(pint):
         for m in range(1, 4):
             p.iterate()
             # the window read path first (wrap state, before any materialisation)
-            w = p.get_levels(prob.N - prob.k, prob.k)
-            ref = basis.to_grid(md[m][-prob.k:])
+            w = p.get_levels(prob.N - prob.k, prob.k).reshape(prob.k, -1)
+            ref = basis.to_grid(md[m][-prob.k:]).reshape(prob.k, -1)
             assert rel(w, ref) <= TOL
+            win = np.array([rel(w[j], ref[j]) for j in range(prob.k)])
+            print(f"C4 forced m={m}: window levels rel = " + " ".join(f"{e:.2e}" for e in win))
+            assert win.max() <= TOL, (m, win)
+            if m < 3:
+                continue
+            # every level of the last iterate (the decaying recipe's test above streams all three; here the
+            # per-iterate coverage is the window, which determines the next iterate: PAPER.md:388)
             err, per, norms = _c4_stream_compare(p, basis, md[m], prob.N)
-            win = per[-prob.k:]
-            print(f"C4 forced m={m}: full-array rel L2 = {err:.3e}; window levels rel = "
-                  + " ".join(f"{e:.2e}" for e in win) + f" (|U^N| / |U^1| = {norms[-1] / norms[0]:.2f})")
+            print(f"C4 forced m={m}: full-array rel L2 = {err:.3e}; window levels (materialised) rel = "
+                  + " ".join(f"{e:.2e}" for e in per[-prob.k:]) + f" (|U^N| / |U^1| = {norms[-1] / norms[0]:.2f})")
             assert norms[-1] > 0.1 * norms[0]
-            assert err <= TOL and win.max() <= TOL, (m, err, win)
+            assert err <= TOL and per[-prob.k:].max() <= TOL, (m, err, per[-prob.k:])
 
 
 @pytest.mark.slow
